@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""Kascade B200 benchmark (BASELINE.json metric: decode-attn us/token &
+prefill-attn ms at 128K ctx; speedup vs dense on B200).
+
+Default workload (N=1): Llama-3.1-8B attention shapes -- 32 layers, 32 Q /
+8 KV heads, d=128, bf16 -- one decode step at 128K context for a batch of 8
+sequences per GPU, Top-k 10% (k_min 128), anchors [0,2,8,13,14]
+(PAPER.md:396), head maps non-identity.  A "step" = all 32 layers of one
+decode step for the batch; value = Kascade decode-attn us/token (lower is
+better).  The same engine in dense (Top-k = 100%) mode is timed beside it
+on the same buffers; the speedup is dense / Kascade.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Under torchrun each rank owns its own batch of 8 sequences (batch
+sharding, weak scaling, no data-path collective); the time is the max over
+ranks.  --impl reference times the CPU oracle (the reference algorithm,
+oracle/kascade_oracle.py) on the host cores.
+"""
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+LLAMA_ANCHORS = [0, 2, 8, 13, 14]
+CFG = dict(model="Llama-3.1-8B attention", layers=32, Hq=32, Hkv=8, d=128)
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="kascade", choices=["kascade", "reference"])
+    ap.add_argument("--ctx", type=int, default=131072)
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--fraction", type=float, default=0.1)
+    ap.add_argument("--k-min", type=int, default=128)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--extra", action="store_true", help="also time configs[1] (32K, k=2.5%)")
+    return ap.parse_args()
+
+
+def head_maps_for(L, Hkv, anchors, seed=1234):
+    """Deterministic non-identity head maps (a fixed permutation per reuse
+    layer), standing in for offline calibration so the bench exercises the
+    cross-head gather."""
+    rng = np.random.default_rng(seed)
+    maps = {}
+    for l in range(L):
+        if l in anchors:
+            continue
+        maps[l] = rng.permutation(Hkv).tolist()
+    return maps
+
+
+def make_plan(L, Hkv, anchors, fraction, k_min):
+    from paper_2512_16391_b200.host_types import AnchorPlan, AnchorPlanCore, HeadMap, KBudgetPolicy
+    maps = head_maps_for(L, Hkv, anchors)
+    hm = {l: HeadMap(l, max(a for a in anchors if a <= l), m) for l, m in maps.items()}
+    return AnchorPlan(AnchorPlanCore(anchors, len(anchors), 0.0), head_maps=hm,
+                      k_policy=KBudgetPolicy(fraction, k_min))
+
+
+def load_peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------------- CPU oracle
+def cpu_decode_sample(ctx, fraction, k_min, threads_note=True):
+    """Time the CPU oracle (restating the reference's decode path) on ONE
+    sequence: one layer of each kind (anchor0, reuse, anchor) at the bench
+    context, composed to a 32-layer step.  Returns seconds per token."""
+    from oracle import kascade_oracle as orc
+    rng = np.random.default_rng(0)
+    L, Hq, Hkv = 3, CFG["Hq"], CFG["Hkv"]
+    q = orc.bf16_round(rng.standard_normal((L, Hq, 128)).astype(np.float32) * 2.0)
+    K = orc.bf16_round(rng.standard_normal((L, Hkv, ctx, 128)).astype(np.float32))
+    V = orc.bf16_round(rng.standard_normal((L, Hkv, ctx, 128)).astype(np.float32))
+    t = {}
+    orc.decode_step(q, K, V, [0, 2], {1: list(range(Hkv))[::-1]}, fraction, k_min, want_mass=False, timings=t)
+    n_anchor = len(LLAMA_ANCHORS) - 1
+    n_reuse = CFG["layers"] - len(LLAMA_ANCHORS)
+    step = t[0] + n_anchor * t[2] + n_reuse * t[1]
+    # dense baseline per layer: dense rows of every head (no selection)
+    t0 = time.perf_counter()
+    for h in range(Hq):
+        orc.dense_row(q[0, h], K[0, h // (Hq // Hkv)], V[0, h // (Hq // Hkv)])
+    t_dense = time.perf_counter() - t0
+    return step, {"anchor0_ms": t[0] * 1e3, "reuse_ms": t[1] * 1e3, "anchor_ms": t[2] * 1e3,
+                  "dense_ms": t_dense * 1e3, "dense_step_s": t_dense * CFG["layers"]}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    cores = os.cpu_count()
+    for _ in range(args.warmup):
+        cpu_decode_sample(args.ctx, args.fraction, args.k_min)
+    per = []
+    detail = None
+    for _ in range(args.steps):
+        s, detail = cpu_decode_sample(args.ctx, args.fraction, args.k_min)
+        per.append(s)
+    us_tok = float(np.mean(per)) * 1e6
+    line = {
+        "metric": "decode-attn us/token @128K ctx (Kascade, Llama-3.1-8B shapes, k=10%)",
+        "value": round(us_tok, 1), "unit": "us/token", "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(us_tok / 1e3, 3),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic N(0,1) bf16-representable",
+        "config": {"workload": f"llama8b-decode-{args.ctx // 1024}k-b1-k{args.fraction:g} (CPU sample)",
+                   "ctx": args.ctx, "batch": 1, "anchors": LLAMA_ANCHORS},
+        "cpu_baseline": {"value": round(us_tok, 1), "unit": "us/token", "cores": cores, "kind": "port",
+                         "sample": "one sequence; one anchor0, one reuse and one anchor layer timed, "
+                                   "composed to 32 layers (1 anchor0 + 4 anchor + 27 reuse); numpy oracle "
+                                   "restating the reference (BLAS threads = all host cores)",
+                         "per_layer": {k: round(v, 2) for k, v in detail.items()}},
+        "e2e": {"value": round(us_tok, 1), "unit": "us/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2512_16391_b200 import engine, ops
+    from paper_2512_16391_b200._lib import load as load_lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    load_lib()
+    L, Hq, Hkv, B, n = CFG["layers"], CFG["Hq"], CFG["Hkv"], args.batch, args.ctx
+    plan = make_plan(L, Hkv, LLAMA_ANCHORS, args.fraction, args.k_min)
+    k = min(max(math.floor(args.fraction * n), args.k_min), n)
+
+    # ---- KV caches: distinct per layer when they fit, else a pool of layers
+    per_layer = 2 * B * Hkv * n * 128 * 2
+    free, total = torch.cuda.mem_get_info(dev)
+    budget = free - 12 * 2**30
+    n_distinct = max(2, min(L, budget // per_layer))
+    gen = torch.Generator(device=dev)
+    Kc, Vc = [], []
+    for i in range(n_distinct):
+        gen.manual_seed(1000 * (rank + 1) + i)
+        Kc.append(torch.randn(B, Hkv, n, 128, device=dev, dtype=torch.bfloat16, generator=gen))
+        Vc.append(torch.randn(B, Hkv, n, 128, device=dev, dtype=torch.bfloat16, generator=gen))
+    Ks = [Kc[l % n_distinct] for l in range(L)]
+    Vs = [Vc[l % n_distinct] for l in range(L)]
+    gen.manual_seed(7 + rank)
+    q = (torch.randn(L, B, Hq, 128, device=dev, generator=gen) * 2.0).to(torch.bfloat16)
+
+    dec = engine.KascadeDecoder(plan, L, B, Hq, Hkv, n, device=dev)
+    g_kas = dec.capture(q, Ks, Vs, n)
+    out_kas = dec.out.clone()
+    g_den = dec.capture(q, Ks, Vs, n, dense=True)
+
+    def timed(graph, steps):
+        for _ in range(args.warmup):
+            graph.replay()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(steps):
+            graph.replay()
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / steps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms_kas = timed(g_kas, args.steps)
+    clk = clocks.stop()
+    ms_den = timed(g_den, args.steps)
+
+    # ---- dominant kernel: reuse-layer sparse decode, per-launch CUDA events
+    reuse_layers = [l for l in range(L) if l not in LLAMA_ANCHORS]
+    dec.step(q, Ks, Vs, n)  # fresh index lists from the last anchor
+    evs = []
+    torch.cuda.synchronize()
+    for rep in range(max(1, args.steps // 2)):
+        for l in reuse_layers:
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            ops.sparse_decode(q[l], Ks[l], Vs[l], n, dec.indices, dec.counts, dec.head_maps[l], out=dec.out[l])
+            e.record()
+            evs.append((s, e))
+    torch.cuda.synchronize()
+    reuse_ms = float(np.mean([s.elapsed_time(e) for s, e in evs]))
+    counts = dec.counts.cpu().numpy()
+    reuse_bytes = int(counts.sum()) * (2 * 128 * 2 + 4)   # K+V rows + index per selected key
+    peaks, peaks_kind = load_peaks()
+    hbm = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+    achieved = reuse_bytes / (reuse_ms * 1e-3) / 1e9
+
+    # dense kernel (baseline) per-launch duration for context
+    evs = []
+    for l in range(min(L, 8)):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        ops.dense_decode(q[l], Ks[l], Vs[l], n, out=dec.out[l], lse=dec.lse)
+        e.record()
+        evs.append((s, e))
+    torch.cuda.synchronize()
+    dense_ms_launch = float(np.mean([s.elapsed_time(e) for s, e in evs]))
+    dense_bytes = B * Hkv * n * 512
+
+    # ---- end to end through the public API with host buffers ------------
+    e2e = None
+    if not args.no_e2e:
+        q_host = torch.empty(L, B, Hq, 128, dtype=torch.bfloat16).pin_memory()
+        q_host.copy_(q.cpu())
+        kv_host = torch.randn(L, 2, B, Hkv, 128).to(torch.bfloat16).pin_memory()
+        out_host = torch.empty(L, B, Hq, 128, dtype=torch.float32).pin_memory()
+        kv_dev = torch.empty(L, 2, B, Hkv, 128, dtype=torch.bfloat16, device=dev)
+
+        def e2e_step():
+            q.copy_(q_host, non_blocking=True)
+            kv_dev.copy_(kv_host, non_blocking=True)
+            for l in range(L):   # append the step's token at position n-1
+                Ks[l][:, :, n - 1].copy_(kv_dev[l, 0])
+                Vs[l][:, :, n - 1].copy_(kv_dev[l, 1])
+            g_kas.replay()
+            out_host.copy_(dec.out, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        for _ in range(args.warmup):
+            e2e_step()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        ms_e2e = (time.perf_counter() - t0) * 1e3 / args.steps
+        if world > 1:
+            t = torch.tensor([ms_e2e], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+        e2e = {"value": round(ms_e2e * 1e3 / (B * world), 2), "unit": "us/token",
+               "h2d_bytes_per_step": q_host.numel() * 2 + kv_host.numel() * 2,
+               "d2h_bytes_per_step": out_host.numel() * 4,
+               "note": "KascadeDecoder graph replay + pinned H2D of the step's q and new K/V rows (appended "
+                       "to the caches) + D2H of all 32 layers' outputs, host-synchronised every step"}
+
+    # ---- secondary config: configs[1] 32K, k = 2.5 % -----------------------
+    extra = None
+    if args.extra and n >= 32768:
+        n2 = 32768
+        plan2 = make_plan(L, Hkv, LLAMA_ANCHORS, 0.025, args.k_min)
+        K2 = [x[:, :, :n2] for x in Ks]
+        V2 = [x[:, :, :n2] for x in Vs]
+        dec2 = engine.KascadeDecoder(plan2, L, B, Hq, Hkv, n2, device=dev)
+        ga = dec2.capture(q, K2, V2, n2)
+        gd = dec2.capture(q, K2, V2, n2, dense=True)
+        m_a, m_d = timed(ga, args.steps), timed(gd, args.steps)
+        extra = {"workload": "configs[1] llama8b-decode-32k-b8-k2.5%", "kascade_us_per_token":
+                 round(m_a * 1e3 / (B * world), 2), "dense_us_per_token": round(m_d * 1e3 / (B * world), 2),
+                 "speedup_vs_dense": round(m_d / m_a, 3)}
+        del dec2, ga, gd
+
+    # ---- CPU baseline (rank 0 only at N=1) -------------------------------
+    cpu = None
+    if not args.no_cpu_baseline and world == 1 and rank == 0:
+        ctx_cpu = n
+        step_s, detail = cpu_decode_sample(ctx_cpu, args.fraction, args.k_min)
+        cpu = {"value": round(step_s * 1e6, 1), "unit": "us/token", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"one sequence at {ctx_cpu} ctx: one anchor0, one reuse, one anchor layer timed, "
+                         "composed to 32 layers; numpy oracle with all host BLAS threads",
+               "per_layer_ms": {k_: round(v, 2) for k_, v in detail.items()}}
+
+    us_tok = ms_kas * 1e3 / (B * world)
+    launches_per_step = 3 + 4 * (len(LLAMA_ANCHORS) - 1) + (L - len(LLAMA_ANCHORS))
+    line = {
+        "metric": "decode-attn us/token @128K ctx (Kascade, Llama-3.1-8B shapes, k=10%)",
+        "value": round(us_tok, 2), "unit": "us/token", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_kas, 4), "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic N(0,1) bf16 Q/K/V (random-init), per-rank seeds",
+        "config": {"workload": f"llama8b-decode-{n // 1024}k-b{B}-k{args.fraction:g}", "model": CFG["model"],
+                   "layers": L, "q_heads": Hq, "kv_heads": Hkv, "head_dim": 128, "ctx": n, "batch_per_gpu": B,
+                   "global_batch": B * world, "k": k, "anchors": LLAMA_ANCHORS, "head_maps": "non-identity",
+                   "parallelism": f"batch-sharded x{world}", "kv_layers_distinct": n_distinct,
+                   "l2": "inputs > L2 (each layer's KV is %.1f GB)" % (per_layer / 1e9),
+                   "cuda_graph": True},
+        "dense_us_per_token": round(ms_den * 1e3 / (B * world), 2),
+        "speedup_vs_dense": round(ms_den / ms_kas, 3),
+        "paper_h100_us_per_token": 1415,
+        "roofline": {"kernel": "kscd sparse_decode (reuse layer)", "bound": "hbm",
+                     "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4), "traffic": None, "peak_kind": peaks_kind,
+                     "bytes_per_launch": reuse_bytes, "launch_ms": round(reuse_ms, 4),
+                     "dense_decode_frac": round(dense_bytes / (dense_ms_launch * 1e-3) / 1e9 / hbm, 4)},
+        "clocks": clk,
+        "gpu_launches": launches_per_step * args.steps,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+    }
+    if extra:
+        line["extra"] = extra
+    del out_kas
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,145 @@
+/*
+ * kascade_b200.h -- C ABI of the B200-native Kascade anchor/reuse attention
+ * engine (libkascade_b200.so, sm_100a).
+ *
+ * Every entry point replaces one step of the reference package's hot path
+ * (kascade 0.1.0, /root/reference/pkg/src/kascade; cited file:line below).
+ * The reference is a pure-Python/numpy library with no FFI, so the boundary
+ * it would bind is this library through ctypes; the
+ * package `paper_2512_16391_b200` is that binding.
+ *
+ * Conventions
+ *   - Plain C: POD parameter structs, raw device pointers, sizes in elements
+ *     unless the name says bytes.  No allocation and no device
+ *     synchronisation happen inside a call: all work is enqueued on `stream`
+ *     (a cudaStream_t passed as void*, NULL = legacy default stream), so the
+ *     calls are CUDA-graph capturable.
+ *   - Dtypes: Q/K/V bf16, head_dim 128 (K/V rows are 256 bytes); outputs,
+ *     scores and LSE fp32; index lists int32.
+ *   - Index-list wire format (anchor -> reuse): int32 idx[rows][k_cap] sorted
+ *     ascending and padded with INT32_MAX, plus int32 counts[rows] -- the
+ *     reference's TopKIndexSet.indices (attention.py:40-67) per (kv head,
+ *     tile), with rows = batch * kv_heads for decode.
+ *   - Return value: KSCD_OK or an error code; kscd_last_error() returns a
+ *     thread-local message for the last failing call on this thread.  The
+ *     Python binding maps the codes to the reference's exception types
+ *     (errors.py:8-58): 1 InvalidArgumentError, 2 UnsupportedOperationError,
+ *     3 KascadeError (CUDA launch/runtime failure).
+ *   - Workspace: callers allocate `kscd_decode_workspace_size()` bytes and
+ *     zero-fill them ONCE at allocation; kernels leave the workspace re-armed.
+ */
+#ifndef KASCADE_B200_H_
+#define KASCADE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KSCD_OK 0
+#define KSCD_INVALID_ARGUMENT 1
+#define KSCD_UNSUPPORTED 2
+#define KSCD_CUDA_ERROR 3
+
+#define KSCD_ABI_VERSION 1
+
+/* One decode step of one layer for a batch of sequences (the reference's
+ * decode tile [t, t+1) with causal bound n = t + 1, tiles.py:145-150). */
+typedef struct kscd_decode_params {
+  int32_t batch;          /* B */
+  int32_t num_q_heads;    /* Hq; query head h reads kv head h / (Hq/Hkv), trace.py:38-43 */
+  int32_t num_kv_heads;   /* Hkv */
+  int32_t head_dim;       /* must be 128 */
+  int32_t seq_len;        /* n: keys 0..n-1 are visible (the step's own token included) */
+  const void* q;          /* bf16 [B][Hq][128], contiguous */
+  const void* k_cache;    /* bf16; row j of (b, g) at k_cache + b*kv_stride_batch + g*kv_stride_head + j*128 */
+  const void* v_cache;    /* bf16, same layout as k_cache */
+  int64_t kv_stride_batch, kv_stride_head;   /* elements; rows are contiguous (stride 128) */
+  float softmax_scale;    /* <= 0 selects 1/sqrt(head_dim) (attention.py:120) */
+  float* out;             /* fp32 [B][Hq][128] */
+  float* lse;             /* fp32 [B][Hq] natural-log normaliser; may be NULL */
+  /* sparse selection (kscd_sparse_decode): the list of kv head g in
+   * sequence b is indices + (b*num_src_heads + src)*k_cap with
+   * src = head_map[g] (runner.py:210-225), length counts[b*num_src_heads + src]. */
+  const int32_t* indices;
+  const int32_t* counts;
+  int32_t k_cap;
+  int32_t num_src_heads;  /* kv heads of the anchor's list (usually Hkv) */
+  const int32_t* head_map;/* device int32 [Hkv]; NULL = identity */
+  /* log2-domain scores s*log2(e) of every (b, h, key) (anchor layers);
+   * kscd_dense_decode writes them when non-NULL. */
+  float* scores;          /* fp32 [B][Hq][score_stride], score_stride even and >= n */
+  int64_t score_stride;
+  void* workspace;
+  size_t workspace_bytes;
+  int32_t num_splits;     /* split-K factor; 0 = automatic */
+} kscd_decode_params;
+
+/* Selection of one decode step: pooled post-softmax weights of the G heads
+ * of each kv head (runner.py:148-152), k = k_budget(n) (tiles.py:81-89) and
+ * the exact Top-k (attention.py:147-174). */
+typedef struct kscd_select_decode_params {
+  int32_t batch, num_q_heads, num_kv_heads, seq_len;
+  const float* scores;    /* from kscd_dense_decode / kscd_anchor_scores_decode */
+  int64_t score_stride;
+  const float* lse;       /* natural-log LSE of the same call */
+  float* pooled;          /* scratch fp32 [B*Hkv][pooled_stride], pooled_stride % 4 == 0, >= n */
+  int64_t pooled_stride;
+  double topk_fraction;   /* KBudgetPolicy.fraction in (0, 1] */
+  int32_t k_min;          /* KBudgetPolicy.k_min >= 1 */
+  int32_t* indices;       /* int32 [B*Hkv][k_cap] */
+  int32_t* counts;        /* int32 [B*Hkv] */
+  int32_t k_cap;          /* >= k_budget(n) */
+} kscd_select_decode_params;
+
+/* Generic exact Top-k over rows of fp32 values (oracle_topk_indices). */
+typedef struct kscd_topk_params {
+  int32_t rows;
+  const float* values;    /* row r at values + r*value_stride */
+  int64_t value_stride;
+  const int32_t* lengths; /* device [rows] or NULL (=> length) */
+  int32_t length;
+  const int32_t* ks;      /* device [rows] or NULL (=> k) */
+  int32_t k;
+  int32_t* indices;       /* [rows][k_cap] */
+  int32_t* counts;        /* [rows] = min(k, length) */
+  int32_t k_cap;
+} kscd_topk_params;
+
+int kscd_abi_version(void);
+const char* kscd_last_error(void);
+
+/* Bytes of workspace the decode entry points need for these shapes. */
+int kscd_decode_workspace_size(const kscd_decode_params* p, size_t* bytes);
+
+/* Dense attention of the step's query over keys 0..n-1: out, lse, and --
+ * when p->scores != NULL -- the scores the anchor-0 selection pools.
+ * Replaces dense_attention (attention.py:106-144) for the decode row; the
+ * dense (Top-k = 100%) baseline mode and layer 0 of run_kascade
+ * (runner.py:250-262). */
+int kscd_dense_decode(const kscd_decode_params* p, void* stream);
+
+/* Anchor pass 1: scores + lse only, V untouched. */
+int kscd_anchor_scores_decode(const kscd_decode_params* p, void* stream);
+
+/* Sparse attention over a selected key list per kv head, gathered through
+ * the head-remap table: topk_attention (attention.py:185-253) on the
+ * decode tile with _routed_selections (runner.py:210-225). */
+int kscd_sparse_decode(const kscd_decode_params* p, void* stream);
+
+/* Pooled post-softmax weights + k_budget + exact Top-k of one decode step
+ * (runner.py:164-207 in remapped mode). */
+int kscd_select_decode(const kscd_select_decode_params* p, void* stream);
+
+/* oracle_topk_indices (attention.py:147-174) over device rows. */
+int kscd_topk(const kscd_topk_params* p, void* stream);
+
+/* k_budget (tiles.py:81-89): min(max(floor(fraction*n), k_min), n). */
+int32_t kscd_k_budget(double fraction, int32_t k_min, int32_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KASCADE_B200_H_ */

@@ -357,14 +357,15 @@ def dense_row(q: np.ndarray, Kg: np.ndarray, Vg: np.ndarray):
 def decode_step(q: np.ndarray, K: np.ndarray, V: np.ndarray, anchors: Sequence[int],
                 head_maps: Dict[int, Sequence[int]], fraction: float, k_min: int,
                 pooling: str = POST, mode: str = REMAPPED, want_mass: bool = True,
-                layers: Optional[Iterable[int]] = None):
+                layers: Optional[Iterable[int]] = None, timings: Optional[Dict[int, float]] = None):
     """One decode step (the last token t = n-1) of ``run_kascade(phase=
     'decode')`` for one sequence, in O(n) per layer.
 
     q [L][Hq][d] is the step's query, K/V [L][Hkv][n][d] the cache including
     the token itself.  Returns (Y [L][Hq][d], sels {layer: [Hkv] arrays of the
     selection used by that layer}, mass [L][Hq]).  Tile = [n-1, n), causal
-    bound n, k = k_budget(n) (runner.py:199-206, tiles.py:145-150)."""
+    bound n, k = k_budget(n) (runner.py:199-206, tiles.py:145-150).
+    ``timings`` (optional) receives the wall time of every layer."""
     L, Hq, d = q.shape
     Hkv, n = K.shape[1], K.shape[2]
     G = Hq // Hkv
@@ -375,10 +376,12 @@ def decode_step(q: np.ndarray, K: np.ndarray, V: np.ndarray, anchors: Sequence[i
     aset = set(anchors)
     cur = None
     todo = set(range(L)) if layers is None else set(layers)
+    clock = __import__("time").perf_counter
     for l in range(L):
         is_anchor = l == 0 or l in aset
         if l not in todo and not is_anchor:
             continue
+        t_start = clock()
         P = np.zeros((Hq, 1, n), np.float32)
         Yd = np.zeros((Hq, d), np.float32)
         if l == 0 or want_mass or (is_anchor and pooling == POST):
@@ -398,6 +401,8 @@ def decode_step(q: np.ndarray, K: np.ndarray, V: np.ndarray, anchors: Sequence[i
             Y[0] = Yd
             mass[0] = 1.0
             sels_used[0] = [cur[(g, n - 1)] for g in range(Hkv)]
+            if timings is not None:
+                timings[0] = clock() - t_start
             continue
         if l in aset:
             sels = cur
@@ -418,6 +423,8 @@ def decode_step(q: np.ndarray, K: np.ndarray, V: np.ndarray, anchors: Sequence[i
                 Y[l, h] = (p @ vs)[0]
                 if want_mass:
                     mass[l, h] = np.float32(P[h, 0, sel].astype(np.float64).sum())
+        if timings is not None:
+            timings[l] = clock() - t_start
     del kk
     return Y, sels_used, mass
 

@@ -1,0 +1,242 @@
+// C-ABI layer of libkascade_b200.so: host-side validation (the reference's
+// InvalidArgument / Unsupported conditions), split-K planning and launches.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <string.h>
+
+#include <string>
+
+#include "../../include/kascade_b200.h"
+#include "kscd_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return KSCD_OK;
+  return fail(KSCD_CUDA_ERROR, "%s: %s", what, cudaGetErrorString(e));
+}
+
+constexpr int kMaxSplits = 64;
+constexpr int kSmCount = 148;
+constexpr int kCtasPerSm = 2;
+
+// Split-K factor: enough CTAs to cover the SMs in whole waves, each CTA a
+// contiguous run of 64-key tiles of one (b, g).
+int plan_splits(int pairs, int keys, int requested) {
+  const int tiles = (keys + kscd::decode_tile_keys() - 1) / kscd::decode_tile_keys();
+  if (requested > 0) return std::max(1, std::min({requested, kMaxSplits, std::max(tiles, 1)}));
+  const int slots = kSmCount * kCtasPerSm;
+  const int want = std::max(1, (slots + pairs - 1) / pairs);
+  int best = 1;
+  double best_eff = -1.0;
+  for (int s = want; s <= std::min(std::max(4 * want, want), kMaxSplits); ++s) {
+    if (s > tiles) break;
+    const int tps = (tiles + s - 1) / s;
+    const int used = (tiles + tps - 1) / tps;            // splits that get work
+    const double waves = (double)pairs * s / slots;
+    const double eff = (waves / ceil(waves)) * ((double)tiles / (tps * (double)used));
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
+  }
+  return std::max(1, std::min(best, std::max(tiles, 1)));
+}
+
+size_t decode_ws_bytes(const kscd_decode_params* p) {
+  const size_t bh = (size_t)p->batch * p->num_q_heads;
+  size_t bytes = bh * kMaxSplits * (kscd::kHeadDimC + 2) * sizeof(float);
+  bytes = (bytes + 255) & ~(size_t)255;
+  bytes += (size_t)p->batch * p->num_kv_heads * sizeof(int);
+  return bytes;
+}
+
+int check_decode(const kscd_decode_params* p, bool need_v, bool sparse) {
+  if (!p) return fail(KSCD_INVALID_ARGUMENT, "params is NULL");
+  if (p->head_dim != 128) return fail(KSCD_UNSUPPORTED, "head_dim %d unsupported (engine is d=128)", p->head_dim);
+  if (p->batch < 1 || p->num_q_heads < 1 || p->num_kv_heads < 1)
+    return fail(KSCD_INVALID_ARGUMENT, "batch/num_q_heads/num_kv_heads must be >= 1");
+  if (p->num_q_heads % p->num_kv_heads)
+    return fail(KSCD_INVALID_ARGUMENT, "num_query_heads (%d) must be divisible by num_kv_heads (%d)",
+                p->num_q_heads, p->num_kv_heads);
+  const int G = p->num_q_heads / p->num_kv_heads;
+  if (G > 16) return fail(KSCD_UNSUPPORTED, "group size %d > 16 unsupported", G);
+  if (p->seq_len < 1) return fail(KSCD_INVALID_ARGUMENT, "seq_len must be >= 1");
+  if (!p->q || !p->k_cache || (need_v && !p->v_cache))
+    return fail(KSCD_INVALID_ARGUMENT, "q/k_cache/v_cache must be non-NULL");
+  if (need_v && !p->out) return fail(KSCD_INVALID_ARGUMENT, "out must be non-NULL");
+  if (((uintptr_t)p->q | (uintptr_t)p->k_cache | (uintptr_t)p->v_cache) & 15)
+    return fail(KSCD_INVALID_ARGUMENT, "q/k/v must be 16-byte aligned");
+  if ((p->kv_stride_batch | p->kv_stride_head) & 7)
+    return fail(KSCD_INVALID_ARGUMENT, "kv strides must be multiples of 8 elements");
+  if (sparse) {
+    if (!p->indices || !p->counts) return fail(KSCD_INVALID_ARGUMENT, "indices/counts must be non-NULL");
+    if (p->k_cap < 1) return fail(KSCD_INVALID_ARGUMENT, "k_cap must be >= 1");
+    if (p->num_src_heads < 1) return fail(KSCD_INVALID_ARGUMENT, "num_src_heads must be >= 1");
+  }
+  if (p->scores) {
+    if (p->score_stride < p->seq_len || (p->score_stride & 1))
+      return fail(KSCD_INVALID_ARGUMENT, "score_stride must be even and >= seq_len");
+  }
+  if (!p->workspace || p->workspace_bytes < decode_ws_bytes(p))
+    return fail(KSCD_INVALID_ARGUMENT, "workspace too small (%zu < %zu bytes)", p->workspace_bytes,
+                decode_ws_bytes(p));
+  return KSCD_OK;
+}
+
+kscd::DecodeArgs make_args(const kscd_decode_params* p, int keys) {
+  kscd::DecodeArgs a{};
+  a.B = p->batch;
+  a.Hq = p->num_q_heads;
+  a.Hkv = p->num_kv_heads;
+  a.G = p->num_q_heads / p->num_kv_heads;
+  a.n = p->seq_len;
+  a.q = (const __nv_bfloat16*)p->q;
+  a.k = (const __nv_bfloat16*)p->k_cache;
+  a.v = (const __nv_bfloat16*)p->v_cache;
+  a.kv_sb = p->kv_stride_batch;
+  a.kv_sh = p->kv_stride_head;
+  const float scale = p->softmax_scale > 0.f ? p->softmax_scale : (float)(1.0 / sqrt((double)p->head_dim));
+  a.scale_log2 = scale * kscd::kLog2eC;
+  a.out = p->out;
+  a.lse = p->lse;
+  a.idx = p->indices;
+  a.cnt = p->counts;
+  a.k_cap = p->k_cap;
+  a.idx_sb = (int64_t)p->num_src_heads * p->k_cap;
+  a.idx_sh = p->k_cap;
+  a.cnt_sb = p->num_src_heads;
+  a.head_map = p->head_map;
+  a.scores = p->scores;
+  a.score_stride = p->score_stride;
+  a.splits = plan_splits(a.B * a.Hkv, keys, p->num_splits);
+  const size_t bh = (size_t)a.B * a.Hq;
+  a.part = (float*)p->workspace;
+  a.part_ml = a.part + bh * a.splits * kscd::kHeadDimC;
+  size_t off = bh * kMaxSplits * (kscd::kHeadDimC + 2) * sizeof(float);
+  off = (off + 255) & ~(size_t)255;
+  a.counters = (int*)((char*)p->workspace + off);
+  return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+int kscd_abi_version(void) { return KSCD_ABI_VERSION; }
+
+const char* kscd_last_error(void) { return g_last_error.c_str(); }
+
+int32_t kscd_k_budget(double fraction, int32_t k_min, int32_t n) {
+  if (n < 1) return 0;
+  long long k = (long long)floor(fraction * (double)n);
+  if (k < k_min) k = k_min;
+  if (k > n) k = n;
+  return (int32_t)k;
+}
+
+int kscd_decode_workspace_size(const kscd_decode_params* p, size_t* bytes) {
+  if (!p || !bytes) return fail(KSCD_INVALID_ARGUMENT, "NULL argument");
+  *bytes = decode_ws_bytes(p);
+  return KSCD_OK;
+}
+
+int kscd_dense_decode(const kscd_decode_params* p, void* stream) {
+  int rc = check_decode(p, true, false);
+  if (rc) return rc;
+  kscd::DecodeArgs a = make_args(p, p->seq_len);
+  return cuda_status(kscd::launch_decode_attn(kscd::MODE_DENSE, a, (cudaStream_t)stream), "kscd_dense_decode");
+}
+
+int kscd_anchor_scores_decode(const kscd_decode_params* p, void* stream) {
+  int rc = check_decode(p, false, false);
+  if (rc) return rc;
+  if (!p->scores || !p->lse) return fail(KSCD_INVALID_ARGUMENT, "scores and lse must be non-NULL");
+  kscd::DecodeArgs a = make_args(p, p->seq_len);
+  return cuda_status(kscd::launch_decode_attn(kscd::MODE_SCORES, a, (cudaStream_t)stream),
+                     "kscd_anchor_scores_decode");
+}
+
+int kscd_sparse_decode(const kscd_decode_params* p, void* stream) {
+  int rc = check_decode(p, true, true);
+  if (rc) return rc;
+  kscd::DecodeArgs a = make_args(p, p->k_cap);
+  a.scores = nullptr;
+  return cuda_status(kscd::launch_decode_attn(kscd::MODE_SPARSE, a, (cudaStream_t)stream), "kscd_sparse_decode");
+}
+
+int kscd_select_decode(const kscd_select_decode_params* p, void* stream) {
+  if (!p) return fail(KSCD_INVALID_ARGUMENT, "params is NULL");
+  if (p->batch < 1 || p->num_q_heads < 1 || p->num_kv_heads < 1 || p->num_q_heads % p->num_kv_heads)
+    return fail(KSCD_INVALID_ARGUMENT, "bad head/batch shape");
+  if (p->seq_len < 1) return fail(KSCD_INVALID_ARGUMENT, "seq_len must be >= 1");
+  if (!(p->topk_fraction > 0.0 && p->topk_fraction <= 1.0))
+    return fail(KSCD_INVALID_ARGUMENT, "fraction must be in (0, 1], got %g", p->topk_fraction);
+  if (p->k_min < 1) return fail(KSCD_INVALID_ARGUMENT, "k_min must be >= 1, got %d", p->k_min);
+  if (!p->scores || !p->lse || !p->pooled || !p->indices || !p->counts)
+    return fail(KSCD_INVALID_ARGUMENT, "NULL buffer");
+  if (p->pooled_stride < p->seq_len || (p->pooled_stride & 3) || (p->score_stride & 3) ||
+      (((uintptr_t)p->scores | (uintptr_t)p->pooled) & 15))
+    return fail(KSCD_INVALID_ARGUMENT, "pooled/score strides must be multiples of 4 and buffers 16-byte aligned");
+  const int k = kscd_k_budget(p->topk_fraction, p->k_min, p->seq_len);
+  if (p->k_cap < k) return fail(KSCD_INVALID_ARGUMENT, "k_cap %d < k_budget %d", p->k_cap, k);
+  kscd::PoolDecodeArgs pa{};
+  pa.B = p->batch;
+  pa.Hq = p->num_q_heads;
+  pa.Hkv = p->num_kv_heads;
+  pa.G = p->num_q_heads / p->num_kv_heads;
+  pa.n = p->seq_len;
+  pa.scores = p->scores;
+  pa.score_stride = p->score_stride;
+  pa.lse = p->lse;
+  pa.pooled = p->pooled;
+  pa.pool_stride = p->pooled_stride;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = cuda_status(kscd::launch_pool_decode(pa, st), "pool_decode");
+  if (rc) return rc;
+  kscd::TopkArgs ta{};
+  ta.rows = p->batch * p->num_kv_heads;
+  ta.vals = p->pooled;
+  ta.val_stride = p->pooled_stride;
+  ta.len = p->seq_len;
+  ta.k = k;
+  ta.idx = p->indices;
+  ta.counts = p->counts;
+  ta.k_cap = p->k_cap;
+  return cuda_status(kscd::launch_topk(ta, st), "topk");
+}
+
+int kscd_topk(const kscd_topk_params* p, void* stream) {
+  if (!p) return fail(KSCD_INVALID_ARGUMENT, "params is NULL");
+  if (p->rows < 0) return fail(KSCD_INVALID_ARGUMENT, "rows must be >= 0");
+  if (!p->ks && p->k < 1) return fail(KSCD_INVALID_ARGUMENT, "k must be >= 1, got %d", p->k);
+  if (!p->lengths && p->length < 1) return fail(KSCD_INVALID_ARGUMENT, "p must be a non-empty vector");
+  if (!p->values || !p->indices || !p->counts) return fail(KSCD_INVALID_ARGUMENT, "NULL buffer");
+  kscd::TopkArgs ta{};
+  ta.rows = p->rows;
+  ta.vals = p->values;
+  ta.val_stride = p->value_stride;
+  ta.lens = p->lengths;
+  ta.len = p->length;
+  ta.ks = p->ks;
+  ta.k = p->k;
+  ta.idx = p->indices;
+  ta.counts = p->counts;
+  ta.k_cap = p->k_cap;
+  return cuda_status(kscd::launch_topk(ta, (cudaStream_t)stream), "kscd_topk");
+}
+
+}  // extern "C"

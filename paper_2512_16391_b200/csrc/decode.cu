@@ -1,0 +1,343 @@
+// Split-K decode attention for Kascade (one query token per sequence).
+//
+// One kernel template covers the three decode layer kinds:
+//   MODE_DENSE   keys 0..n-1 of kv head g   (dense baseline and anchor-0;
+//                optionally emits the log2-domain scores the anchor-0
+//                selection pools)                    attention.py:106-144
+//   MODE_SPARSE  keys idx[b][map[g]][0..cnt) (reuse layers through the head
+//                remap table, and anchors over their own fresh sets)
+//                                                    attention.py:185-253,
+//                                                    runner.py:210-225
+//   MODE_SCORES  QK^T only: scores + LSE, V is never read (anchor pass 1)
+//
+// Grid = (splits, Hkv, B); 4 warps per CTA.  K/V rows (256 B each) stream
+// through a cp.async (LDGSTS) ring of 64-key tiles -- contiguous rows for the
+// dense modes, gathered rows for the sparse mode -- XOR-swizzled so the
+// ldmatrix reads are bank-conflict free.  Each warp owns 16 keys of a tile
+// and keeps its own online-softmax state for the G query heads of the group
+// (G <= 16 rows of one m16n8k16 tile), so there is no CTA barrier per tile
+// beyond the ring's.  Partial (m, l, O) of the 4 warps are merged in shared
+// memory; the last CTA of a (b, g) to finish merges the splits (warp-shuffle
+// LSE merge) and resets its arrival counter, so no extra launch is needed.
+#include "common.cuh"
+#include "kscd_internal.h"
+
+namespace kscd {
+
+constexpr int kTileKeys = 64;
+constexpr int kThreads = 128;
+constexpr int kTileBytes = kTileKeys * kRowBytes;  // 16 KB
+
+template <int MODE>
+struct DecodeCfg {
+  static constexpr bool kHasV = MODE != MODE_SCORES;
+  static constexpr int kStages = kHasV ? 3 : 5;
+  static constexpr int kStageBytes = kHasV ? 2 * kTileBytes : kTileBytes;
+  static constexpr int kPipeBytes = kStages * kStageBytes;
+  // merge scratch reuses the ring: 4 warps x 16 rows x (128 + 2) floats
+  static constexpr int kMergeBytes = 4 * 16 * (kHeadDim + 2) * 4;
+  static constexpr int kSmemBytes = kPipeBytes > kMergeBytes ? kPipeBytes : kMergeBytes;
+};
+
+template <int MODE, bool G16>
+__global__ void __launch_bounds__(kThreads, 2) decode_attn_kernel(const DecodeArgs a) {
+  using Cfg = DecodeCfg<MODE>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int G = a.G;
+
+  const __nv_bfloat16* kbase = a.k + (int64_t)b * a.kv_sb + (int64_t)g * a.kv_sh;
+  const __nv_bfloat16* vbase = a.v + (int64_t)b * a.kv_sb + (int64_t)g * a.kv_sh;
+  const int* sel = nullptr;
+  int count = a.n;
+  if (MODE == MODE_SPARSE) {
+    const int src = a.head_map ? __ldg(a.head_map + g) : g;
+    sel = a.idx + (int64_t)b * a.idx_sb + (int64_t)src * a.idx_sh;
+    count = min(__ldg(a.cnt + (int64_t)b * a.cnt_sb + src), a.k_cap);
+  }
+  const int ntiles = (count + kTileKeys - 1) / kTileKeys;
+  const int tps = (ntiles + a.splits - 1) / a.splits;
+  const int t0 = split * tps;
+  const int t1 = min(ntiles, t0 + tps);
+  const int my_tiles = max(0, t1 - t0);
+
+  // ---- Q fragments (A operand: rows = query heads of the group) --------
+  uint32_t qa0[8], qa2[8], qa1[8], qa3[8];
+  {
+    const __nv_bfloat16* qg = a.q + ((int64_t)b * a.Hq + (int64_t)g * G) * kHeadDim;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int c = ks * 16 + 2 * tig;
+      qa0[ks] = gid < G ? *reinterpret_cast<const uint32_t*>(qg + gid * kHeadDim + c) : 0u;
+      qa2[ks] = gid < G ? *reinterpret_cast<const uint32_t*>(qg + gid * kHeadDim + c + 8) : 0u;
+      if (G16) {
+        const int r = gid + 8;
+        qa1[ks] = r < G ? *reinterpret_cast<const uint32_t*>(qg + r * kHeadDim + c) : 0u;
+        qa3[ks] = r < G ? *reinterpret_cast<const uint32_t*>(qg + r * kHeadDim + c + 8) : 0u;
+      } else {
+        qa1[ks] = 0u;
+        qa3[ks] = 0u;
+      }
+    }
+  }
+
+  const uint32_t pipe = smem_u32(smem);
+  // Each thread copies chunk column (tid & 15) of rows (tid >> 4) + 8 i.
+  const int my_chunk = tid & 15, my_row0 = tid >> 4;
+
+  auto issue_tile = [&](int t, int stage) {
+    const int key0 = (t0 + t) * kTileKeys;
+    const uint32_t kdst = pipe + stage * Cfg::kStageBytes;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row = my_row0 + 8 * i;
+      const int kk = key0 + row;
+      const bool valid = kk < count;
+      int pos = valid ? kk : 0;
+      if (MODE == MODE_SPARSE) pos = valid ? __ldg(sel + kk) : 0;
+      const uint32_t off = row * kRowBytes + swz(row, my_chunk) * 16;
+      const int64_t src = (int64_t)pos * kHeadDim + my_chunk * 8;
+      cp_async16_zfill(kdst + off, kbase + src, valid);
+      if (Cfg::kHasV) cp_async16_zfill(kdst + kTileBytes + off, vbase + src, valid);
+    }
+  };
+
+  // ---- online softmax state (rows gid and gid + 8) ---------------------
+  float m_r[2] = {-INFINITY, -INFINITY};
+  float l_r[2] = {0.f, 0.f};
+  float o[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+
+#pragma unroll
+  for (int s = 0; s < Cfg::kStages - 1; ++s) {
+    if (s < my_tiles) issue_tile(s, s);
+    cp_async_commit();
+  }
+
+  for (int t = 0; t < my_tiles; ++t) {
+    const int stage = t % Cfg::kStages;
+    cp_async_wait<Cfg::kStages - 2>();
+    __syncthreads();
+    {
+      const int tn = t + Cfg::kStages - 1;
+      if (tn < my_tiles) issue_tile(tn, tn % Cfg::kStages);
+      cp_async_commit();
+    }
+    const uint32_t ks_base = pipe + stage * Cfg::kStageBytes;
+    const int key_w = (t0 + t) * kTileKeys + warp * 16;  // list index of this warp's first key
+
+    // S = Q K^T over the warp's 16 keys (two n8 tiles)
+    float s[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+      const int row = warp * 16 + nt * 8 + (lane & 7);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t b0, b1, b2, b3;
+        const int chunk = 4 * j + (lane >> 3);
+        ldsm_x4(ks_base + row * kRowBytes + swz(row, chunk) * 16, b0, b1, b2, b3);
+        mma_bf16_16816(s[nt], qa0[2 * j], qa1[2 * j], qa2[2 * j], qa3[2 * j], b0, b1);
+        mma_bf16_16816(s[nt], qa0[2 * j + 1], qa1[2 * j + 1], qa2[2 * j + 1], qa3[2 * j + 1], b2, b3);
+      }
+    }
+    // scale to log2 domain, mask keys past the list, optionally emit scores
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int kk = key_w + nt * 8 + 2 * tig + (c & 1);
+        s[nt][c] = kk < count ? s[nt][c] * a.scale_log2 : -INFINITY;
+      }
+      if (MODE != MODE_SPARSE && a.scores != nullptr) {
+        const int kk = key_w + nt * 8 + 2 * tig;
+        if (gid < G && kk < count) {
+          float* dst = a.scores + ((int64_t)b * a.Hq + g * G + gid) * a.score_stride + kk;
+          if (kk + 1 < count) *reinterpret_cast<float2*>(dst) = make_float2(s[nt][0], s[nt][1]);
+          else dst[0] = s[nt][0];
+        }
+        if (G16 && gid + 8 < G && kk < count) {
+          float* dst = a.scores + ((int64_t)b * a.Hq + g * G + gid + 8) * a.score_stride + kk;
+          if (kk + 1 < count) *reinterpret_cast<float2*>(dst) = make_float2(s[nt][2], s[nt][3]);
+          else dst[0] = s[nt][2];
+        }
+      }
+    }
+    // online softmax per head row (quad-reduced max, thread-partial sum)
+    float p[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int r = 0; r < (G16 ? 2 : 1); ++r) {
+      float mx = fmaxf(fmaxf(s[0][2 * r], s[0][2 * r + 1]), fmaxf(s[1][2 * r], s[1][2 * r + 1]));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      const float m_new = fmaxf(m_r[r], mx);
+      const float m_use = m_new == -INFINITY ? 0.f : m_new;
+      const float alpha = fast_exp2(m_r[r] - m_use);
+      m_r[r] = m_new;
+      float sum = 0.f;
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        p[nt][2 * r] = fast_exp2(s[nt][2 * r] - m_use);
+        p[nt][2 * r + 1] = fast_exp2(s[nt][2 * r + 1] - m_use);
+        sum += p[nt][2 * r] + p[nt][2 * r + 1];
+      }
+      l_r[r] = l_r[r] * alpha + sum;
+      if (Cfg::kHasV) {
+#pragma unroll
+        for (int dn = 0; dn < 16; ++dn) {
+          o[dn][2 * r] *= alpha;
+          o[dn][2 * r + 1] *= alpha;
+        }
+      }
+    }
+    if (Cfg::kHasV) {
+      // O += P V : A = P (rows = heads, k = the warp's 16 keys), B = V rows
+      const uint32_t pa0 = pack_bf16(p[0][0], p[0][1]);
+      const uint32_t pa1 = G16 ? pack_bf16(p[0][2], p[0][3]) : 0u;
+      const uint32_t pa2 = pack_bf16(p[1][0], p[1][1]);
+      const uint32_t pa3 = G16 ? pack_bf16(p[1][2], p[1][3]) : 0u;
+      const uint32_t vs_base = ks_base + kTileBytes;
+      const int mtx = lane >> 3;
+      const int row = warp * 16 + (mtx & 1) * 8 + (lane & 7);
+#pragma unroll
+      for (int c = 0; c < 16; c += 2) {
+        uint32_t b0, b1, b2, b3;
+        const int chunk = c + (mtx >> 1);
+        ldsm_x4_t(vs_base + row * kRowBytes + swz(row, chunk) * 16, b0, b1, b2, b3);
+        mma_bf16_16816(o[c], pa0, pa1, pa2, pa3, b0, b1);
+        mma_bf16_16816(o[c + 1], pa0, pa1, pa2, pa3, b2, b3);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+
+  // ---- merge the 4 warps of the CTA in shared memory --------------------
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 1);
+    l_r[r] += __shfl_xor_sync(0xffffffffu, l_r[r], 2);
+  }
+  float* ms = reinterpret_cast<float*>(smem);                 // [4][16] m
+  float* ls = ms + 64;                                         // [4][16] l
+  float* os = ls + 64;                                         // [4][16][128] O
+  if (tig == 0) {
+    ms[warp * 16 + gid] = m_r[0];
+    ls[warp * 16 + gid] = l_r[0];
+    ms[warp * 16 + gid + 8] = m_r[1];
+    ls[warp * 16 + gid + 8] = l_r[1];
+  }
+  if (Cfg::kHasV) {
+#pragma unroll
+    for (int dn = 0; dn < 16; ++dn) {
+      const int col = dn * 8 + 2 * tig;
+      *reinterpret_cast<float2*>(os + (warp * 16 + gid) * kHeadDim + col) = make_float2(o[dn][0], o[dn][1]);
+      if (G16)
+        *reinterpret_cast<float2*>(os + (warp * 16 + gid + 8) * kHeadDim + col) = make_float2(o[dn][2], o[dn][3]);
+    }
+  }
+  __syncthreads();
+
+  // warp w merges heads w, w+4, ...; lane covers 4 dims
+  const int64_t bh0 = (int64_t)b * a.Hq + (int64_t)g * G;
+  for (int h = warp; h < G; h += 4) {
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, ms[w * 16 + h]);
+    const float Mu = M == -INFINITY ? 0.f : M;
+    float L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float sc = fast_exp2(ms[w * 16 + h] - Mu);
+      L += sc * ls[w * 16 + h];
+      if (Cfg::kHasV) {
+        const float4 v = *reinterpret_cast<const float4*>(os + (w * 16 + h) * kHeadDim + lane * 4);
+        acc.x += sc * v.x; acc.y += sc * v.y; acc.z += sc * v.z; acc.w += sc * v.w;
+      }
+    }
+    if (a.splits == 1) {
+      const float inv = L > 0.f ? 1.f / L : 0.f;
+      if (Cfg::kHasV)
+        *reinterpret_cast<float4*>(a.out + (bh0 + h) * kHeadDim + lane * 4) =
+            make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+      if (lane == 0 && a.lse) a.lse[bh0 + h] = (M + __log2f(L)) * kLn2;
+    } else {
+      const int64_t pi = (bh0 + h) * a.splits + split;
+      if (Cfg::kHasV) *reinterpret_cast<float4*>(a.part + pi * kHeadDim + lane * 4) = acc;
+      if (lane == 0) *reinterpret_cast<float2*>(a.part_ml + pi * 2) = make_float2(M, L);
+    }
+  }
+  if (a.splits == 1) return;
+
+  // ---- last CTA of this (b, g) merges the splits -------------------------
+  __shared__ int is_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    int* ctr = a.counters + (int64_t)b * a.Hkv + g;
+    const int prev = atomicAdd(ctr, 1);
+    is_last = prev == a.splits - 1;
+    if (is_last) *ctr = 0;  // re-arm for the next launch / graph replay
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  for (int h = warp; h < G; h += 4) {
+    const int64_t p0 = (bh0 + h) * a.splits;
+    float M = -INFINITY;
+    for (int sp = lane; sp < a.splits; sp += 32) M = fmaxf(M, __ldcg(a.part_ml + (p0 + sp) * 2));
+    M = warp_max(M);
+    const float Mu = M == -INFINITY ? 0.f : M;
+    float L = 0.f;
+    for (int sp = lane; sp < a.splits; sp += 32) {
+      const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.part_ml + (p0 + sp) * 2));
+      L += fast_exp2(ml.x - Mu) * ml.y;
+    }
+    L = warp_sum(L);
+    if (Cfg::kHasV) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int sp = 0; sp < a.splits; ++sp) {
+        const float sc = fast_exp2(__ldcg(a.part_ml + (p0 + sp) * 2) - Mu);
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(a.part + (p0 + sp) * kHeadDim + lane * 4));
+        acc.x += sc * v.x; acc.y += sc * v.y; acc.z += sc * v.z; acc.w += sc * v.w;
+      }
+      const float inv = L > 0.f ? 1.f / L : 0.f;
+      *reinterpret_cast<float4*>(a.out + (bh0 + h) * kHeadDim + lane * 4) =
+          make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    }
+    if (lane == 0 && a.lse) a.lse[bh0 + h] = (M + __log2f(L)) * kLn2;
+  }
+}
+
+template <int MODE>
+static cudaError_t launch_mode(const DecodeArgs& a, cudaStream_t st) {
+  using Cfg = DecodeCfg<MODE>;
+  dim3 grid(a.splits, a.Hkv, a.B);
+  const int smem = Cfg::kSmemBytes;
+  // one-time opt-in to >48 KB dynamic shared memory per instantiation
+  static const cudaError_t attr_hi = cudaFuncSetAttribute(
+      decode_attn_kernel<MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  static const cudaError_t attr_lo = cudaFuncSetAttribute(
+      decode_attn_kernel<MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (attr_hi != cudaSuccess) return attr_hi;
+  if (attr_lo != cudaSuccess) return attr_lo;
+  if (a.G > 8) decode_attn_kernel<MODE, true><<<grid, kThreads, smem, st>>>(a);
+  else decode_attn_kernel<MODE, false><<<grid, kThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decode_attn(int mode, const DecodeArgs& a, cudaStream_t st) {
+  switch (mode) {
+    case MODE_DENSE: return launch_mode<MODE_DENSE>(a, st);
+    case MODE_SPARSE: return launch_mode<MODE_SPARSE>(a, st);
+    default: return launch_mode<MODE_SCORES>(a, st);
+  }
+}
+
+int decode_tile_keys() { return kTileKeys; }
+
+}  // namespace kscd

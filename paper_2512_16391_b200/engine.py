@@ -1,0 +1,114 @@
+"""Layer-loop executors: the device-side counterpart of run_kascade's loop
+(runner.py:228-297) without the reference's always-on dense pass.
+
+``KascadeDecoder.step`` runs one decode step (one query token per sequence)
+through every layer of a plan:
+
+  layer 0      dense attention + scores -> pooled Top-k   (anchor0)
+  anchor l     scores-only pass -> pooled Top-k -> sparse over its own sets
+  reuse l      sparse over the latest anchor's sets routed by head_map[l]
+
+and ``dense_step`` is the Top-k = 100% baseline over the same layers.  All
+buffers are preallocated, so a step can be captured once in a CUDA graph
+and replayed (``capture``), which removes the per-kernel launch gaps that
+dominate the small reuse layers.
+"""
+
+from __future__ import annotations
+
+from typing import Dict, List, Optional, Sequence
+
+import torch
+
+from . import ops
+from .exceptions import InvalidArgumentError
+from .host_types import (KIND_ANCHOR, KIND_ANCHOR0, KIND_REUSE, MODE_ALL_HEADS_POOLED, MODE_REMAPPED,
+                         POOL_POST, k_budget, validate_plan)
+
+
+def layer_kinds(plan, num_layers: int) -> List[str]:
+    anchors = set(plan.core.anchors)
+    return [KIND_ANCHOR0 if l == 0 else KIND_ANCHOR if l in anchors else KIND_REUSE
+            for l in range(num_layers)]
+
+
+class KascadeDecoder:
+    def __init__(self, plan, num_layers: int, batch: int, num_q_heads: int, num_kv_heads: int,
+                 max_seq_len: int, device=None):
+        validate_plan(plan, num_layers, num_kv_heads)
+        if plan.pooling != POOL_POST:
+            raise InvalidArgumentError("decode engine implements post-softmax pooling (the paper's mode)")
+        self.plan = plan
+        self.L, self.B, self.Hq, self.Hkv = num_layers, batch, num_q_heads, num_kv_heads
+        self.n_max = max_seq_len
+        self.device = torch.device(device or "cuda")
+        self.kinds = layer_kinds(plan, num_layers)
+        self.all_heads = plan.mode == MODE_ALL_HEADS_POOLED
+        Hsrc = 1 if self.all_heads else num_kv_heads
+        dev = self.device
+        self.head_maps: Dict[int, Optional[torch.Tensor]] = {}
+        for l, kind in enumerate(self.kinds):
+            if kind != KIND_REUSE:
+                continue
+            if self.all_heads:
+                self.head_maps[l] = torch.zeros(num_kv_heads, dtype=torch.int32, device=dev)
+            else:
+                hm = plan.head_maps[l]
+                self.head_maps[l] = torch.tensor(hm.map, dtype=torch.int32, device=dev)
+        self.shared_map = torch.zeros(num_kv_heads, dtype=torch.int32, device=dev) if self.all_heads else None
+        k_cap = k_budget(plan.k_policy, max_seq_len)
+        n_pad = (max_seq_len + 3) // 4 * 4
+        self.scores = torch.empty(batch, num_q_heads, n_pad, dtype=torch.float32, device=dev)
+        self.pooled = torch.empty(batch * Hsrc, n_pad, dtype=torch.float32, device=dev)
+        self.lse = torch.empty(batch, num_q_heads, dtype=torch.float32, device=dev)
+        self.indices = torch.empty(batch, Hsrc, k_cap, dtype=torch.int32, device=dev)
+        self.counts = torch.zeros(batch, Hsrc, dtype=torch.int32, device=dev)
+        self.out = torch.empty(num_layers, batch, num_q_heads, 128, dtype=torch.float32, device=dev)
+        self._graphs = {}
+
+    # -------------------------------------------------------------- eager
+    def step(self, q: torch.Tensor, k_caches: Sequence[torch.Tensor], v_caches: Sequence[torch.Tensor],
+             seq_len: int) -> torch.Tensor:
+        """q [L][B][Hq][128] bf16; k/v_caches: L tensors [B][Hkv][n_cap][128].
+        Returns the preallocated fp32 outputs [L][B][Hq][128]."""
+        if seq_len > self.n_max:
+            raise InvalidArgumentError(f"seq_len {seq_len} exceeds max_seq_len {self.n_max}")
+        pol = self.plan.k_policy
+        k = k_budget(pol, seq_len)
+        idx = self.indices[:, :, :k]
+        for l, kind in enumerate(self.kinds):
+            ql, kl, vl = q[l], k_caches[l], v_caches[l]
+            if kind == KIND_REUSE:
+                ops.sparse_decode(ql, kl, vl, seq_len, self.indices, self.counts, self.head_maps[l],
+                                  out=self.out[l])
+                continue
+            if kind == KIND_ANCHOR0:
+                ops.dense_decode(ql, kl, vl, seq_len, out=self.out[l], lse=self.lse, scores=self.scores)
+            else:
+                ops.anchor_scores_decode(ql, kl, seq_len, self.scores, self.lse)
+            ops.select_decode(self.scores, self.lse, seq_len, pol, self.Hkv, indices=self.indices,
+                              counts=self.counts, pooled=self.pooled, all_heads=self.all_heads)
+            if kind == KIND_ANCHOR:
+                ops.sparse_decode(ql, kl, vl, seq_len, self.indices, self.counts, self.shared_map,
+                                  out=self.out[l])
+        del idx
+        return self.out
+
+    def dense_step(self, q, k_caches, v_caches, seq_len: int) -> torch.Tensor:
+        """Top-k = 100% baseline: dense attention on every layer."""
+        for l in range(self.L):
+            ops.dense_decode(q[l], k_caches[l], v_caches[l], seq_len, out=self.out[l], lse=self.lse)
+        return self.out
+
+    # -------------------------------------------------------------- graphs
+    def capture(self, q, k_caches, v_caches, seq_len: int, dense: bool = False) -> torch.cuda.CUDAGraph:
+        """Capture one step (fixed buffers and seq_len) in a CUDA graph; replay
+        with ``graph.replay()`` after writing new queries into ``q``."""
+        fn = self.dense_step if dense else self.step
+        fn(q, k_caches, v_caches, seq_len)  # warm-up: one-time kernel attributes outside capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn(q, k_caches, v_caches, seq_len)
+        self._graphs[(seq_len, dense)] = g
+        return g

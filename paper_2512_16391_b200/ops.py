@@ -1,0 +1,254 @@
+"""Batched PyTorch API over the C ABI (device tensors in, device tensors out).
+
+Decode (one query token per sequence; the reference's decode tile
+[n-1, n) with causal bound n, tiles.py:145-150):
+
+    dense_decode(q, k, v, n)                       -> out, lse    (+scores)
+    anchor_decode(q, k, v, n, policy, layer0=...)  -> out, lse, indices, counts
+    reuse_decode(q, k, v, n, indices, counts, head_map) -> out
+    select_decode(scores, lse, n, policy, Hkv)     -> indices, counts
+    topk(values, k)                                -> indices, counts
+
+Layouts: q bf16 [B][Hq][128]; K/V caches bf16 [B][Hkv][n_cap][128] (any
+batch/head strides, rows contiguous); out fp32 [B][Hq][128]; lse fp32
+[B][Hq] (natural log); indices int32 [B][Hkv][k_cap] sorted ascending and
+INT32_MAX-padded; counts int32 [B][Hkv].  Everything is enqueued on the
+current torch stream; nothing synchronises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from typing import Optional, Tuple
+
+import torch
+
+from . import _lib
+from .exceptions import InvalidArgumentError, UnsupportedOperationError
+from .host_types import KBudgetPolicy, k_budget
+
+HEAD_DIM = 128
+INT32_MAX = 2**31 - 1
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _need_cuda(t: torch.Tensor, name: str) -> None:
+    if not t.is_cuda:
+        raise InvalidArgumentError(f"{name} must be a CUDA tensor (the engine has no CPU path)")
+
+
+def _check_q(q: torch.Tensor) -> Tuple[int, int]:
+    _need_cuda(q, "q")
+    if q.dtype != torch.bfloat16:
+        raise UnsupportedOperationError(f"q must be bf16, got {q.dtype}")
+    if q.dim() != 3 or q.shape[-1] != HEAD_DIM or not q.is_contiguous():
+        raise InvalidArgumentError(f"q must be contiguous [B][Hq][128], got {tuple(q.shape)}")
+    return q.shape[0], q.shape[1]
+
+
+def _check_kv(k: torch.Tensor, v: Optional[torch.Tensor], B: int) -> Tuple[int, int, int, int]:
+    _need_cuda(k, "k_cache")
+    for name, t in (("k_cache", k), ("v_cache", v)):
+        if t is None:
+            continue
+        if t.dtype != torch.bfloat16:
+            raise UnsupportedOperationError(f"{name} must be bf16, got {t.dtype}")
+        if t.dim() != 4 or t.shape[-1] != HEAD_DIM or t.stride(3) != 1 or t.stride(2) != HEAD_DIM:
+            raise InvalidArgumentError(f"{name} must be [B][Hkv][n_cap][128] with contiguous rows")
+        if t.shape[0] != B:
+            raise InvalidArgumentError(f"{name} batch {t.shape[0]} != q batch {B}")
+    if v is not None and (v.shape != k.shape or v.stride() != k.stride()):
+        raise InvalidArgumentError("k_cache and v_cache must share shape and strides")
+    return k.shape[1], k.shape[2], k.stride(0), k.stride(1)
+
+
+_WS = {}
+
+
+def decode_workspace(device: torch.device, B: int, Hq: int, Hkv: int) -> torch.Tensor:
+    """Zero-filled split-K workspace, cached per (device, shape); the kernels
+    leave it re-armed so it is reused across calls and graph replays."""
+    key = (device.index if device.index is not None else torch.cuda.current_device(), B, Hq, Hkv)
+    ws = _WS.get(key)
+    if ws is None:
+        p = _lib.DecodeParams(batch=B, num_q_heads=Hq, num_kv_heads=Hkv, head_dim=HEAD_DIM, seq_len=1)
+        nbytes = _lib.c_sz(0)
+        _lib.check(_lib.load().kscd_decode_workspace_size(ctypes.byref(p), ctypes.byref(nbytes)))
+        ws = torch.zeros(nbytes.value, dtype=torch.uint8, device=device)
+        _WS[key] = ws
+    return ws
+
+
+def _decode_params(q, k, v, n, out, lse, scores, scale, num_splits) -> _lib.DecodeParams:
+    B, Hq = _check_q(q)
+    Hkv, n_cap, sb, sh = _check_kv(k, v, B)
+    if not (1 <= n <= n_cap):
+        raise InvalidArgumentError(f"seq_len {n} outside [1, {n_cap}]")
+    if Hq % Hkv:
+        raise InvalidArgumentError(f"num_query_heads ({Hq}) must be divisible by num_kv_heads ({Hkv})")
+    ws = decode_workspace(q.device, B, Hq, Hkv)
+    p = _lib.DecodeParams(
+        batch=B, num_q_heads=Hq, num_kv_heads=Hkv, head_dim=HEAD_DIM, seq_len=int(n),
+        q=q.data_ptr(), k_cache=k.data_ptr(), v_cache=_ptr(v), kv_stride_batch=sb, kv_stride_head=sh,
+        softmax_scale=float(scale or 0.0), out=_ptr(out), lse=_ptr(lse),
+        scores=_ptr(scores), score_stride=scores.stride(1) if scores is not None else 0,
+        workspace=ws.data_ptr(), workspace_bytes=ws.numel(), num_splits=int(num_splits))
+    return p
+
+
+def _check_scores(scores: Optional[torch.Tensor], B: int, Hq: int, n: int) -> None:
+    if scores is None:
+        return
+    if scores.dtype != torch.float32 or scores.dim() != 3 or scores.shape[:2] != (B, Hq) \
+            or scores.stride(2) != 1 or scores.shape[2] < n or scores.stride(1) % 4 or \
+            scores.stride(0) != Hq * scores.stride(1):
+        raise InvalidArgumentError("scores must be fp32 [B][Hq][>=n] with a row stride multiple of 4")
+
+
+def score_buffer(B: int, Hq: int, n: int, device) -> torch.Tensor:
+    """log2-domain score scratch for anchor decode layers, rows padded to 4."""
+    return torch.empty(B, Hq, (n + 3) // 4 * 4, dtype=torch.float32, device=device)
+
+
+def dense_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, seq_len: int, *,
+                 out: Optional[torch.Tensor] = None, lse: Optional[torch.Tensor] = None,
+                 scores: Optional[torch.Tensor] = None, scale: Optional[float] = None,
+                 num_splits: int = 0):
+    """Dense attention of the step's query over keys [0, seq_len)
+    (dense_attention's last row, attention.py:106-144).  If ``scores`` is
+    given, the log2-domain scores s*log2(e) are written for the anchor-0
+    selection."""
+    B, Hq = q.shape[0], q.shape[1]
+    out = torch.empty(B, Hq, HEAD_DIM, dtype=torch.float32, device=q.device) if out is None else out
+    lse = torch.empty(B, Hq, dtype=torch.float32, device=q.device) if lse is None else lse
+    _check_scores(scores, B, Hq, seq_len)
+    p = _decode_params(q, k_cache, v_cache, seq_len, out, lse, scores, scale, num_splits)
+    _lib.call("kscd_dense_decode", p, _stream())
+    return out, lse
+
+
+def anchor_scores_decode(q, k_cache, seq_len, scores, lse, *, scale=None, num_splits=0):
+    """Anchor pass 1: log2-domain scores + LSE; V is not read."""
+    B, Hq = q.shape[0], q.shape[1]
+    _check_scores(scores, B, Hq, seq_len)
+    p = _decode_params(q, k_cache, None, seq_len, None, lse, scores, scale, num_splits)
+    _lib.call("kscd_anchor_scores_decode", p, _stream())
+    return scores, lse
+
+
+def sparse_decode(q, k_cache, v_cache, seq_len, indices, counts, head_map=None, *, out=None, lse=None,
+                  scale=None, num_splits=0):
+    """topk_attention over a decode tile (attention.py:185-253): kv head g of
+    sequence b attends the keys indices[b][head_map[g]][:counts[b][head_map[g]]]
+    (runner.py:210-225).  ``head_map`` is a device int32 [Hkv] tensor (None =
+    identity)."""
+    B, Hq = q.shape[0], q.shape[1]
+    if indices.dtype != torch.int32 or counts.dtype != torch.int32 or indices.dim() != 3 \
+            or not indices.is_contiguous() or not counts.is_contiguous() \
+            or counts.shape != indices.shape[:2] or indices.shape[0] != B:
+        raise InvalidArgumentError("indices must be int32 [B][Hsrc][k_cap], counts int32 [B][Hsrc]")
+    out = torch.empty(B, Hq, HEAD_DIM, dtype=torch.float32, device=q.device) if out is None else out
+    p = _decode_params(q, k_cache, v_cache, seq_len, out, lse, None, scale, num_splits)
+    if head_map is not None:
+        if head_map.dtype != torch.int32 or head_map.numel() != p.num_kv_heads or not head_map.is_cuda:
+            raise InvalidArgumentError("head_map must be a CUDA int32 tensor with one entry per kv head")
+    p.indices, p.counts = indices.data_ptr(), counts.data_ptr()
+    p.k_cap, p.num_src_heads = indices.shape[2], indices.shape[1]
+    p.head_map = _ptr(head_map)
+    _lib.call("kscd_sparse_decode", p, _stream())
+    return out
+
+
+def select_decode(scores, lse, seq_len, policy: KBudgetPolicy, num_kv_heads: int, *, indices=None,
+                  counts=None, pooled=None, all_heads: bool = False):
+    """Pooled post-softmax weights + k_budget + exact Top-k of one decode
+    step (runner.py:164-207).  With ``all_heads`` the pooled vectors of all
+    kv heads are combined into one shared set (all-heads-pooled mode,
+    runner.py:180-197): the result then has one source head."""
+    B, Hq = scores.shape[0], scores.shape[1]
+    Hsrc = 1 if all_heads else num_kv_heads
+    k = k_budget(policy, seq_len)
+    dev = scores.device
+    if pooled is None:
+        pooled = torch.empty(B * Hsrc, (seq_len + 3) // 4 * 4, dtype=torch.float32, device=dev)
+    if indices is None:
+        indices = torch.empty(B, Hsrc, k, dtype=torch.int32, device=dev)
+    if counts is None:
+        counts = torch.empty(B, Hsrc, dtype=torch.int32, device=dev)
+    p = _lib.SelectDecodeParams(
+        batch=B, num_q_heads=Hq, num_kv_heads=Hsrc, seq_len=int(seq_len), scores=scores.data_ptr(),
+        score_stride=scores.stride(1), lse=lse.data_ptr(), pooled=pooled.data_ptr(),
+        pooled_stride=pooled.stride(0), topk_fraction=float(policy.fraction), k_min=int(policy.k_min),
+        indices=indices.data_ptr(), counts=counts.data_ptr(), k_cap=indices.shape[-1])
+    _lib.call("kscd_select_decode", p, _stream())
+    return indices, counts
+
+
+def topk(values: torch.Tensor, k, lengths: Optional[torch.Tensor] = None, k_cap: Optional[int] = None):
+    """oracle_topk_indices (attention.py:147-174) for every row of a device
+    fp32 matrix: ties to the smaller index, ascending output.  ``k`` is an
+    int or a device int32 [rows] tensor."""
+    _need_cuda(values, "values")
+    if values.dtype != torch.float32 or values.dim() != 2 or values.stride(1) != 1:
+        raise InvalidArgumentError("values must be fp32 [rows][len] with contiguous rows")
+    rows, length = values.shape
+    if isinstance(k, int):
+        if k < 1:
+            raise InvalidArgumentError(f"k must be >= 1, got {k}")
+        kc = k_cap or min(k, length)
+        ks = None
+    else:
+        ks = k
+        kc = k_cap or length
+    idx = torch.empty(rows, max(kc, 1), dtype=torch.int32, device=values.device)
+    cnt = torch.empty(rows, dtype=torch.int32, device=values.device)
+    p = _lib.TopkParams(rows=rows, values=values.data_ptr(), value_stride=values.stride(0),
+                        lengths=_ptr(lengths), length=length, ks=_ptr(ks), k=k if ks is None else 0,
+                        indices=idx.data_ptr(), counts=cnt.data_ptr(), k_cap=idx.shape[1])
+    _lib.call("kscd_topk", p, _stream())
+    return idx, cnt
+
+
+def anchor_decode(q, k_cache, v_cache, seq_len, policy: KBudgetPolicy, *, layer0: bool = False,
+                  scores=None, lse=None, out=None, indices=None, counts=None, pooled=None,
+                  all_heads: bool = False):
+    """One anchor layer of a decode step.  Layer 0 (anchor0) runs dense
+    attention and selects from its scores (runner.py:250-262); other anchors
+    run scores-only pass 1, select, then attend sparsely over their own fresh
+    sets (runner.py:263-266).  Returns (out, lse, indices, counts)."""
+    B, Hq = q.shape[0], q.shape[1]
+    Hkv = k_cache.shape[1]
+    if scores is None:
+        scores = score_buffer(B, Hq, seq_len, q.device)
+    lse = torch.empty(B, Hq, dtype=torch.float32, device=q.device) if lse is None else lse
+    if layer0:
+        out, lse = dense_decode(q, k_cache, v_cache, seq_len, out=out, lse=lse, scores=scores)
+        indices, counts = select_decode(scores, lse, seq_len, policy, Hkv, indices=indices, counts=counts,
+                                        pooled=pooled, all_heads=all_heads)
+        return out, lse, indices, counts
+    anchor_scores_decode(q, k_cache, seq_len, scores, lse)
+    indices, counts = select_decode(scores, lse, seq_len, policy, Hkv, indices=indices, counts=counts,
+                                    pooled=pooled, all_heads=all_heads)
+    hm = None
+    if all_heads:
+        hm = torch.zeros(Hkv, dtype=torch.int32, device=q.device)
+    out = sparse_decode(q, k_cache, v_cache, seq_len, indices, counts, hm, out=out)
+    return out, lse, indices, counts
+
+
+def reuse_decode(q, k_cache, v_cache, seq_len, indices, counts, head_map=None, *, out=None):
+    """One reuse layer: the most recent anchor's sets routed through the
+    head map (runner.py:267-275)."""
+    return sparse_decode(q, k_cache, v_cache, seq_len, indices, counts, head_map, out=out)
+
+
+def default_scale() -> float:
+    return 1.0 / math.sqrt(HEAD_DIM)

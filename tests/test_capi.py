@@ -1,0 +1,70 @@
+"""CPU checks of the C-ABI boundary: the library builds, loads, exports every
+symbol include/kascade_b200.h declares, and rejects bad arguments with the
+reference's error classes before any launch (no GPU needed)."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from conftest import REPO
+
+HEADER = os.path.join(REPO, "include", "kascade_b200.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2512_16391_b200 import _lib, build
+    build.build()
+    return _lib.load()
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|const char\*)\s+(kscd_\w+)\s*\(", text, re.M)))
+
+
+def test_every_declared_symbol_is_exported(lib):
+    names = declared_functions()
+    assert len(names) >= 8
+    for name in names:
+        assert hasattr(lib, name), name
+
+
+def test_abi_version_and_k_budget(lib):
+    assert lib.kscd_abi_version() == 1
+    # tiles.py:81-89 pins (pkg/tests/test_tiles.py:18-23)
+    for n, k in ((64, 64), (1000, 128), (1280, 128), (4096, 409)):
+        assert lib.kscd_k_budget(0.1, 128, n) == k
+    assert lib.kscd_k_budget(0.1, 1, 4096) == 409  # floor, not round
+    assert lib.kscd_k_budget(1.0, 4096, 10) == 10
+
+
+def test_invalid_arguments_map_to_reference_errors(lib):
+    from paper_2512_16391_b200 import _lib
+    from paper_2512_16391_b200.exceptions import InvalidArgumentError, UnsupportedOperationError
+    p = _lib.DecodeParams(batch=1, num_q_heads=8, num_kv_heads=2, head_dim=64, seq_len=4)
+    with pytest.raises(UnsupportedOperationError):
+        _lib.call("kscd_dense_decode", p, 0)
+    p.head_dim = 128
+    p.num_kv_heads = 3
+    with pytest.raises(InvalidArgumentError, match="divisible"):
+        _lib.call("kscd_dense_decode", p, 0)
+    p.num_kv_heads = 2
+    with pytest.raises(InvalidArgumentError, match="non-NULL"):
+        _lib.call("kscd_sparse_decode", p, 0)
+    t = _lib.TopkParams(rows=1, values=1, length=5, k=0, indices=1, counts=1, k_cap=1)
+    with pytest.raises(InvalidArgumentError, match="k must be >= 1"):
+        _lib.call("kscd_topk", t, 0)
+    s = _lib.SelectDecodeParams(batch=1, num_q_heads=8, num_kv_heads=2, seq_len=10, topk_fraction=0.0, k_min=1)
+    with pytest.raises(InvalidArgumentError, match="fraction"):
+        _lib.call("kscd_select_decode", s, 0)
+
+
+def test_workspace_size_query(lib):
+    from paper_2512_16391_b200 import _lib
+    p = _lib.DecodeParams(batch=8, num_q_heads=32, num_kv_heads=8, head_dim=128, seq_len=131072)
+    nb = ctypes.c_size_t(0)
+    assert lib.kscd_decode_workspace_size(ctypes.byref(p), ctypes.byref(nb)) == 0
+    assert nb.value >= 8 * 32 * 130 * 4
