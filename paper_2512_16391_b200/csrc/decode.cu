@@ -87,6 +87,18 @@ __global__ void __launch_bounds__(kThreads, 2) decode_attn_kernel(const DecodeAr
   // Each thread copies chunk column (tid & 15) of rows (tid >> 4) + 8 i.
   const int my_chunk = tid & 15, my_row0 = tid >> 4;
 
+  // Sparse mode: the gather positions of a tile are loaded one iteration
+  // before its cp.async is issued, so the dependent index load never sits on
+  // the issue path (an L2 round trip per tile otherwise).
+  int pos_next[8];
+  auto load_positions = [&](int t) {
+    const int key0 = (t0 + t) * kTileKeys;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int kk = key0 + my_row0 + 8 * i;
+      pos_next[i] = (MODE == MODE_SPARSE) ? ((t < my_tiles && kk < count) ? __ldg(sel + kk) : 0) : kk;
+    }
+  };
   auto issue_tile = [&](int t, int stage) {
     const int key0 = (t0 + t) * kTileKeys;
     const uint32_t kdst = pipe + stage * Cfg::kStageBytes;
@@ -95,8 +107,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_attn_kernel(const DecodeAr
       const int row = my_row0 + 8 * i;
       const int kk = key0 + row;
       const bool valid = kk < count;
-      int pos = valid ? kk : 0;
-      if (MODE == MODE_SPARSE) pos = valid ? __ldg(sel + kk) : 0;
+      const int pos = valid ? pos_next[i] : 0;
       const uint32_t off = row * kRowBytes + swz(row, my_chunk) * 16;
       const int64_t src = (int64_t)pos * kHeadDim + my_chunk * 8;
       cp_async16_zfill(kdst + off, kbase + src, valid);
@@ -113,9 +124,11 @@ __global__ void __launch_bounds__(kThreads, 2) decode_attn_kernel(const DecodeAr
 
 #pragma unroll
   for (int s = 0; s < Cfg::kStages - 1; ++s) {
+    load_positions(s);
     if (s < my_tiles) issue_tile(s, s);
     cp_async_commit();
   }
+  load_positions(Cfg::kStages - 1);
 
   for (int t = 0; t < my_tiles; ++t) {
     const int stage = t % Cfg::kStages;
@@ -125,6 +138,7 @@ __global__ void __launch_bounds__(kThreads, 2) decode_attn_kernel(const DecodeAr
       const int tn = t + Cfg::kStages - 1;
       if (tn < my_tiles) issue_tile(tn, tn % Cfg::kStages);
       cp_async_commit();
+      load_positions(tn + 1);
     }
     const uint32_t ks_base = pipe + stage * Cfg::kStageBytes;
     const int key_w = (t0 + t) * kTileKeys + warp * 16;  // list index of this warp's first key

@@ -57,7 +57,7 @@ def test_dense_decode_matches_oracle(cuda_ok, n):
     torch.cuda.synchronize()
     assert_outputs_close(out.cpu().numpy(), Y)
     np.testing.assert_allclose(lse_g.cpu().numpy(), lse, rtol=1e-5, atol=1e-4)
-    s_ref = np.einsum("bgnd,bhd->bhn", K[:, :, :n].astype(np.float64).repeat(Hq // Hkv, axis=1),
+    s_ref = np.einsum("bhnd,bhd->bhn", K[:, :, :n].astype(np.float64).repeat(Hq // Hkv, axis=1),
                       q.astype(np.float64)) / math.sqrt(128) * (1 / math.log(2))
     np.testing.assert_allclose(sc[:, :, :n].cpu().numpy(), s_ref, rtol=1e-5, atol=2e-5)
 
@@ -69,7 +69,11 @@ def test_dense_decode_split_invariance(cuda_ok, splits):
     args = [_dev(q, torch.bfloat16), _dev(K, torch.bfloat16), _dev(V, torch.bfloat16), 3000]
     ref, _ = ops.dense_decode(*args, num_splits=1)
     got, _ = ops.dense_decode(*args, num_splits=splits)
-    np.testing.assert_allclose(got.cpu().numpy(), ref.cpu().numpy(), rtol=0, atol=2e-6)
+    # P is rounded to bf16 relative to each split's running max, so splits
+    # agree to bf16 rounding of P, not bit-for-bit; repeat runs are exact
+    np.testing.assert_allclose(got.cpu().numpy(), ref.cpu().numpy(), rtol=0, atol=1e-3)
+    again, _ = ops.dense_decode(*args, num_splits=splits)
+    np.testing.assert_array_equal(again.cpu().numpy(), got.cpu().numpy())
 
 
 def test_dense_decode_group16(cuda_ok):
