@@ -108,6 +108,48 @@ typedef struct kscd_topk_params {
   int32_t k_cap;
 } kscd_topk_params;
 
+/* Prefill of one layer (batch 1, the paper's prefill setting).  Query tiles
+ * are the reference's prefill tiles of 128 rows (tiles.py:137-144). */
+typedef struct kscd_prefill_params {
+  int32_t num_q_heads, num_kv_heads, head_dim, seq_len;   /* head_dim must be 128 */
+  int32_t causal;          /* 1: row r sees keys <= r (attention.py:123-127) */
+  const void* q;           /* bf16 [Hq][N][128], rows contiguous, head stride q_stride_head */
+  const void* k;           /* bf16 [Hkv][N][128], head stride kv_stride_head */
+  const void* v;
+  int64_t q_stride_head, kv_stride_head;   /* elements, multiples of 8 */
+  float softmax_scale;     /* <= 0 selects 1/sqrt(head_dim) */
+  void* out;               /* bf16 [Hq][N][128] contiguous */
+  float* lse;              /* fp32 [Hq][N] natural-log normaliser (nullable for attention) */
+  /* sparse: the list of (source kv head s, tile t) is indices + (s*T + t)*k_cap,
+   * sorted ascending, length counts[s*T + t]; kv head g reads s = head_map[g]. */
+  const int32_t* indices;
+  const int32_t* counts;
+  int32_t k_cap;
+  int32_t num_src_heads;
+  const int32_t* head_map; /* device int32 [Hkv]; NULL = identity */
+  int32_t tile_size;       /* must be 128 */
+} kscd_prefill_params;
+
+/* Pooled post-softmax weights of every prefill tile (anchor pass B) + the
+ * exact Top-k of each (kv head, tile) with k = k_budget(causal bound). */
+typedef struct kscd_select_prefill_params {
+  int32_t num_q_heads, num_kv_heads, head_dim, seq_len;
+  const void* q;
+  const void* k;
+  int64_t q_stride_head, kv_stride_head;
+  float softmax_scale;
+  const float* lse;        /* fp32 [Hq][N] from kscd_dense_prefill / kscd_anchor_lse_prefill */
+  float* pooled;           /* scratch fp32 [Hkv][T][pooled_stride] (all-heads: [1][T][...]) */
+  int64_t pooled_stride;   /* >= N, multiple of 4 */
+  double topk_fraction;
+  int32_t k_min;
+  int32_t all_heads;       /* 1: all-heads-pooled mode, one shared set per tile (runner.py:180-197) */
+  int32_t* indices;        /* int32 [Hkv or 1][T][k_cap] */
+  int32_t* counts;         /* int32 [Hkv or 1][T] */
+  int32_t k_cap;           /* >= k_budget(N) */
+  int32_t tile_size;       /* must be 128 */
+} kscd_select_prefill_params;
+
 int kscd_abi_version(void);
 const char* kscd_last_error(void);
 
@@ -135,6 +177,22 @@ int kscd_select_decode(const kscd_select_decode_params* p, void* stream);
 
 /* oracle_topk_indices (attention.py:147-174) over device rows. */
 int kscd_topk(const kscd_topk_params* p, void* stream);
+
+/* Dense causal prefill attention: O and LSE for every row (dense_attention,
+ * attention.py:106-144, without materialising P); the Top-k = 100% baseline
+ * and the anchor-0 layer. */
+int kscd_dense_prefill(const kscd_prefill_params* p, void* stream);
+
+/* Anchor pass A: LSE of every row only (no P V). */
+int kscd_anchor_lse_prefill(const kscd_prefill_params* p, void* stream);
+
+/* Sparse prefill over the (kv head, tile) selections routed through the head
+ * map, with the causal staircase and the diagonal fallback (topk_attention,
+ * attention.py:185-253; runner.py:210-225). */
+int kscd_sparse_prefill(const kscd_prefill_params* p, void* stream);
+
+/* Anchor selection for prefill (runner.py:164-207). */
+int kscd_select_prefill(const kscd_select_prefill_params* p, void* stream);
 
 /* k_budget (tiles.py:81-89): min(max(floor(fraction*n), k_min), n). */
 int32_t kscd_k_budget(double fraction, int32_t k_min, int32_t n);

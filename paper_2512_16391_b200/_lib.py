@@ -54,6 +54,30 @@ class TopkParams(ctypes.Structure):
     ]
 
 
+class PrefillParams(ctypes.Structure):
+    _fields_ = [
+        ("num_q_heads", c_i32), ("num_kv_heads", c_i32), ("head_dim", c_i32), ("seq_len", c_i32),
+        ("causal", c_i32),
+        ("q", c_vp), ("k", c_vp), ("v", c_vp),
+        ("q_stride_head", c_i64), ("kv_stride_head", c_i64),
+        ("softmax_scale", c_f32),
+        ("out", c_vp), ("lse", c_vp),
+        ("indices", c_vp), ("counts", c_vp), ("k_cap", c_i32), ("num_src_heads", c_i32),
+        ("head_map", c_vp), ("tile_size", c_i32),
+    ]
+
+
+class SelectPrefillParams(ctypes.Structure):
+    _fields_ = [
+        ("num_q_heads", c_i32), ("num_kv_heads", c_i32), ("head_dim", c_i32), ("seq_len", c_i32),
+        ("q", c_vp), ("k", c_vp), ("q_stride_head", c_i64), ("kv_stride_head", c_i64),
+        ("softmax_scale", c_f32), ("lse", c_vp),
+        ("pooled", c_vp), ("pooled_stride", c_i64),
+        ("topk_fraction", c_f64), ("k_min", c_i32), ("all_heads", c_i32),
+        ("indices", c_vp), ("counts", c_vp), ("k_cap", c_i32), ("tile_size", c_i32),
+    ]
+
+
 # entry point name -> params struct (None for non-struct signatures)
 ENTRY_POINTS = {
     "kscd_dense_decode": DecodeParams,
@@ -61,6 +85,10 @@ ENTRY_POINTS = {
     "kscd_sparse_decode": DecodeParams,
     "kscd_select_decode": SelectDecodeParams,
     "kscd_topk": TopkParams,
+    "kscd_dense_prefill": PrefillParams,
+    "kscd_anchor_lse_prefill": PrefillParams,
+    "kscd_sparse_prefill": PrefillParams,
+    "kscd_select_prefill": SelectPrefillParams,
 }
 
 _lock = threading.Lock()

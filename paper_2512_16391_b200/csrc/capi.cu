@@ -239,4 +239,138 @@ int kscd_topk(const kscd_topk_params* p, void* stream) {
   return cuda_status(kscd::launch_topk(ta, (cudaStream_t)stream), "kscd_topk");
 }
 
+// ------------------------------------------------------------------ prefill
+static int check_prefill(const kscd_prefill_params* p, bool sparse) {
+  if (!p) return fail(KSCD_INVALID_ARGUMENT, "params is NULL");
+  if (p->head_dim != 128) return fail(KSCD_UNSUPPORTED, "head_dim %d unsupported (engine is d=128)", p->head_dim);
+  if (p->tile_size != 128) return fail(KSCD_UNSUPPORTED, "tile_size %d unsupported (engine tiles are 128)", p->tile_size);
+  if (p->num_q_heads < 1 || p->num_kv_heads < 1 || p->num_q_heads % p->num_kv_heads)
+    return fail(KSCD_INVALID_ARGUMENT, "num_query_heads (%d) must be divisible by num_kv_heads (%d)",
+                p->num_q_heads, p->num_kv_heads);
+  if (p->seq_len < 1) return fail(KSCD_INVALID_ARGUMENT, "seq_len must be >= 1");
+  if (!p->q || !p->k || !p->v) return fail(KSCD_INVALID_ARGUMENT, "q/k/v must be non-NULL");
+  if ((((uintptr_t)p->q | (uintptr_t)p->k | (uintptr_t)p->v) & 15) || ((p->q_stride_head | p->kv_stride_head) & 7))
+    return fail(KSCD_INVALID_ARGUMENT, "q/k/v must be 16-byte aligned with head strides multiple of 8");
+  if (sparse) {
+    if (!p->indices || !p->counts || p->k_cap < 1 || p->num_src_heads < 1)
+      return fail(KSCD_INVALID_ARGUMENT, "sparse prefill needs indices/counts/k_cap/num_src_heads");
+  }
+  return KSCD_OK;
+}
+
+static kscd::PrefillArgs make_prefill_args(const kscd_prefill_params* p) {
+  kscd::PrefillArgs a{};
+  a.Hq = p->num_q_heads;
+  a.Hkv = p->num_kv_heads;
+  a.G = a.Hq / a.Hkv;
+  a.N = p->seq_len;
+  a.Nk = p->seq_len;
+  a.slots = (a.G % 2 == 0) ? 2 : 1;
+  a.causal = p->causal;
+  const float scale = p->softmax_scale > 0.f ? p->softmax_scale : (float)(1.0 / sqrt((double)p->head_dim));
+  a.scale_log2 = scale * kscd::kLog2eC;
+  a.q = (const __nv_bfloat16*)p->q;
+  a.k = (const __nv_bfloat16*)p->k;
+  a.v = (const __nv_bfloat16*)p->v;
+  a.q_sh = p->q_stride_head;
+  a.kv_sh = p->kv_stride_head;
+  const int T = (p->seq_len + 127) / 128;
+  a.idx = p->indices;
+  a.cnt = p->counts;
+  a.k_cap = p->k_cap;
+  a.idx_sg = (int64_t)T * p->k_cap;
+  a.idx_st = p->k_cap;
+  a.cnt_sg = T;
+  a.head_map = p->head_map;
+  a.out = (__nv_bfloat16*)p->out;
+  a.lse = p->lse;
+  return a;
+}
+
+extern "C" int kscd_dense_prefill(const kscd_prefill_params* p, void* stream) {
+  int rc = check_prefill(p, false);
+  if (rc) return rc;
+  if (!p->out) return fail(KSCD_INVALID_ARGUMENT, "out must be non-NULL");
+  return cuda_status(kscd::launch_prefill_attn(kscd::PMODE_DENSE, make_prefill_args(p), (cudaStream_t)stream),
+                     "kscd_dense_prefill");
+}
+
+extern "C" int kscd_anchor_lse_prefill(const kscd_prefill_params* p, void* stream) {
+  int rc = check_prefill(p, false);
+  if (rc) return rc;
+  if (!p->lse) return fail(KSCD_INVALID_ARGUMENT, "lse must be non-NULL");
+  return cuda_status(kscd::launch_prefill_attn(kscd::PMODE_LSE, make_prefill_args(p), (cudaStream_t)stream),
+                     "kscd_anchor_lse_prefill");
+}
+
+extern "C" int kscd_sparse_prefill(const kscd_prefill_params* p, void* stream) {
+  int rc = check_prefill(p, true);
+  if (rc) return rc;
+  if (!p->out) return fail(KSCD_INVALID_ARGUMENT, "out must be non-NULL");
+  if (!p->causal) return fail(KSCD_UNSUPPORTED, "sparse prefill is causal (runner.py:275)");
+  return cuda_status(kscd::launch_prefill_attn(kscd::PMODE_SPARSE, make_prefill_args(p), (cudaStream_t)stream),
+                     "kscd_sparse_prefill");
+}
+
+extern "C" int kscd_select_prefill(const kscd_select_prefill_params* p, void* stream) {
+  if (!p) return fail(KSCD_INVALID_ARGUMENT, "params is NULL");
+  if (p->head_dim != 128) return fail(KSCD_UNSUPPORTED, "head_dim %d unsupported", p->head_dim);
+  if (p->tile_size != 128) return fail(KSCD_UNSUPPORTED, "tile_size %d unsupported", p->tile_size);
+  if (p->num_q_heads < 1 || p->num_kv_heads < 1 || p->num_q_heads % p->num_kv_heads)
+    return fail(KSCD_INVALID_ARGUMENT, "bad head shape");
+  if (p->seq_len < 1) return fail(KSCD_INVALID_ARGUMENT, "seq_len must be >= 1");
+  if (!(p->topk_fraction > 0.0 && p->topk_fraction <= 1.0))
+    return fail(KSCD_INVALID_ARGUMENT, "fraction must be in (0, 1], got %g", p->topk_fraction);
+  if (p->k_min < 1) return fail(KSCD_INVALID_ARGUMENT, "k_min must be >= 1, got %d", p->k_min);
+  if (!p->q || !p->k || !p->lse || !p->pooled || !p->indices || !p->counts)
+    return fail(KSCD_INVALID_ARGUMENT, "NULL buffer");
+  if (p->pooled_stride < p->seq_len) return fail(KSCD_INVALID_ARGUMENT, "pooled_stride < seq_len");
+  const int kmax = kscd_k_budget(p->topk_fraction, p->k_min, p->seq_len);
+  if (p->k_cap < kmax) return fail(KSCD_INVALID_ARGUMENT, "k_cap %d < k_budget %d", p->k_cap, kmax);
+  const int G = p->num_q_heads / p->num_kv_heads;
+  const int T = (p->seq_len + 127) / 128;
+  cudaStream_t st = (cudaStream_t)stream;
+  kscd::PoolPrefillArgs pa{};
+  pa.Hq = p->num_q_heads;
+  pa.Hkv = p->num_kv_heads;
+  pa.G = G;
+  pa.N = p->seq_len;
+  const float scale = p->softmax_scale > 0.f ? p->softmax_scale : (float)(1.0 / sqrt((double)p->head_dim));
+  pa.scale_log2 = scale * kscd::kLog2eC;
+  pa.q = (const __nv_bfloat16*)p->q;
+  pa.k = (const __nv_bfloat16*)p->k;
+  pa.q_sh = p->q_stride_head;
+  pa.kv_sh = p->kv_stride_head;
+  pa.lse = p->lse;
+  pa.pooled = p->pooled;
+  pa.pool_stride = p->pooled_stride;
+  const int gcount = p->all_heads ? p->num_kv_heads : 1;
+  int launches = 0;
+  for (int gi = 0; gi < gcount; ++gi) {
+    for (int hb = 0; hb < G; hb += 4) {
+      pa.head_begin = hb;
+      pa.nheads = std::min(4, G - hb);
+      pa.g_fixed = p->all_heads ? gi : -1;
+      pa.accumulate = launches > 0;
+      int rc = cuda_status(kscd::launch_pool_prefill(pa, st), "pool_prefill");
+      if (rc) return rc;
+      ++launches;
+    }
+  }
+  kscd::TopkArgs ta{};
+  ta.rows = (p->all_heads ? 1 : p->num_kv_heads) * T;
+  ta.vals = p->pooled;
+  ta.val_stride = p->pooled_stride;
+  ta.len = p->seq_len;
+  ta.k = kmax;
+  ta.idx = p->indices;
+  ta.counts = p->counts;
+  ta.k_cap = p->k_cap;
+  ta.tile = 128;
+  ta.T = T;
+  ta.fraction = p->topk_fraction;
+  ta.k_min = p->k_min;
+  return cuda_status(kscd::launch_topk(ta, st), "topk");
+}
+
 }  // extern "C"

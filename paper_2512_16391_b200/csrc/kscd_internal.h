@@ -62,7 +62,52 @@ struct TopkArgs {
   int* idx;                               // row r at idx + r*k_cap
   int* counts;                            // [rows]
   int k_cap;
+  // prefill tiles: when tile > 0, row r is tile (r % T) with length
+  // min(len, tile*(i+1)) and k = k_budget(fraction, k_min, length)
+  int tile, T;
+  double fraction;
+  int k_min;
 };
 cudaError_t launch_topk(const TopkArgs& a, cudaStream_t st);
+
+// ------------------------------------------------------------------ prefill
+enum { PMODE_DENSE = 0, PMODE_SPARSE = 1, PMODE_LSE = 2 };
+
+struct PrefillArgs {
+  int Hq, Hkv, G, N, Nk;                  // batch 1 (the paper's prefill setting)
+  int slots;                              // query tiles per CTA: 2 heads of a group (G even) or 1
+  int causal;
+  float scale_log2;
+  const __nv_bfloat16* q;                 // [Hq][N][128], head stride q_sh
+  const __nv_bfloat16* k;                 // [Hkv][Nk][128], head stride kv_sh
+  const __nv_bfloat16* v;
+  int64_t q_sh, kv_sh;
+  // sparse: list of (kv head src, tile t) at idx + src*idx_sg + t*idx_st, length cnt[src*cnt_sg + t]
+  const int* idx;
+  const int* cnt;
+  int k_cap;
+  int64_t idx_sg, idx_st, cnt_sg;
+  const int* head_map;                    // [Hkv] (nullable = identity)
+  __nv_bfloat16* out;                     // [Hq][N][128]
+  float* lse;                             // [Hq][N] natural log (nullable)
+};
+cudaError_t launch_prefill_attn(int mode, const PrefillArgs& a, cudaStream_t st);
+
+// Anchor pass B (tile-pooled post-softmax weights), one chunk of <= 4 heads
+// of every kv group per launch.
+struct PoolPrefillArgs {
+  int Hq, Hkv, G, N;
+  int head_begin, nheads;                 // head chunk inside each group
+  int accumulate;                         // add into pooled instead of storing
+  int g_fixed;                            // >= 0: only this kv head, rows indexed by tile only
+  float scale_log2;
+  const __nv_bfloat16* q;
+  const __nv_bfloat16* k;
+  int64_t q_sh, kv_sh;
+  const float* lse;                       // [Hq][N] natural
+  float* pooled;                          // [Hkv or 1][T][pool_stride]
+  int64_t pool_stride;
+};
+cudaError_t launch_pool_prefill(const PoolPrefillArgs& a, cudaStream_t st);
 
 }  // namespace kscd

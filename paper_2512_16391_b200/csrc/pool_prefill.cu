@@ -1,0 +1,201 @@
+// Anchor pass B for prefill: tile-pooled post-softmax weights on tcgen05.
+//
+// For query tile i (rows [128i, 128i+128)) and kv head g the reference pools
+// the post-softmax rows of the G heads of the group over the tile's rows,
+// truncated at the causal bound t1 = min(N, 128(i+1)) (_post_pooled,
+// runner.py:148-152):
+//
+//     pooled[g][i][j] = sum_{h in g, r in tile} exp(s[h][r][j] - lse[h][r]),  j < t1
+//
+// (the reference's mean divides by G*T, a constant that does not change the
+// Top-k).  The kernel computes S^T = K Q^T with KEYS on the MMA M dimension:
+// TMEM lane = key, TMEM column = (head, row), so each thread owns one key and
+// sums exp2(s*scale*log2e - lse2[row]) over its columns in an fp32 register --
+// the column sum needs no shuffles and no bf16 rounding of P (which would
+// break Top-k parity).  LSE comes from the dense / LSE pass of the same layer.
+//
+// CTA = (tile i, kv head g, head chunk of <= 4 heads).  Q of the chunk is
+// resident in shared memory ([half][rows][128 B], 128B-swizzled, so any
+// 256-row slice is one canonical UMMA operand); K blocks stream through a
+// 2-stage TMA ring.  The 512 TMEM columns hold S^T of rows 0-255 and
+// 256-511; two warpgroups each consume one half and ping-pong with the MMA.
+#include "sm100.cuh"
+#include "kscd_internal.h"
+
+namespace kscd {
+using namespace sm100;
+
+namespace pp {
+constexpr int kThreads = 384;
+constexpr int kStages = 2;
+constexpr int kBlock = 128;
+constexpr int kHalfRows = 512 * 128;        // bytes of one 64-column half for 512 rows
+constexpr int kOffQ = 0;                    // [2 halves][512 rows][128 B] = 128 KB
+constexpr int kOffK = 2 * kHalfRows;        // stages x 32 KB
+constexpr int kOffLse = kOffK + kStages * 32768;   // float[512]
+constexpr int kOffRed = kOffLse + 512 * 4;         // float[2][128]
+constexpr int kOffBar = kOffRed + 2 * 128 * 4;
+constexpr int kOffTmem = kOffBar + 16 * 8;
+constexpr int kSmemBytes = kOffTmem + 16 + 1024;
+}  // namespace pp
+
+struct PoolTmaps {
+  CUtensorMap q, k;
+};
+
+// bars: 0 q_full | 1-2 k_full[s] | 3-4 k_empty[s] | 5-6 s_full[x] | 7-8 buf_free[x]
+__global__ void __launch_bounds__(pp::kThreads, 1)
+    pool_prefill_kernel(const __grid_constant__ PoolTmaps tm, const PoolPrefillArgs a) {
+  using namespace pp;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmem);
+  float* lse2 = reinterpret_cast<float*>(smem + kOffLse);
+  float* red = reinterpret_cast<float*>(smem + kOffRed);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T = (a.N + 127) / 128;
+  const int ti = T - 1 - (int)blockIdx.x;        // long (late) tiles first
+  const int g = a.g_fixed >= 0 ? a.g_fixed : (int)blockIdx.y;
+  const int r0 = ti * 128;
+  const int t1 = min(a.N, r0 + 128);             // causal bound of the tile
+  const int nb = (t1 + kBlock - 1) / kBlock;
+  const int nh = a.nheads;                       // heads of this chunk (<= 4)
+  const int hbase = g * a.G + a.head_begin;
+  const int nrows = nh * 128;
+  const int nhalves = (nrows + 255) / 256;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&bars[1 + s], 1);
+      mbar_init(&bars[3 + s], 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&bars[5 + x], 1);
+      mbar_init(&bars[7 + x], 128);
+    }
+    fence_barrier_init();
+  }
+  // per-row log2-domain LSE of the chunk's rows; rows past N never count
+  for (int r = threadIdx.x; r < 512; r += kThreads) {
+    const int hh = r >> 7, rr = r & 127;
+    float v = INFINITY;
+    if (hh < nh && r0 + rr < a.N) v = a.lse[(int64_t)(hbase + hh) * a.N + r0 + rr] * kLog2e;
+    lse2[r] = v;
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
+    if (warp == 0 && lane == 0) {
+      // ------------------------------------------------------- TMA producer
+      tma_prefetch(&tm.q);
+      tma_prefetch(&tm.k);
+      mbar_expect_tx(&bars[0], nh * 2 * 16384);
+      for (int hh = 0; hh < nh; ++hh)
+        for (int hf = 0; hf < 2; ++hf)
+          tma_load_3d(smem + kOffQ + hf * kHalfRows + hh * 16384, &tm.q, &bars[0], hf * 64, r0, hbase + hh);
+      for (int j = 0; j < nb; ++j) {
+        const int st = j % kStages;
+        if (j >= kStages) mbar_wait(&bars[3 + st], ((j / kStages) - 1) & 1);
+        mbar_expect_tx(&bars[1 + st], 32768);
+        for (int hf = 0; hf < 2; ++hf)
+          tma_load_3d(smem + kOffK + st * 32768 + hf * 16384, &tm.k, &bars[1 + st], hf * 64, j * kBlock, g);
+      }
+    } else if (warp == 3 && lane == 0) {
+      // --------------------------------------------------------- MMA issuer
+      const uint32_t qaddr = smem_u32(smem + kOffQ);
+      const uint32_t kaddr = smem_u32(smem + kOffK);
+      mbar_wait(&bars[0], 0);
+      for (int j = 0; j < nb; ++j) {
+        const int st = j % kStages;
+        mbar_wait(&bars[1 + st], (j / kStages) & 1);
+        for (int x = 0; x < nhalves; ++x) {
+          if (j > 0) mbar_wait(&bars[7 + x], (j - 1) & 1);   // WG x has read block j-1
+          tc_fence_after();
+          const int ncols = min(256, nrows - 256 * x);
+          const uint32_t idesc = idesc_bf16(128, ncols, false, false);
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            const uint32_t koff = (ks >> 2) * 16384 + (ks & 3) * 32;
+            const uint32_t qoff = (ks >> 2) * kHalfRows + x * 256 * 128 + (ks & 3) * 32;
+            mma_ss(tmem + 256 * x, sw128_desc(kaddr + st * 32768 + koff, 16, 1024),
+                   sw128_desc(qaddr + qoff, 16, 1024), idesc, ks > 0);
+          }
+          mma_commit(&bars[5 + x]);
+        }
+        mma_commit(&bars[3 + st]);
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n");
+    // --------------------------------------------------- column-sum warpgroups
+    const int x = (warp - 4) >> 2;                 // which 256-row half
+    const int q = warp & 3;
+    const int key_in_blk = q * 32 + lane;          // TMEM lane = key
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + 256 * x;
+    const int ncols = x < nhalves ? min(256, nrows - 256 * x) : 0;
+    // all-heads-pooled mode writes one row per tile (runner.py:180-197)
+    float* out_row = a.pooled + ((int64_t)(a.g_fixed >= 0 ? 0 : g) * T + ti) * a.pool_stride;
+    for (int j = 0; j < nb; ++j) {
+      const int key = j * kBlock + key_in_blk;
+      float acc = 0.f;
+      if (ncols > 0) {
+        mbar_wait(&bars[5 + x], j & 1);
+        tc_fence_after();
+        const bool diag = (j == nb - 1);           // only the last block crosses the staircase
+        for (int c0 = 0; c0 < ncols; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(lane_base + c0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int col = 256 * x + c0 + i;      // chunk row index (head*128 + row)
+            float e = fast_exp2(__uint_as_float(r[i]) * a.scale_log2 - lse2[col]);
+            if (diag && key > r0 + (col & 127)) e = 0.f;
+            acc += e;
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&bars[7 + x]);
+      }
+      // combine the two halves: WG1 parks its sums, WG0 adds and stores
+      if (x == 1) red[(j & 1) * 128 + key_in_blk] = acc;
+      named_bar_sync(2, 256);
+      if (x == 0 && key < t1) {
+        float v = acc + red[(j & 1) * 128 + key_in_blk];
+        if (a.accumulate) v += out_row[key];
+        out_row[key] = v;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// ------------------------------------------------------------------- host
+bool make_prefill_map(CUtensorMap* m, const void* base, int heads, int rows, int64_t head_stride);
+
+cudaError_t launch_pool_prefill(const PoolPrefillArgs& a, cudaStream_t st) {
+  PoolTmaps tm;
+  if (!make_prefill_map(&tm.q, a.q, a.Hq, a.N, a.q_sh)) return cudaErrorInvalidValue;
+  if (!make_prefill_map(&tm.k, a.k, a.Hkv, a.N, a.kv_sh)) return cudaErrorInvalidValue;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(pool_prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pp::kSmemBytes);
+  if (attr != cudaSuccess) return attr;
+  const int T = (a.N + 127) / 128;
+  dim3 grid(T, a.g_fixed >= 0 ? 1 : a.Hkv);
+  pool_prefill_kernel<<<grid, pp::kThreads, pp::kSmemBytes, st>>>(tm, a);
+  return cudaGetLastError();
+}
+
+}  // namespace kscd

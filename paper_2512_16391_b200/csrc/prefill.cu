@@ -1,0 +1,449 @@
+// Prefill attention on the 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+//
+// One CTA = two query tiles of 128 rows -- two query heads of the same kv
+// group at the same token range, so every K/V block is loaded once and used
+// by both -- and a warp-specialised pipeline:
+//
+//   warp 0 (lane 0)  TMA producer: Q tiles once, K/V blocks through a
+//                    2-stage ring (dense modes)
+//   warps 0-2        cp.async gather producers (sparse mode): K/V rows at
+//                    the selected positions into the same 128B-swizzled
+//                    layout TMA would produce
+//   warp 3 (lane 0)  MMA issuer: S_t = Q_t K^T (SS, fp32 in TMEM), then
+//                    O_t += P_t V (TS: P read back from TMEM as bf16)
+//   warps 4-7 / 8-11 softmax warpgroups of tile 0 / tile 1: one thread per
+//                    row (TMEM lane), so the row max / sum need no shuffles;
+//                    P is written over S in TMEM; O is rescaled lazily (only
+//                    when the running max grows by > 2^8), so the correction
+//                    step is rare.
+//
+// The two tiles ping-pong: while one warpgroup exponentiates block j, the
+// tensor core runs the other tile's PV / next S.  TMEM: S0|P0, O0, S1|P1,
+// O1 = 4 x 128 columns (all 512).
+//
+// Modes (reference semantics):
+//   DENSE   causal (or full) attention over keys [0, N): O, LSE
+//           dense_attention, attention.py:106-144 (never materialising P)
+//   SPARSE  keys = the (kv head, tile) selection routed through head_map;
+//           row r sees the selected keys <= r (the staircase), a row with
+//           none falls back to V[r]: topk_attention, attention.py:185-253,
+//           _routed_selections, runner.py:210-225.  O, LSE
+//   LSE     QK^T + online softmax statistics only (anchor pass A)
+#include "sm100.cuh"
+#include "kscd_internal.h"
+
+namespace kscd {
+using namespace sm100;
+
+namespace pf {
+constexpr int kTileM = 128;          // rows per query tile (= Kascade prefill tile)
+constexpr int kBlockN = 128;         // keys per block
+constexpr int kStages = 2;
+constexpr int kThreads = 384;
+constexpr int kTileBytes = 128 * 256;  // 128 rows x 128 bf16
+constexpr int kHalf = 16384;           // one 64-column 128B-swizzled half tile
+// smem layout (bytes, 1024-aligned where needed)
+constexpr int kOffQ = 0;                                   // 2 tiles
+constexpr int kOffK = kOffQ + 2 * kTileBytes;              // stages
+constexpr int kOffV = kOffK + kStages * kTileBytes;
+constexpr int kOffPos = kOffV + kStages * kTileBytes;      // int[stages][128]
+constexpr int kOffBar = kOffPos + kStages * 128 * 4;
+constexpr int kNumBars = 16;
+constexpr int kOffTmem = kOffBar + kNumBars * 8;
+constexpr int kSmemBytes = kOffTmem + 16 + 1024;           // + alignment slack
+constexpr uint32_t kIdescS = idesc_bf16(128, 128, false, false);
+constexpr uint32_t kIdescPV = idesc_bf16(128, 128, false, true);
+constexpr float kRescaleThreshold = 8.0f;                  // log2 units
+}  // namespace pf
+
+struct PrefillTmaps {
+  CUtensorMap q, k, v;
+};
+
+// bars: 0 q_full | 1-2 k_full[s] | 3-4 v_full[s] | 5-6 kv_empty[s] |
+//       7-8 s_full[t] | 9-10 p_full[t] | 11-12 o_done[t]
+template <int MODE>
+__global__ void __launch_bounds__(pf::kThreads, 1)
+    prefill_attn_kernel(const __grid_constant__ PrefillTmaps tm, const PrefillArgs a) {
+  using namespace pf;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmem);
+  int* posbuf = reinterpret_cast<int*>(smem + kOffPos);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_tiles = (a.N + kTileM - 1) / kTileM;
+  const int ti = num_tiles - 1 - (int)blockIdx.x;     // heavy (late) tiles first
+  const int r0 = ti * kTileM;
+  const int nslots = a.slots;                          // 2 (G even) or 1
+  const int h0 = blockIdx.y * nslots;
+  const int g = h0 / a.G;
+
+  // key blocks this tile visits
+  int count = 0;                                       // sparse: selected entries
+  const int* sel = nullptr;
+  int nb;
+  if (MODE == PMODE_SPARSE) {
+    const int src = a.head_map ? __ldg(a.head_map + g) : g;
+    sel = a.idx + (int64_t)src * a.idx_sg + (int64_t)ti * a.idx_st;
+    count = min(__ldg(a.cnt + (int64_t)src * a.cnt_sg + ti), a.k_cap);
+    nb = (count + kBlockN - 1) / kBlockN;
+  } else {
+    const int kend = a.causal ? min(a.N, r0 + kTileM) : a.N;
+    nb = (kend + kBlockN - 1) / kBlockN;
+  }
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&bars[1 + s], MODE == PMODE_SPARSE ? 96 : 1);
+      mbar_init(&bars[3 + s], MODE == PMODE_SPARSE ? 96 : 1);
+      mbar_init(&bars[5 + s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&bars[7 + t], 1);
+      mbar_init(&bars[9 + t], 128);
+      mbar_init(&bars[11 + t], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
+    // ================================================ producers / MMA
+    if (warp == 3) {
+      if (lane == 0 && nb > 0) {
+        // --------------------------------------------------- MMA issuer
+        const uint32_t qaddr = smem_u32(smem + kOffQ);
+        const uint32_t kaddr = smem_u32(smem + kOffK);
+        const uint32_t vaddr = smem_u32(smem + kOffV);
+        auto issue_s = [&](int t, int st) {
+          const uint32_t d = tmem + t * 256;
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            const uint32_t off = (ks >> 2) * kHalf + (ks & 3) * 32;
+            mma_ss(d, sw128_desc(qaddr + t * kTileBytes + off, 16, 1024),
+                   sw128_desc(kaddr + st * kTileBytes + off, 16, 1024), kIdescS, ks > 0);
+          }
+          mma_commit(&bars[7 + t]);
+        };
+        auto issue_pv = [&](int t, int st, int j) {
+          const uint32_t d = tmem + t * 256 + 128;
+          const uint32_t p = tmem + t * 256;
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            mma_ts(d, p + ks * 8, sw128_desc(vaddr + st * kTileBytes + ks * 2048, kHalf, 1024), kIdescPV,
+                   (j > 0 || ks > 0) ? 1u : 0u);
+          }
+        };
+        mbar_wait(&bars[0], 0);
+        mbar_wait(&bars[1], 0);
+        tc_fence_after();
+        for (int t = 0; t < nslots; ++t) issue_s(t, 0);
+        for (int j = 0; j < nb; ++j) {
+          const int st = j % kStages;
+          const uint32_t ph = (j / kStages) & 1;
+          const bool more = j + 1 < nb;
+          const int st1 = (j + 1) % kStages;
+          const uint32_t ph1 = ((j + 1) / kStages) & 1;
+          if (MODE != PMODE_LSE) mbar_wait(&bars[3 + st], ph);
+          // tile 0: PV_j, then S_{j+1}
+          mbar_wait(&bars[9], j & 1);
+          tc_fence_after();
+          if (MODE != PMODE_LSE) {
+            issue_pv(0, st, j);
+            if (j == nb - 1) mma_commit(&bars[11]);
+          }
+          if (more) {
+            mbar_wait(&bars[1 + st1], ph1);
+            tc_fence_after();
+            issue_s(0, st1);
+          }
+          if (nslots == 2) {
+            mbar_wait(&bars[10], j & 1);
+            tc_fence_after();
+            if (MODE != PMODE_LSE) {
+              issue_pv(1, st, j);
+              if (j == nb - 1) mma_commit(&bars[12]);
+            }
+          }
+          mma_commit(&bars[5 + st]);   // K/V stage free once everything so far retires
+          if (more && nslots == 2) issue_s(1, st1);
+        }
+      }
+    } else if (MODE != PMODE_SPARSE) {
+      if (warp == 0 && lane == 0 && nb > 0) {
+        // ----------------------------------------------- TMA producer
+        tma_prefetch(&tm.q);
+        tma_prefetch(&tm.k);
+        tma_prefetch(&tm.v);
+        mbar_expect_tx(&bars[0], nslots * kTileBytes);
+        for (int t = 0; t < nslots; ++t)
+          for (int hf = 0; hf < 2; ++hf)
+            tma_load_3d(smem + kOffQ + t * kTileBytes + hf * kHalf, &tm.q, &bars[0], hf * 64, r0, h0 + t);
+        for (int j = 0; j < nb; ++j) {
+          const int st = j % kStages;
+          if (j >= kStages) mbar_wait(&bars[5 + st], ((j / kStages) - 1) & 1);
+          mbar_expect_tx(&bars[1 + st], kTileBytes);
+          for (int hf = 0; hf < 2; ++hf)
+            tma_load_3d(smem + kOffK + st * kTileBytes + hf * kHalf, &tm.k, &bars[1 + st], hf * 64, j * kBlockN, g);
+          if (MODE != PMODE_LSE) {
+            mbar_expect_tx(&bars[3 + st], kTileBytes);
+            for (int hf = 0; hf < 2; ++hf)
+              tma_load_3d(smem + kOffV + st * kTileBytes + hf * kHalf, &tm.v, &bars[3 + st], hf * 64,
+                          j * kBlockN, g);
+          }
+        }
+      }
+    } else {
+      // ------------------------------------- sparse gather producers (96)
+      const int pt = threadIdx.x;  // 0..95
+      if (pt == 0 && nb > 0) {
+        tma_prefetch(&tm.q);
+        mbar_expect_tx(&bars[0], nslots * kTileBytes);
+        for (int t = 0; t < nslots; ++t)
+          for (int hf = 0; hf < 2; ++hf)
+            tma_load_3d(smem + kOffQ + t * kTileBytes + hf * kHalf, &tm.q, &bars[0], hf * 64, r0, h0 + t);
+      }
+      // Block j's rows are gathered while block j-1's copies are still in
+      // flight; completion is published per block (wait_group, proxy fence,
+      // mbarrier arrive) so the tensor core reads coherent shared memory.
+      const __nv_bfloat16* kg = a.k + (int64_t)g * a.kv_sh;
+      const __nv_bfloat16* vg = a.v + (int64_t)g * a.kv_sh;
+      for (int j = 0; j < nb; ++j) {
+        const int st = j % kStages;
+        if (j >= kStages) mbar_wait(&bars[5 + st], ((j / kStages) - 1) & 1);
+        int* pos = posbuf + st * 128;
+        for (int r = pt; r < 128; r += 96) {
+          const int e = j * kBlockN + r;
+          pos[r] = e < count ? __ldg(sel + e) : 0x7fffffff;
+        }
+        named_bar_sync(1, 96);
+        const uint32_t kdst = smem_u32(smem + kOffK + st * kTileBytes);
+        const uint32_t vdst = smem_u32(smem + kOffV + st * kTileBytes);
+        for (int c = pt; c < 128 * 16; c += 96) {
+          const int r = c >> 4, ch = c & 15;
+          const int p = pos[r];
+          const bool valid = p != 0x7fffffff;
+          const uint32_t off = (ch >> 3) * kHalf + r * 128 + (((ch & 7) ^ (r & 7)) << 4);
+          const int64_t src = (int64_t)(valid ? p : 0) * 128 + ch * 8;
+          cp_async16_zfill(kdst + off, kg + src, valid);
+          cp_async16_zfill(vdst + off, vg + src, valid);
+        }
+        cp_async_commit();
+        if (j > 0) {
+          cp_async_wait<1>();
+          fence_proxy_async_smem();
+          mbar_arrive(&bars[1 + (j - 1) % kStages]);
+          mbar_arrive(&bars[3 + (j - 1) % kStages]);
+        }
+      }
+      if (nb > 0) {
+        cp_async_wait<0>();
+        fence_proxy_async_smem();
+        mbar_arrive(&bars[1 + (nb - 1) % kStages]);
+        mbar_arrive(&bars[3 + (nb - 1) % kStages]);
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n");
+    // ================================================== softmax warpgroups
+    const int t = (warp - 4) >> 2;          // tile slot
+    const int q = warp & 3;                 // TMEM lane quarter
+    const int row_in_tile = q * 32 + lane;
+    const int row = r0 + row_in_tile;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    const uint32_t s_col = t * 256, o_col = t * 256 + 128;
+    if (t < nslots) {
+      const int h = h0 + t;
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < nb; ++j) {
+        mbar_wait(&bars[7 + t], j & 1);
+        tc_fence_after();
+        float s[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[32];
+          tmem_ld32(lane_base + s_col + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]) * a.scale_log2;
+        }
+        // masking: keys past the end / after the row (causal) / unselected
+        if (MODE == PMODE_SPARSE) {
+          const int* pos = posbuf + (j % kStages) * 128;
+#pragma unroll
+          for (int c = 0; c < 128; ++c) {
+            const int p = pos[c];
+            if (p > row) s[c] = -INFINITY;   // also pads (INT32_MAX)
+          }
+        } else {
+          const int k0 = j * kBlockN;
+          const int lim = a.causal ? min(row, a.N - 1) : a.N - 1;   // last visible key
+          if (k0 + kBlockN - 1 > lim) {
+#pragma unroll
+            for (int c = 0; c < 128; ++c)
+              if (k0 + c > lim) s[c] = -INFINITY;
+          }
+        }
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 128; ++c) mx = fmaxf(mx, s[c]);
+        if (mx > m_used + kRescaleThreshold) {
+          if (m_used != -INFINITY && MODE != PMODE_LSE) {
+            // O_t holds blocks < j (their PV completed before S_j was committed)
+            const float alpha = exp2f(m_used - mx);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint32_t r[32];
+              tmem_ld32(lane_base + o_col + c * 32, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+              tmem_st32(lane_base + o_col + c * 32, r);
+            }
+            l *= alpha;
+          } else if (m_used != -INFINITY) {
+            l *= exp2f(m_used - mx);
+          }
+          m_used = mx;
+        }
+        const float mu = m_used == -INFINITY ? 0.f : m_used;
+        float sum = 0.f;
+        if (MODE == PMODE_LSE) {
+#pragma unroll
+          for (int c = 0; c < 128; ++c) sum += fast_exp2(s[c] - mu);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t r[32];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float p0 = fast_exp2(s[c * 32 + 2 * i] - mu);
+              const float p1 = fast_exp2(s[c * 32 + 2 * i + 1] - mu);
+              sum += p0 + p1;
+              r[i] = pack_bf16(p0, p1);
+            }
+            // 16 packed columns: the key pairs of this 32-key chunk
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n"
+                ::"r"(lane_base + s_col + c * 16), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]),
+                "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]),
+                "r"(r[13]), "r"(r[14]), "r"(r[15])
+                : "memory");
+          }
+          tmem_st_wait();
+        }
+        l += sum;
+        tc_fence_before();
+        mbar_arrive(&bars[9 + t]);
+      }
+      // ---------------------------------------------------------- epilogue
+      const bool live = row < a.N;
+      if (MODE != PMODE_LSE && nb > 0) {
+        mbar_wait(&bars[11 + t], 0);
+        tc_fence_after();
+      }
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      if (MODE != PMODE_LSE) {
+        __nv_bfloat16* orow = a.out + ((int64_t)h * a.N + row) * 128;
+        const bool fallback = (MODE == PMODE_SPARSE) && l == 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[32];
+          if (nb > 0) {
+            tmem_ld32(lane_base + o_col + c * 32, r);
+            tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = 0u;
+          }
+          if (live) {
+            uint4 w[4];
+            uint32_t* wp = reinterpret_cast<uint32_t*>(w);
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              wp[i] = pack_bf16(__uint_as_float(r[2 * i]) * inv, __uint_as_float(r[2 * i + 1]) * inv);
+            if (fallback) {
+              // attention.py:248-252: no selected key visible -> V[g][row]
+              const uint4* vrow = reinterpret_cast<const uint4*>(a.v + (int64_t)g * a.kv_sh + (int64_t)row * 128 + c * 32);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) w[i] = __ldg(vrow + i);
+            }
+            uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dst[i] = w[i];
+          }
+        }
+      }
+      if (live && a.lse) a.lse[(int64_t)h * a.N + row] = l > 0.f ? (m_used + __log2f(l)) * kLn2 : -INFINITY;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// ------------------------------------------------------------------- host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// [heads][rows][128] bf16 with row stride 128 and head stride `head_stride`
+// elements, box {64, 128, 1}, 128B swizzle.
+bool make_prefill_map(CUtensorMap* m, const void* base, int heads, int rows, int64_t head_stride) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {128, (cuuint64_t)rows, (cuuint64_t)heads};
+  cuuint64_t strides[2] = {256, (cuuint64_t)head_stride * 2};
+  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int MODE>
+static cudaError_t launch_prefill_mode(const PrefillArgs& a, cudaStream_t st) {
+  PrefillTmaps tm;
+  if (!make_prefill_map(&tm.q, a.q, a.Hq, a.N, a.q_sh)) return cudaErrorInvalidValue;
+  if (!make_prefill_map(&tm.k, a.k, a.Hkv, a.Nk, a.kv_sh)) return cudaErrorInvalidValue;
+  if (!make_prefill_map(&tm.v, a.v, a.Hkv, a.Nk, a.kv_sh)) return cudaErrorInvalidValue;
+  static const cudaError_t attr = cudaFuncSetAttribute(prefill_attn_kernel<MODE>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, pf::kSmemBytes);
+  if (attr != cudaSuccess) return attr;
+  const int tiles = (a.N + pf::kTileM - 1) / pf::kTileM;
+  dim3 grid(tiles, a.Hq / a.slots);
+  prefill_attn_kernel<MODE><<<grid, pf::kThreads, pf::kSmemBytes, st>>>(tm, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prefill_attn(int mode, const PrefillArgs& a, cudaStream_t st) {
+  switch (mode) {
+    case PMODE_DENSE: return launch_prefill_mode<PMODE_DENSE>(a, st);
+    case PMODE_SPARSE: return launch_prefill_mode<PMODE_SPARSE>(a, st);
+    default: return launch_prefill_mode<PMODE_LSE>(a, st);
+  }
+}
+
+}  // namespace kscd

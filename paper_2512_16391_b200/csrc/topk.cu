@@ -94,8 +94,15 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
   __shared__ uint32_t scan_buf[33];
   __shared__ uint32_t sel_bin, sel_above;
   const int r = blockIdx.x, tid = threadIdx.x;
-  const int n = a.lens ? a.lens[r] : a.len;
-  const int k = a.ks ? a.ks[r] : a.k;
+  int n = a.lens ? a.lens[r] : a.len;
+  int k = a.ks ? a.ks[r] : a.k;
+  if (a.tile > 0) {
+    // k_budget (tiles.py:81-89) of the tile's causal bound, in the same fp64
+    n = min(a.len, a.tile * (r % a.T + 1));
+    long long kk = (long long)floor(a.fraction * (double)n);
+    kk = kk < a.k_min ? a.k_min : kk;
+    k = (int)(kk > n ? n : kk);
+  }
   const int take = n < k ? n : k;
   const float* vals = a.vals + (int64_t)r * a.val_stride;
   int* out = a.idx + (int64_t)r * a.k_cap;

@@ -101,7 +101,7 @@ class KascadeDecoder:
         return self.out
 
     # -------------------------------------------------------------- graphs
-    def capture(self, q, k_caches, v_caches, seq_len: int, dense: bool = False) -> torch.cuda.CUDAGraph:
+    def capture(self, q, k_caches, v_caches, seq_len: int, dense: bool = False) -> torch.cuda.CUDAGraph:  # noqa: D102
         """Capture one step (fixed buffers and seq_len) in a CUDA graph; replay
         with ``graph.replay()`` after writing new queries into ``q``."""
         fn = self.dense_step if dense else self.step
@@ -112,3 +112,66 @@ class KascadeDecoder:
             fn(q, k_caches, v_caches, seq_len)
         self._graphs[(seq_len, dense)] = g
         return g
+
+
+class KascadePrefill:
+    """Prefill executor over every layer of a plan (batch 1, tiles of 128
+    query rows -- the reference's prefill phase, tiles.py:137-144):
+
+      layer 0   dense attention (O, LSE) -> pass B pooled Top-k per tile
+      anchor l  pass A (LSE) -> pass B pooled Top-k -> sparse over own sets
+      reuse l   sparse over the latest anchor's sets routed by head_map[l]
+
+    ``dense_forward`` is the Top-k = 100% baseline over the same layers."""
+
+    def __init__(self, plan, num_layers: int, num_q_heads: int, num_kv_heads: int, seq_len: int, device=None):
+        validate_plan(plan, num_layers, num_kv_heads)
+        if plan.pooling != POOL_POST:
+            raise InvalidArgumentError("prefill engine implements post-softmax pooling (the paper's mode)")
+        if plan.tile_size != ops.TILE:
+            raise InvalidArgumentError(f"prefill engine tiles are {ops.TILE} rows (plan has {plan.tile_size})")
+        self.plan = plan
+        self.L, self.Hq, self.Hkv, self.N = num_layers, num_q_heads, num_kv_heads, seq_len
+        self.device = torch.device(device or "cuda")
+        self.kinds = layer_kinds(plan, num_layers)
+        self.all_heads = plan.mode == MODE_ALL_HEADS_POOLED
+        dev = self.device
+        T = (seq_len + ops.TILE - 1) // ops.TILE
+        rows = 1 if self.all_heads else num_kv_heads
+        kc = k_budget(plan.k_policy, seq_len)
+        self.head_maps: Dict[int, Optional[torch.Tensor]] = {}
+        for l, kind in enumerate(self.kinds):
+            if kind == KIND_REUSE:
+                m = [0] * num_kv_heads if self.all_heads else plan.head_maps[l].map
+                self.head_maps[l] = torch.tensor(m, dtype=torch.int32, device=dev)
+        self.shared_map = torch.zeros(num_kv_heads, dtype=torch.int32, device=dev) if self.all_heads else None
+        self.lse = torch.empty(num_q_heads, seq_len, dtype=torch.float32, device=dev)
+        self.pooled = torch.empty(rows, T, (seq_len + 3) // 4 * 4, dtype=torch.float32, device=dev)
+        self.indices = torch.empty(rows, T, kc, dtype=torch.int32, device=dev)
+        self.counts = torch.zeros(rows, T, dtype=torch.int32, device=dev)
+        self.out = torch.empty(num_layers, num_q_heads, seq_len, 128, dtype=torch.bfloat16, device=dev)
+
+    def forward(self, qs: Sequence[torch.Tensor], ks: Sequence[torch.Tensor], vs: Sequence[torch.Tensor],
+                layers: Optional[Sequence[int]] = None) -> torch.Tensor:
+        """qs/ks/vs: per-layer [Hq][N][128] / [Hkv][N][128] bf16.  Returns the
+        bf16 outputs [L][Hq][N][128]."""
+        pol = self.plan.k_policy
+        for l, kind in enumerate(self.kinds):
+            q, k, v = qs[l], ks[l], vs[l]
+            if kind == KIND_REUSE:
+                ops.sparse_prefill(q, k, v, self.indices, self.counts, self.head_maps[l], out=self.out[l])
+                continue
+            if kind == KIND_ANCHOR0:
+                ops.dense_prefill(q, k, v, out=self.out[l], lse=self.lse)
+            else:
+                ops.anchor_lse_prefill(q, k, lse=self.lse)
+            ops.select_prefill(q, k, self.lse, pol, indices=self.indices, counts=self.counts, pooled=self.pooled,
+                               all_heads=self.all_heads)
+            if kind == KIND_ANCHOR:
+                ops.sparse_prefill(q, k, v, self.indices, self.counts, self.shared_map, out=self.out[l])
+        return self.out
+
+    def dense_forward(self, qs, ks, vs) -> torch.Tensor:
+        for l in range(self.L):
+            ops.dense_prefill(qs[l], ks[l], vs[l], out=self.out[l], lse=self.lse)
+        return self.out

@@ -9,6 +9,19 @@ Decode (one query token per sequence; the reference's decode tile
     select_decode(scores, lse, n, policy, Hkv)     -> indices, counts
     topk(values, k)                                -> indices, counts
 
+Prefill (one layer, batch 1; tiles of 128 query rows, tiles.py:137-144):
+
+    dense_prefill(q, k, v)                         -> out, lse
+    anchor_lse_prefill(q, k)                       -> lse
+    select_prefill(q, k, lse, policy)              -> indices, counts
+    sparse_prefill(q, k, v, indices, counts, head_map) -> out, lse
+    anchor_prefill(q, k, v, policy, layer0=...)    -> out, lse, indices, counts
+    reuse_prefill(q, k, v, indices, counts, head_map) -> out
+
+Prefill layouts: q bf16 [Hq][N][128], k/v bf16 [Hkv][N][128] (rows
+contiguous, any head stride); out bf16 [Hq][N][128]; lse fp32 [Hq][N];
+indices int32 [Hkv][T][k_cap] (T = ceil(N/128)), counts int32 [Hkv][T].
+
 Layouts: q bf16 [B][Hq][128]; K/V caches bf16 [B][Hkv][n_cap][128] (any
 batch/head strides, rows contiguous); out fp32 [B][Hq][128]; lse fp32
 [B][Hq] (natural log); indices int32 [B][Hkv][k_cap] sorted ascending and
@@ -252,3 +265,128 @@ def reuse_decode(q, k_cache, v_cache, seq_len, indices, counts, head_map=None, *
 
 def default_scale() -> float:
     return 1.0 / math.sqrt(HEAD_DIM)
+
+
+# ------------------------------------------------------------------ prefill
+TILE = 128
+
+
+def _check_prefill_qkv(q, k, v):
+    for name, t in (("q", q), ("k", k), ("v", v)):
+        if t is None:
+            continue
+        _need_cuda(t, name)
+        if t.dtype != torch.bfloat16:
+            raise UnsupportedOperationError(f"{name} must be bf16, got {t.dtype}")
+        if t.dim() != 3 or t.shape[-1] != HEAD_DIM or t.stride(2) != 1 or t.stride(1) != HEAD_DIM \
+                or t.stride(0) % 8:
+            raise InvalidArgumentError(f"{name} must be [H][N][128] with contiguous rows")
+    Hq, N = q.shape[0], q.shape[1]
+    Hkv = k.shape[0]
+    if k.shape[1] != N or (v is not None and tuple(v.shape) != tuple(k.shape)):
+        raise InvalidArgumentError("q/k/v sequence lengths differ")
+    if v is not None and v.stride() != k.stride():
+        raise InvalidArgumentError("k and v must share strides")
+    if Hq % Hkv:
+        raise InvalidArgumentError(f"num_query_heads ({Hq}) must be divisible by num_kv_heads ({Hkv})")
+    return Hq, Hkv, N
+
+
+def _prefill_params(q, k, v, out, lse, causal, scale) -> _lib.PrefillParams:
+    Hq, Hkv, N = _check_prefill_qkv(q, k, v)
+    return _lib.PrefillParams(
+        num_q_heads=Hq, num_kv_heads=Hkv, head_dim=HEAD_DIM, seq_len=N, causal=1 if causal else 0,
+        q=q.data_ptr(), k=k.data_ptr(), v=(v if v is not None else k).data_ptr(),
+        q_stride_head=q.stride(0), kv_stride_head=k.stride(0), softmax_scale=float(scale or 0.0),
+        out=_ptr(out), lse=_ptr(lse), tile_size=TILE)
+
+
+def dense_prefill(q, k, v, *, causal: bool = True, out=None, lse=None, scale=None):
+    """Dense prefill attention of one layer (attention.py:106-144): bf16 O
+    and fp32 LSE per row; the Top-k = 100% baseline and anchor 0."""
+    Hq, N = q.shape[0], q.shape[1]
+    out = torch.empty(Hq, N, HEAD_DIM, dtype=torch.bfloat16, device=q.device) if out is None else out
+    lse = torch.empty(Hq, N, dtype=torch.float32, device=q.device) if lse is None else lse
+    _lib.call("kscd_dense_prefill", _prefill_params(q, k, v, out, lse, causal, scale), _stream())
+    return out, lse
+
+
+def anchor_lse_prefill(q, k, *, causal: bool = True, lse=None, scale=None):
+    """Anchor pass A: per-row LSE only (QK^T and the online softmax sums)."""
+    Hq, N = q.shape[0], q.shape[1]
+    lse = torch.empty(Hq, N, dtype=torch.float32, device=q.device) if lse is None else lse
+    _lib.call("kscd_anchor_lse_prefill", _prefill_params(q, k, None, None, lse, causal, scale), _stream())
+    return lse
+
+
+def prefill_k_cap(policy: KBudgetPolicy, N: int) -> int:
+    return k_budget(policy, N)
+
+
+def select_prefill(q, k, lse, policy: KBudgetPolicy, *, indices=None, counts=None, pooled=None,
+                   all_heads: bool = False, scale=None):
+    """Anchor selection of every (kv head, tile): pooled post-softmax weights
+    (pass B, runner.py:148-152) and the exact Top-k with k = k_budget(causal
+    bound) (runner.py:199-206).  all_heads -> one shared set per tile."""
+    Hq, Hkv, N = _check_prefill_qkv(q, k, None)
+    T = (N + TILE - 1) // TILE
+    rows = 1 if all_heads else Hkv
+    kc = prefill_k_cap(policy, N)
+    dev = q.device
+    if pooled is None:
+        pooled = torch.empty(rows, T, (N + 3) // 4 * 4, dtype=torch.float32, device=dev)
+    if indices is None:
+        indices = torch.empty(rows, T, kc, dtype=torch.int32, device=dev)
+    if counts is None:
+        counts = torch.empty(rows, T, dtype=torch.int32, device=dev)
+    p = _lib.SelectPrefillParams(
+        num_q_heads=Hq, num_kv_heads=Hkv, head_dim=HEAD_DIM, seq_len=N, q=q.data_ptr(), k=k.data_ptr(),
+        q_stride_head=q.stride(0), kv_stride_head=k.stride(0), softmax_scale=float(scale or 0.0),
+        lse=lse.data_ptr(), pooled=pooled.data_ptr(), pooled_stride=pooled.stride(1),
+        topk_fraction=float(policy.fraction), k_min=int(policy.k_min), all_heads=1 if all_heads else 0,
+        indices=indices.data_ptr(), counts=counts.data_ptr(), k_cap=indices.shape[-1], tile_size=TILE)
+    _lib.call("kscd_select_prefill", p, _stream())
+    return indices, counts
+
+
+def sparse_prefill(q, k, v, indices, counts, head_map=None, *, out=None, lse=None, scale=None):
+    """topk_attention over every prefill tile (attention.py:185-253) with the
+    selections routed through head_map (runner.py:210-225)."""
+    Hq, Hkv, N = _check_prefill_qkv(q, k, v)
+    T = (N + TILE - 1) // TILE
+    if indices.dtype != torch.int32 or indices.dim() != 3 or indices.shape[1] != T or not indices.is_contiguous() \
+            or counts.shape != indices.shape[:2] or not counts.is_contiguous():
+        raise InvalidArgumentError("indices must be int32 [Hsrc][T][k_cap], counts int32 [Hsrc][T]")
+    if head_map is not None and (head_map.dtype != torch.int32 or head_map.numel() != Hkv):
+        raise InvalidArgumentError("head_map must be int32 with one entry per kv head")
+    out = torch.empty(Hq, N, HEAD_DIM, dtype=torch.bfloat16, device=q.device) if out is None else out
+    p = _prefill_params(q, k, v, out, lse, True, scale)
+    p.indices, p.counts = indices.data_ptr(), counts.data_ptr()
+    p.k_cap, p.num_src_heads = indices.shape[2], indices.shape[0]
+    p.head_map = _ptr(head_map)
+    _lib.call("kscd_sparse_prefill", p, _stream())
+    return out, lse
+
+
+def anchor_prefill(q, k, v, policy: KBudgetPolicy, *, layer0: bool = False, out=None, lse=None,
+                   indices=None, counts=None, pooled=None, all_heads: bool = False):
+    """One anchor layer of a prefill: layer 0 runs dense attention and selects
+    from it (runner.py:250-262); other anchors run pass A (LSE), pass B +
+    Top-k, then attend sparsely over their own sets (runner.py:263-266)."""
+    Hq, N = q.shape[0], q.shape[1]
+    lse = torch.empty(Hq, N, dtype=torch.float32, device=q.device) if lse is None else lse
+    if layer0:
+        out, lse = dense_prefill(q, k, v, out=out, lse=lse)
+    else:
+        anchor_lse_prefill(q, k, lse=lse)
+    indices, counts = select_prefill(q, k, lse, policy, indices=indices, counts=counts, pooled=pooled,
+                                     all_heads=all_heads)
+    if not layer0:
+        hm = torch.zeros(k.shape[0], dtype=torch.int32, device=q.device) if all_heads else None
+        out, _ = sparse_prefill(q, k, v, indices, counts, hm, out=out)
+    return out, lse, indices, counts
+
+
+def reuse_prefill(q, k, v, indices, counts, head_map=None, *, out=None):
+    """One reuse layer of a prefill (runner.py:267-275)."""
+    return sparse_prefill(q, k, v, indices, counts, head_map, out=out)[0]
