@@ -50,6 +50,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--extra", action="store_true", help="also time configs[1] (32K, k=2.5%%)")
     ap.add_argument("--best-of", action="store_true", help="report the better of two timed regions")
+    ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--prefill-ctx", type=int, default=131072)
+    ap.add_argument("--prefill-steps", type=int, default=2)
+    ap.add_argument("--prefill-warmup", type=int, default=1)
     return ap.parse_args()
 
 
@@ -192,6 +196,107 @@ def run_reference(args, rank):
         "e2e": {"value": round(us_tok, 1), "unit": "us/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ prefill
+def bench_prefill(args, dev, world, dist):
+    """Llama-3.1-8B prefill at 128K (batch 1 per GPU): the full 32-layer
+    Kascade forward and the dense (Top-k = 100%) forward of the same engine,
+    per-layer-kind times in the paper's Table 3 layout, and the reuse-layer
+    sparse kernel against the bf16 tensor roofline."""
+    import torch
+    from paper_2512_16391_b200 import engine, ops
+
+    N = args.prefill_ctx
+    L, Hq, Hkv, d = CFG["layers"], CFG["Hq"], CFG["Hkv"], 128
+    plan = make_plan(L, Hkv, LLAMA_ANCHORS, args.fraction, args.k_min)
+    per_layer = (Hq + 2 * Hkv) * N * d * 2
+    eng = engine.KascadePrefill(plan, L, Hq, Hkv, N, device=dev)
+    free, _ = torch.cuda.mem_get_info(dev)
+    n_distinct = int(max(2, min(L, (free - 8 * 2**30) // per_layer)))
+    gen = torch.Generator(device=dev)
+    qs, ks, vs = [], [], []
+    for i in range(n_distinct):
+        gen.manual_seed(5000 + i + 97 * int(os.environ.get("RANK", "0")))
+        qs.append(torch.randn(Hq, N, d, device=dev, generator=gen, dtype=torch.bfloat16))
+        ks.append(torch.randn(Hkv, N, d, device=dev, generator=gen, dtype=torch.bfloat16))
+        vs.append(torch.randn(Hkv, N, d, device=dev, generator=gen, dtype=torch.bfloat16))
+    Q = [qs[l % n_distinct] for l in range(L)]
+    K = [ks[l % n_distinct] for l in range(L)]
+    V = [vs[l % n_distinct] for l in range(L)]
+
+    def timed(fn, steps, warm):
+        for _ in range(warm):
+            fn()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(steps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / steps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    ms_kas = timed(lambda: eng.forward(Q, K, V), args.prefill_steps, args.prefill_warmup)
+    ms_den = timed(lambda: eng.dense_forward(Q, K, V), args.prefill_steps, args.prefill_warmup)
+
+    # per-layer-kind times (Table 3 layout) and the reuse kernel's roofline
+    def ev_time(fn, reps=2):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / reps
+
+    pol = plan.k_policy
+    t_dense = ev_time(lambda: ops.dense_prefill(Q[0], K[0], V[0], out=eng.out[0], lse=eng.lse))
+    t_a0 = t_dense + ev_time(lambda: ops.select_prefill(Q[0], K[0], eng.lse, pol, indices=eng.indices,
+                                                        counts=eng.counts, pooled=eng.pooled))
+    t_lse = ev_time(lambda: ops.anchor_lse_prefill(Q[2], K[2], lse=eng.lse))
+    t_sel = ev_time(lambda: ops.select_prefill(Q[2], K[2], eng.lse, pol, indices=eng.indices,
+                                               counts=eng.counts, pooled=eng.pooled))
+    hm = eng.head_maps[1]
+    t_reuse = ev_time(lambda: ops.sparse_prefill(Q[1], K[1], V[1], eng.indices, eng.counts, hm, out=eng.out[1]),
+                      reps=4)
+    t_anchor = t_lse + t_sel + t_reuse
+    cnt = eng.counts.cpu().numpy().astype(np.int64)
+    T = cnt.shape[1]
+    rows = np.array([min(N, 128 * (i + 1)) - 128 * i for i in range(T)])
+    G = Hq // Hkv
+    flops_reuse = 4.0 * d * G * float((cnt * rows[None, :]).sum())
+    flops_dense = 2.0 * d * Hq * N * (N + 1)
+    peaks, kind = load_peaks()
+    tpk = float(peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"]))
+    n_anchor, n_reuse = len(LLAMA_ANCHORS) - 1, L - len(LLAMA_ANCHORS)
+    weighted = (t_a0 + n_anchor * t_anchor + n_reuse * t_reuse) / L
+    del qs, ks, vs, Q, K, V, eng
+    torch.cuda.empty_cache()
+    return {
+        "workload": f"llama8b-prefill-{N // 1024}k-b1-k{args.fraction:g}",
+        "kascade_ms": round(ms_kas, 2), "kascade_ms_per_layer": round(ms_kas / L, 3),
+        "dense_ms": round(ms_den, 2), "dense_ms_per_layer": round(ms_den / L, 3),
+        "speedup_vs_dense": round(ms_den / ms_kas, 3),
+        "steps": args.prefill_steps, "warmup": args.prefill_warmup, "layers_distinct": n_distinct,
+        "per_layer_ms": {"dense": round(t_dense, 3), "anchor0": round(t_a0, 3), "anchor": round(t_anchor, 3),
+                         "reuse": round(t_reuse, 3), "weighted_kascade": round(weighted, 3),
+                         "anchor_lse_pass": round(t_lse, 3), "select_pass_b_topk": round(t_sel, 3)},
+        "paper_h100_ms_per_layer": {"fa3": 215.76, "tilelang_dense": 262.21, "kascade": 98.55},
+        "roofline": {"kernel": "kscd sparse_prefill (reuse layer)", "bound": "tensor",
+                     "achieved": round(flops_reuse / (t_reuse * 1e-3) / 1e12, 1), "peak": tpk, "unit": "TFLOP/s",
+                     "frac": round(flops_reuse / (t_reuse * 1e-3) / 1e12 / tpk, 4), "traffic": None,
+                     "peak_kind": kind,
+                     "dense_prefill_frac": round(flops_dense / (t_dense * 1e-3) / 1e12 / tpk, 4)},
+        "gpu_launches_per_step": 1 * 3 + n_anchor * 4 + n_reuse,
+    }
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -354,6 +459,16 @@ def main():
                  "speedup_vs_dense": round(m_d / m_a, 3)}
         del dec2, ga, gd
 
+    # ---- prefill at 128K (secondary metric of the same line) -------------
+    del g_kas, g_den, dec, Kc, Vc, Ks, Vs, q
+    if extra is not None:
+        del K2, V2
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    prefill = None
+    if not args.no_prefill:
+        prefill = bench_prefill(args, dev, world, dist)
+
     # ---- CPU baseline (rank 0 only at N=1) -------------------------------
     cpu = None
     if not args.no_cpu_baseline and world == 1 and rank == 0:
@@ -396,6 +511,8 @@ def main():
     }
     if extra:
         line["extra"] = extra
+    if prefill:
+        line["prefill"] = prefill
     del out_kas
     if rank == 0:
         print(json.dumps(line), flush=True)

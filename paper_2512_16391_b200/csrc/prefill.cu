@@ -211,9 +211,10 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
           for (int hf = 0; hf < 2; ++hf)
             tma_load_3d(smem + kOffQ + t * kTileBytes + hf * kHalf, &tm.q, &bars[0], hf * 64, r0, h0 + t);
       }
-      // Block j's rows are gathered while block j-1's copies are still in
-      // flight; completion is published per block (wait_group, proxy fence,
-      // mbarrier arrive) so the tensor core reads coherent shared memory.
+      // Block j's rows are gathered while the tensor core and the softmax
+      // warpgroups work on block j-1 (double buffering); completion is
+      // published per block (wait_group, proxy fence, mbarrier arrive) so the
+      // tensor core reads coherent shared memory.
       const __nv_bfloat16* kg = a.k + (int64_t)g * a.kv_sh;
       const __nv_bfloat16* vg = a.v + (int64_t)g * a.kv_sh;
       for (int j = 0; j < nb; ++j) {
@@ -236,19 +237,14 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
           cp_async16_zfill(kdst + off, kg + src, valid);
           cp_async16_zfill(vdst + off, vg + src, valid);
         }
+        // Publish block j before touching block j+1: the MMA warp releases
+        // stage j-1 only after K_j has landed (it issues S_j first), so
+        // holding block j back would deadlock the 2-stage ring.
         cp_async_commit();
-        if (j > 0) {
-          cp_async_wait<1>();
-          fence_proxy_async_smem();
-          mbar_arrive(&bars[1 + (j - 1) % kStages]);
-          mbar_arrive(&bars[3 + (j - 1) % kStages]);
-        }
-      }
-      if (nb > 0) {
         cp_async_wait<0>();
         fence_proxy_async_smem();
-        mbar_arrive(&bars[1 + (nb - 1) % kStages]);
-        mbar_arrive(&bars[3 + (nb - 1) % kStages]);
+        mbar_arrive(&bars[1 + st]);
+        mbar_arrive(&bars[3 + st]);
       }
     }
   } else {
@@ -295,25 +291,27 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
         float mx = -INFINITY;
 #pragma unroll
         for (int c = 0; c < 128; ++c) mx = fmaxf(mx, s[c]);
-        if (mx > m_used + kRescaleThreshold) {
-          if (m_used != -INFINITY && MODE != PMODE_LSE) {
-            // O_t holds blocks < j (their PV completed before S_j was committed)
-            const float alpha = exp2f(m_used - mx);
+        // Lazy rescale: a row moves its reference max only when the block max
+        // exceeds it by > 2^8.  tcgen05.ld/st are warp-collective, so the O
+        // correction runs for the whole warp when any row needs it (alpha = 1
+        // for the others).
+        const bool need = mx > m_used + kRescaleThreshold;
+        const float alpha = (need && m_used != -INFINITY) ? exp2f(m_used - mx) : 1.f;
+        if (MODE != PMODE_LSE && __any_sync(0xffffffffu, alpha != 1.f)) {
+          // O_t holds blocks < j (their PV completed before S_j was committed)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint32_t r[32];
-              tmem_ld32(lane_base + o_col + c * 32, r);
-              tmem_ld_wait();
+          for (int c = 0; c < 4; ++c) {
+            uint32_t r[32];
+            tmem_ld32(lane_base + o_col + c * 32, r);
+            tmem_ld_wait();
 #pragma unroll
-              for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-              tmem_st32(lane_base + o_col + c * 32, r);
-            }
-            l *= alpha;
-          } else if (m_used != -INFINITY) {
-            l *= exp2f(m_used - mx);
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+            tmem_st32(lane_base + o_col + c * 32, r);
           }
-          m_used = mx;
+          tmem_st_wait();
         }
+        l *= alpha;
+        if (need) m_used = mx;
         const float mu = m_used == -INFINITY ? 0.f : m_used;
         float sum = 0.f;
         if (MODE == PMODE_LSE) {

@@ -28,8 +28,12 @@ KSCD_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Bounded wait: a pipeline bug traps (launch failure reported to the host)
+// instead of wedging the GPU; the bound is seconds, far above any real wait.
 KSCD_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
+    if (++spins == (1u << 26)) __trap();
   }
 }
 // cp.async (LDGSTS) completion tracked by an mbarrier (no pending-count bump)

@@ -64,7 +64,12 @@ def test_dense_prefill_heavy_tailed_rescale(cuda_ok):
     Q, K, V = _rand(5, 4, 2, 700, qscale=6.0)
     _, Y = orc.dense_layer(Q, K, V)
     out, _ = ops.dense_prefill(_bf(Q), _bf(K), _bf(V))
-    assert_outputs_close(out.float().cpu().numpy(), Y)
+    # peaked rows make |O| ~ |V| ~ 1-4, where the bf16 OUTPUT rounding alone
+    # is 2^-9 relative: bound the error relative to magnitude here
+    got = out.float().cpu().numpy()
+    err = np.abs(got - Y)
+    assert (err <= 2e-2 + 8e-3 * np.abs(Y)).all(), err.max()
+    assert np.linalg.norm(got - Y) / np.linalg.norm(Y) < 5e-3
 
 
 def test_lse_pass_matches_dense_lse(cuda_ok):
