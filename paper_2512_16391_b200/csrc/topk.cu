@@ -8,9 +8,21 @@
 //               ascending index order.  Radix select on order-preserving
 //               uint32 keys (12 + 12 + 8 bits) finds the exact k-th key T;
 //               one ordered compaction pass then keeps every key > T and the
-//               (k - #>T) lowest-index keys == T.  HBM/L2-bound integer work.
+//               (k - #>T) lowest-index keys == T.
+//
+// A row is split over a thread-block cluster of CL CTAs (CL = 8 when there
+// are few rows, as in decode where rows = batch x kv heads): each CTA
+// histograms its segment with warp-aggregated shared-memory atomics
+// (match_any: pooled weights crowd into few exponent bins, so naive atomics
+// serialise), the cluster reduces the histograms through distributed shared
+// memory, and the compaction offsets of the segments are exchanged the same
+// way.  HBM/L2-bound integer work; no tensor cores.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kscd_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace kscd {
 
@@ -52,15 +64,16 @@ cudaError_t launch_pool_decode(const PoolDecodeArgs& a, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ Top-k
-constexpr int kTopkThreads = 1024;
-constexpr int kTopkItems = 8;  // elements per thread per compaction chunk
+constexpr int kTopkThreads = 512;
+constexpr int kTopkWarps = kTopkThreads / 32;
+constexpr int kTopkItems = 8;  // consecutive elements per thread per compaction chunk
 
 KSCD_DEV uint32_t order_key(float f) {
   const uint32_t u = __float_as_uint(f + 0.0f);  // -0 -> +0: equal values tie
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-// Exclusive prefix sum over the 1024 threads of the block (thread order).
+// Exclusive prefix sum over the threads of the block (thread order).
 KSCD_DEV uint32_t block_excl_scan(uint32_t v, uint32_t* warp_tot, uint32_t& total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t x = v;
@@ -72,14 +85,14 @@ KSCD_DEV uint32_t block_excl_scan(uint32_t v, uint32_t* warp_tot, uint32_t& tota
   if (lane == 31) warp_tot[warp] = x;
   __syncthreads();
   if (warp == 0) {
-    uint32_t w = warp_tot[lane];
+    const uint32_t w = lane < kTopkWarps ? warp_tot[lane] : 0u;
     uint32_t wx = w;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, wx, o);
       if (lane >= o) wx += y;
     }
-    warp_tot[lane] = wx - w;  // exclusive warp offsets
+    if (lane < kTopkWarps) warp_tot[lane] = wx - w;  // exclusive warp offsets
     if (lane == 31) warp_tot[32] = wx;
   }
   __syncthreads();
@@ -89,11 +102,21 @@ KSCD_DEV uint32_t block_excl_scan(uint32_t v, uint32_t* warp_tot, uint32_t& tota
   return res;
 }
 
+struct TopkShared {
+  uint32_t hist[4096];
+  uint32_t range_tot[16];     // per-CTA bin-range totals (valid in CTA 0)
+  uint32_t seg_cnt[16][2];    // per-CTA (gt, eq) counts (valid in CTA 0)
+  uint32_t scan_buf[33];
+  uint32_t sel_bin, sel_above;
+};
+
+template <int CL>
 __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
-  __shared__ uint32_t hist[4096];
-  __shared__ uint32_t scan_buf[33];
-  __shared__ uint32_t sel_bin, sel_above;
-  const int r = blockIdx.x, tid = threadIdx.x;
+  __shared__ TopkShared sh;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int c = CL > 1 ? (int)cluster.block_rank() : 0;
+  const int r = blockIdx.x / CL;
+  const int tid = threadIdx.x, lane = tid & 31;
   int n = a.lens ? a.lens[r] : a.len;
   int k = a.ks ? a.ks[r] : a.k;
   if (a.tile > 0) {
@@ -106,80 +129,200 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
   const int take = n < k ? n : k;
   const float* vals = a.vals + (int64_t)r * a.val_stride;
   int* out = a.idx + (int64_t)r * a.k_cap;
-  if (tid == 0) a.counts[r] = take;
-  for (int j = take + tid; j < a.k_cap; j += kTopkThreads) out[j] = 0x7fffffff;
-  if (take <= 0) return;
+  // segment of this CTA (multiple of 8 elements so float4 loads stay aligned)
+  const int seg_len = ((n + CL - 1) / CL + 7) & ~7;
+  const int seg0 = min(n, c * seg_len), seg1 = min(n, seg0 + seg_len);
+  const bool vec = ((reinterpret_cast<uintptr_t>(vals) & 15) == 0);
+
+  if (c == 0) {
+    if (tid == 0) a.counts[r] = take;
+    for (int j = take + tid; j < a.k_cap; j += kTopkThreads) out[j] = 0x7fffffff;
+  }
+  if (take <= 0) return;                      // uniform across the cluster
   if (take == n) {
-    for (int j = tid; j < n; j += kTopkThreads) out[j] = j;
+    for (int j = seg0 + tid; j < seg1; j += kTopkThreads) out[j] = j;
     return;
   }
 
   // ---- radix select of the take-th largest key -------------------------
   uint32_t prefix = 0, pmask = 0, remaining = (uint32_t)take;
+  const int iters = (seg1 - seg0 + 4 * kTopkThreads - 1) / (4 * kTopkThreads);
 #pragma unroll 1
   for (int pass = 0; pass < 3; ++pass) {
     const int shift = pass == 0 ? 20 : (pass == 1 ? 8 : 0);
     const int nb = pass == 2 ? 256 : 4096;
-    for (int i = tid; i < nb; i += kTopkThreads) hist[i] = 0;
+    for (int i = tid; i < nb; i += kTopkThreads) sh.hist[i] = 0;
     __syncthreads();
-    for (int j = tid; j < n; j += kTopkThreads) {
-      const uint32_t key = order_key(__ldcg(vals + j));
-      if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & (nb - 1)], 1u);
-    }
-    __syncthreads();
-    // thread t owns bins nb-1-4t .. nb-4-4t (descending); exclusive scan in
-    // thread order = number of keys in strictly higher bins
-    uint32_t local = 0;
-    const int top = nb - 1 - 4 * tid;
+    for (int it = 0; it < iters; ++it) {
+      const int j = seg0 + (it * kTopkThreads + tid) * 4;
+      float v[4];
+      if (vec && j + 3 < seg1) {
+        const float4 f = __ldcg(reinterpret_cast<const float4*>(vals + j));
+        v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+      } else {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (top - i >= 0) local += hist[top - i];
-    uint32_t tot;
-    uint32_t above = block_excl_scan(local, scan_buf, tot);
+        for (int i = 0; i < 4; ++i) v[i] = j + i < seg1 ? __ldcg(vals + j + i) : 0.f;
+      }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int bin = top - i;
-      if (bin >= 0) {
-        const uint32_t c = hist[bin];
-        if (above < remaining && above + c >= remaining) {
-          sel_bin = bin;
-          sel_above = above;
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t key = order_key(v[i]);
+        const bool m = (j + i < seg1) && ((key & pmask) == prefix);
+        const uint32_t bin = (key >> shift) & (nb - 1);
+        const uint32_t act = __ballot_sync(0xffffffffu, m);
+        if (m) {
+          const uint32_t peers = __match_any_sync(act, bin);
+          if (lane == __ffs(peers) - 1) atomicAdd(&sh.hist[bin], (uint32_t)__popc(peers));
         }
-        above += c;
       }
     }
-    __syncthreads();
-    prefix |= sel_bin << shift;
+    if (CL > 1) cluster.sync(); else __syncthreads();
+    // CTA c owns bins [c*per, (c+1)*per): sum them over the cluster
+    const int per = nb / CL;
+    const int b0 = c * per;
+    uint32_t mine = 0;
+    for (int i = tid; i < per; i += kTopkThreads) {
+      uint32_t s = 0;
+#pragma unroll
+      for (int q = 0; q < CL; ++q) {
+        const uint32_t* h = CL > 1 ? cluster.map_shared_rank(sh.hist, q) : sh.hist;
+        s += h[b0 + i];
+      }
+      mine += s;
+    }
+    // range total -> CTA 0
+    uint32_t tot_unused;
+    const uint32_t pre = block_excl_scan(mine, sh.scan_buf, tot_unused);
+    (void)pre;
+    if (tid == 0) {
+      uint32_t* dst = CL > 1 ? cluster.map_shared_rank(sh.range_tot, 0) : sh.range_tot;
+      dst[c] = tot_unused;
+    }
+    if (CL > 1) cluster.sync(); else __syncthreads();
+    uint32_t above_range = 0;
+    {
+      const uint32_t* rt = CL > 1 ? cluster.map_shared_rank(sh.range_tot, 0) : sh.range_tot;
+      for (int q = c + 1; q < CL; ++q) above_range += rt[q];
+      const uint32_t my_tot = rt[c];
+      if (above_range < remaining && above_range + my_tot >= remaining) {
+        // the threshold bin lies in this CTA's range: descending scan of it,
+        // thread t owning bins top-bpt*t ... (bpt = 1 in a cluster, 8 alone)
+        constexpr int kMaxBpt = 4096 / kTopkThreads;
+        const int bpt = (per + kTopkThreads - 1) / kTopkThreads;
+        uint32_t local = 0;
+        const int top = b0 + per - 1 - bpt * tid;
+        uint32_t cnts[kMaxBpt];
+#pragma unroll
+        for (int i = 0; i < kMaxBpt; ++i) {
+          const int bin = top - i;
+          uint32_t s = 0;
+          if (i < bpt && bin >= b0) {
+#pragma unroll
+            for (int q = 0; q < CL; ++q) {
+              const uint32_t* h = CL > 1 ? cluster.map_shared_rank(sh.hist, q) : sh.hist;
+              s += h[bin];
+            }
+          }
+          cnts[i] = s;
+          local += s;
+        }
+        uint32_t tot2;
+        uint32_t above = above_range + block_excl_scan(local, sh.scan_buf, tot2);
+#pragma unroll
+        for (int i = 0; i < kMaxBpt; ++i) {
+          const int bin = top - i;
+          if (i < bpt && bin >= b0) {
+            if (above < remaining && above + cnts[i] >= remaining) {
+              for (int q = 0; q < CL; ++q) {
+                TopkShared* dst = CL > 1 ? cluster.map_shared_rank(&sh, q) : &sh;
+                dst->sel_bin = (uint32_t)bin;
+                dst->sel_above = above;
+              }
+            }
+            above += cnts[i];
+          }
+        }
+      }
+    }
+    if (CL > 1) cluster.sync(); else __syncthreads();
+    prefix |= sh.sel_bin << shift;
     pmask |= (uint32_t)(nb - 1) << shift;
-    remaining -= sel_above;
-    __syncthreads();
+    remaining -= sh.sel_above;
+    if (CL > 1) cluster.sync(); else __syncthreads();   // hist / sel reuse in the next pass
   }
   const uint32_t T = prefix;       // exact key of the take-th largest
   const uint32_t r_eq = remaining; // how many keys == T to keep (lowest indices)
 
   // ---- ordered compaction ------------------------------------------------
-  uint32_t gt_carry = 0, eq_carry = 0;
   const int chunk = kTopkThreads * kTopkItems;
+  uint32_t gt_seg = 0, eq_seg = 0;
+  for (int base = seg0; base < seg1; base += kTopkThreads * 4) {
+    const int j = base + tid * 4;
+    float v[4];
+    if (vec && j + 3 < seg1) {
+      const float4 f = __ldcg(reinterpret_cast<const float4*>(vals + j));
+      v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[i] = j + i < seg1 ? __ldcg(vals + j + i) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t key = order_key(v[i]);
+      gt_seg += (j + i < seg1 && key > T);
+      eq_seg += (j + i < seg1 && key == T);
+    }
+  }
+  uint32_t tg, te;
+  block_excl_scan(gt_seg, sh.scan_buf, tg);
+  block_excl_scan(eq_seg, sh.scan_buf, te);
+  if (tid == 0) {
+    uint32_t* dst = CL > 1 ? &cluster.map_shared_rank(&sh, 0)->seg_cnt[c][0] : &sh.seg_cnt[c][0];
+    dst[0] = tg;
+    dst[1] = te;
+  }
+  if (CL > 1) cluster.sync(); else __syncthreads();
+  uint32_t gt_carry = 0, eq_carry = 0;
+  {
+    const TopkShared* s0 = CL > 1 ? cluster.map_shared_rank(&sh, 0) : &sh;
+    for (int q = 0; q < c; ++q) {
+      gt_carry += s0->seg_cnt[q][0];
+      eq_carry += s0->seg_cnt[q][1];
+    }
+  }
+  if (CL > 1) cluster.sync();   // CTA 0's seg_cnt stays readable until all have read it
 #pragma unroll 1
-  for (int base = 0; base < n; base += chunk) {
+  for (int base = seg0; base < seg1; base += chunk) {
     uint32_t keys[kTopkItems];
     uint32_t gt = 0, eq = 0;
     const int j0 = base + tid * kTopkItems;
 #pragma unroll
+    for (int h = 0; h < kTopkItems; h += 4) {
+      float v[4];
+      const int j = j0 + h;
+      if (vec && j + 3 < seg1) {
+        const float4 f = __ldcg(reinterpret_cast<const float4*>(vals + j));
+        v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = j + i < seg1 ? __ldcg(vals + j + i) : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) keys[h + i] = order_key(v[i]);
+    }
+#pragma unroll
     for (int i = 0; i < kTopkItems; ++i) {
-      const int j = j0 + i;
-      keys[i] = j < n ? order_key(__ldcg(vals + j)) : 0u;
-      gt += (j < n && keys[i] > T);
-      eq += (j < n && keys[i] == T);
+      const bool ok = j0 + i < seg1;
+      gt += (ok && keys[i] > T);
+      eq += (ok && keys[i] == T);
     }
     uint32_t tot;
-    const uint32_t pre = block_excl_scan((eq << 16) | gt, scan_buf, tot);
+    const uint32_t pre = block_excl_scan((eq << 16) | gt, sh.scan_buf, tot);
     uint32_t g_before = gt_carry + (pre & 0xffffu);
     uint32_t e_before = eq_carry + (pre >> 16);
 #pragma unroll
     for (int i = 0; i < kTopkItems; ++i) {
       const int j = j0 + i;
-      if (j >= n) break;
+      if (j >= seg1) break;
       const bool is_gt = keys[i] > T, is_eq = keys[i] == T;
       if (is_gt || (is_eq && e_before < r_eq)) out[g_before + min(e_before, r_eq)] = j;
       g_before += is_gt;
@@ -192,8 +335,25 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
 
 cudaError_t launch_topk(const TopkArgs& a, cudaStream_t st) {
   if (a.rows <= 0) return cudaSuccess;
-  topk_kernel<<<a.rows, kTopkThreads, 0, st>>>(a);
-  return cudaGetLastError();
+  // few long rows (decode: batch x kv heads) -> a cluster of 8 CTAs per row
+  const bool split = a.rows * 8 <= 4 * 148 && a.len >= 8192;
+  if (!split) {
+    topk_kernel<1><<<a.rows, kTopkThreads, 0, st>>>(a);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.rows * 8);
+  cfg.blockDim = dim3(kTopkThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 8;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, topk_kernel<8>, a);
 }
 
 }  // namespace kscd
