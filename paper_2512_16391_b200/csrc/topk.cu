@@ -10,14 +10,15 @@
 //               one ordered compaction pass then keeps every key > T and the
 //               (k - #>T) lowest-index keys == T.
 //
-// A row is split over a thread-block cluster of CL CTAs (CL = 8 when there
+// A row is split over a thread-block cluster of CL CTAs (CL = 4 when there
 // are few rows, as in decode where rows = batch x kv heads): each CTA
-// histograms its segment with warp-aggregated shared-memory atomics
-// (match_any: pooled weights crowd into few exponent bins, so naive atomics
-// serialise), the cluster reduces the histograms through distributed shared
-// memory, and the compaction offsets of the segments are exchanged the same
-// way.  HBM/L2-bound integer work; no tensor cores.
+// histograms its segment with shared-memory atomics, the cluster reduces the
+// histograms through distributed shared memory, and the compaction offsets
+// of the segments are exchanged the same way.  HBM/L2-bound integer work; no
+// tensor cores.  The first radix pass is shared-atomic bound (~0.5 atomic /
+// clk / SM), which is why splitting a row across SMs pays.
 #include <cooperative_groups.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kscd_internal.h"
@@ -110,7 +111,7 @@ struct TopkShared {
   uint32_t sel_bin, sel_above;
 };
 
-template <int CL>
+template <int CL, int AGG>
 __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
   __shared__ TopkShared sh;
   cg::cluster_group cluster = cg::this_cluster();
@@ -168,10 +169,14 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
         const uint32_t key = order_key(v[i]);
         const bool m = (j + i < seg1) && ((key & pmask) == prefix);
         const uint32_t bin = (key >> shift) & (nb - 1);
-        const uint32_t act = __ballot_sync(0xffffffffu, m);
-        if (m) {
-          const uint32_t peers = __match_any_sync(act, bin);
-          if (lane == __ffs(peers) - 1) atomicAdd(&sh.hist[bin], (uint32_t)__popc(peers));
+        if (AGG) {
+          const uint32_t act = __ballot_sync(0xffffffffu, m);
+          if (m) {
+            const uint32_t peers = __match_any_sync(act, bin);
+            if (lane == __ffs(peers) - 1) atomicAdd(&sh.hist[bin], (uint32_t)__popc(peers));
+          }
+        } else if (m) {
+          atomicAdd(&sh.hist[bin], 1u);
         }
       }
     }
@@ -333,27 +338,45 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
   }
 }
 
-cudaError_t launch_topk(const TopkArgs& a, cudaStream_t st) {
-  if (a.rows <= 0) return cudaSuccess;
-  // few long rows (decode: batch x kv heads) -> a cluster of 8 CTAs per row
-  const bool split = a.rows * 8 <= 4 * 148 && a.len >= 8192;
-  if (!split) {
-    topk_kernel<1><<<a.rows, kTopkThreads, 0, st>>>(a);
+template <int CL, int AGG>
+static cudaError_t launch_topk_cl(const TopkArgs& a, cudaStream_t st) {
+  if (CL == 1) {
+    topk_kernel<1, AGG><<<a.rows, kTopkThreads, 0, st>>>(a);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(a.rows * 8);
+  cfg.gridDim = dim3(a.rows * CL);
   cfg.blockDim = dim3(kTopkThreads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 8;
+  attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, topk_kernel<8>, a);
+  return cudaLaunchKernelEx(&cfg, topk_kernel<CL, AGG>, a);
+}
+
+cudaError_t launch_topk(const TopkArgs& a, cudaStream_t st) {
+  if (a.rows <= 0) return cudaSuccess;
+  // KSCD_TOPK_VARIANT (dev knob): <cluster><agg>, e.g. "80", "81", "10", "11"
+  static const char* forced = getenv("KSCD_TOPK_VARIANT");
+  int cl = 1, agg = 0;
+  if (forced && forced[0]) {
+    cl = forced[0] == '8' ? 8 : (forced[0] == '4' ? 4 : (forced[0] == '2' ? 2 : 1));
+    agg = forced[1] == '1';
+  } else {
+    // Few long rows (decode: batch x kv heads) -> a cluster of 4 CTAs per row.
+    // Measured on B200 (64 rows x 128K): 1 CTA 141 us, 2: 83, 4: 65, 8: 85;
+    // match_any aggregation costs more than the atomics it saves.
+    cl = (a.rows * 4 <= 4 * 148 && a.len >= 8192) ? 4 : 1;
+  }
+  if (cl == 8) return agg ? launch_topk_cl<8, 1>(a, st) : launch_topk_cl<8, 0>(a, st);
+  if (cl == 4) return agg ? launch_topk_cl<4, 1>(a, st) : launch_topk_cl<4, 0>(a, st);
+  if (cl == 2) return agg ? launch_topk_cl<2, 1>(a, st) : launch_topk_cl<2, 0>(a, st);
+  return agg ? launch_topk_cl<1, 1>(a, st) : launch_topk_cl<1, 0>(a, st);
 }
 
 }  // namespace kscd
