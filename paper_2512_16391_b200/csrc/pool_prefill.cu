@@ -150,18 +150,35 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
         mbar_wait(&bars[5 + x], j & 1);
         tc_fence_after();
         const bool diag = (j == nb - 1);           // only the last block crosses the staircase
-        for (int c0 = 0; c0 < ncols; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld32(lane_base + c0, r);
+        const float2 sc2 = make_float2(a.scale_log2, a.scale_log2);
+        float2 acc2 = make_float2(0.f, 0.f);
+        for (int c0 = 0; c0 < ncols; c0 += 64) {
+          // two 32-column TMEM loads in flight per wait
+          uint32_t r[64];
+          tmem_ld32(lane_base + c0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          tmem_ld32(lane_base + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
           tmem_ld_wait();
+          const float4* l4 = reinterpret_cast<const float4*>(lse2 + 256 * x + c0);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int col = 256 * x + c0 + i;      // chunk row index (head*128 + row)
-            float e = fast_exp2(__uint_as_float(r[i]) * a.scale_log2 - lse2[col]);
-            if (diag && key > r0 + (col & 127)) e = 0.f;
-            acc += e;
+          for (int i = 0; i < 64; i += 4) {
+            const float4 lv = l4[i >> 2];          // broadcast read: same rows for every key
+            float2 e0 = __ffma2_rn(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sc2,
+                                   make_float2(-lv.x, -lv.y));
+            float2 e1 = __ffma2_rn(make_float2(__uint_as_float(r[i + 2]), __uint_as_float(r[i + 3])), sc2,
+                                   make_float2(-lv.z, -lv.w));
+            e0 = make_float2(fast_exp2(e0.x), fast_exp2(e0.y));
+            e1 = make_float2(fast_exp2(e1.x), fast_exp2(e1.y));
+            if (diag) {
+              const int rr = (c0 + i) & 127;       // row within the tile of column c0+i
+              if (key > r0 + rr) e0.x = 0.f;
+              if (key > r0 + rr + 1) e0.y = 0.f;
+              if (key > r0 + rr + 2) e1.x = 0.f;
+              if (key > r0 + rr + 3) e1.y = 0.f;
+            }
+            acc2 = __fadd2_rn(acc2, __fadd2_rn(e0, e1));
           }
         }
+        acc = acc2.x + acc2.y;
         tc_fence_before();
         mbar_arrive(&bars[7 + x]);
       }

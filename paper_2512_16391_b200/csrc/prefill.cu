@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;\n");
     // ================================================ producers / MMA
     if (warp == 3) {
       if (lane == 0 && nb > 0) {
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
       }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n");
     // ================================================== softmax warpgroups
     const int t = (warp - 4) >> 2;          // tile slot
     const int q = warp & 3;                 // TMEM lane quarter
@@ -262,22 +262,26 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
       for (int j = 0; j < nb; ++j) {
         mbar_wait(&bars[7 + t], j & 1);
         tc_fence_after();
+        // the whole 128-key row of S in one batch of TMEM loads, one wait
         float s[128];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t r[32];
-          tmem_ld32(lane_base + s_col + c * 32, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(r[i]) * a.scale_log2;
-        }
-        // masking: keys past the end / after the row (causal) / unselected
+        for (int c = 0; c < 4; ++c)
+          tmem_ld32(lane_base + s_col + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]));
+        tmem_ld_wait();
+        // masking on raw scores: keys past the end / after the row (causal) /
+        // unselected.  Sorted selections only reach the tile's own rows in
+        // their last block(s), so earlier blocks skip the per-key test.
         if (MODE == PMODE_SPARSE) {
           const int* pos = posbuf + (j % kStages) * 128;
+          if (pos[127] > r0) {
 #pragma unroll
-          for (int c = 0; c < 128; ++c) {
-            const int p = pos[c];
-            if (p > row) s[c] = -INFINITY;   // also pads (INT32_MAX)
+            for (int c = 0; c < 128; c += 4) {
+              const int4 p = *reinterpret_cast<const int4*>(pos + c);
+              if (p.x > row) s[c] = -INFINITY;   // also pads (INT32_MAX)
+              if (p.y > row) s[c + 1] = -INFINITY;
+              if (p.z > row) s[c + 2] = -INFINITY;
+              if (p.w > row) s[c + 3] = -INFINITY;
+            }
           }
         } else {
           const int k0 = j * kBlockN;
@@ -288,9 +292,10 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
               if (k0 + c > lim) s[c] = -INFINITY;
           }
         }
-        float mx = -INFINITY;
+        float mx_raw = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 128; ++c) mx = fmaxf(mx, s[c]);
+        for (int c = 0; c < 128; ++c) mx_raw = fmaxf(mx_raw, s[c]);
+        const float mx = mx_raw * a.scale_log2;   // scale > 0: max commutes
         // Lazy rescale: a row moves its reference max only when the block max
         // exceeds it by > 2^8.  tcgen05.ld/st are warp-collective, so the O
         // correction runs for the whole warp when any row needs it (alpha = 1
@@ -312,21 +317,27 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
         }
         l *= alpha;
         if (need) m_used = mx;
+        // p = exp2(s*scale*log2e - m): one packed FFMA2 per key pair + MUFU
         const float mu = m_used == -INFINITY ? 0.f : m_used;
-        float sum = 0.f;
+        const float2 sc2 = make_float2(a.scale_log2, a.scale_log2);
+        const float2 nm2 = make_float2(-mu, -mu);
+        float2 sum2 = make_float2(0.f, 0.f);
         if (MODE == PMODE_LSE) {
 #pragma unroll
-          for (int c = 0; c < 128; ++c) sum += fast_exp2(s[c] - mu);
+          for (int c = 0; c < 128; c += 2) {
+            const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sc2, nm2);
+            sum2 = __fadd2_rn(sum2, make_float2(fast_exp2(x.x), fast_exp2(x.y)));
+          }
         } else {
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            uint32_t r[32];
+            uint32_t r[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              const float p0 = fast_exp2(s[c * 32 + 2 * i] - mu);
-              const float p1 = fast_exp2(s[c * 32 + 2 * i + 1] - mu);
-              sum += p0 + p1;
-              r[i] = pack_bf16(p0, p1);
+              const float2 x = __ffma2_rn(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sc2, nm2);
+              const float2 p = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+              sum2 = __fadd2_rn(sum2, p);
+              r[i] = pack_bf16(p.x, p.y);
             }
             // 16 packed columns: the key pairs of this 32-key chunk
             asm volatile(
@@ -338,7 +349,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
           }
           tmem_st_wait();
         }
-        l += sum;
+        l += sum2.x + sum2.y;
         tc_fence_before();
         mbar_arrive(&bars[9 + t]);
       }
@@ -352,16 +363,19 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
       if (MODE != PMODE_LSE) {
         __nv_bfloat16* orow = a.out + ((int64_t)h * a.N + row) * 128;
         const bool fallback = (MODE == PMODE_SPARSE) && l == 0.f;
+        uint32_t o[128];
+        if (nb > 0) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            tmem_ld32(lane_base + o_col + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 128; ++i) o[i] = 0u;
+        }
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          uint32_t r[32];
-          if (nb > 0) {
-            tmem_ld32(lane_base + o_col + c * 32, r);
-            tmem_ld_wait();
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = 0u;
-          }
+          const uint32_t* r = o + c * 32;
           if (live) {
             uint4 w[4];
             uint32_t* wp = reinterpret_cast<uint32_t*>(w);
