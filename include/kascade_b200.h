@@ -150,6 +150,33 @@ typedef struct kscd_select_prefill_params {
   int32_t tile_size;       /* must be 128 */
 } kscd_select_prefill_params;
 
+/* Reference-scale helpers for the trace-level API (small N only). */
+typedef struct kscd_probs_params {
+  int32_t num_q_heads, num_kv_heads, head_dim, seq_len, causal;
+  const void* q;           /* bf16 [Hq][N][128] */
+  const void* k;           /* bf16 [Hkv][N][128] */
+  int64_t q_stride_head, kv_stride_head;
+  float softmax_scale;     /* <= 0 selects 1/sqrt(head_dim) */
+  const float* lse;        /* fp32 [Hq][N] from kscd_dense_prefill */
+  float* probs;            /* fp32 [Hq][N][N] */
+} kscd_probs_params;
+
+typedef struct kscd_pool_tiles_params {
+  int32_t num_q_heads, num_kv_heads, head_dim, seq_len;
+  int32_t num_tiles;
+  const int32_t* tile_starts;   /* device [T]: rows [start, end) of each tile, end = causal bound */
+  const int32_t* tile_ends;
+  int32_t pooling;              /* 0 post-softmax (needs probs), 1 pre-softmax (needs q, k) */
+  int32_t all_heads;            /* post only: pool every query head into one row per tile */
+  const float* probs;           /* fp32 [Hq][N][N] */
+  const void* q;
+  const void* k;
+  int64_t q_stride_head, kv_stride_head;
+  float* pooled;                /* fp32 [Hkv or 1][T][pooled_stride] */
+  int64_t pooled_stride;
+  double* scratch;              /* pre: fp64 [Hkv][T][pooled_stride] */
+} kscd_pool_tiles_params;
+
 int kscd_abi_version(void);
 const char* kscd_last_error(void);
 
@@ -193,6 +220,15 @@ int kscd_sparse_prefill(const kscd_prefill_params* p, void* stream);
 
 /* Anchor selection for prefill (runner.py:164-207). */
 int kscd_select_prefill(const kscd_select_prefill_params* p, void* stream);
+
+/* dense_attention's materialised P (attention.py:121-142) for small N:
+ * exp(s - lse) on visible entries, exact zeros elsewhere. */
+int kscd_dense_probs(const kscd_probs_params* p, void* stream);
+
+/* Pooled distributions of arbitrary tiles (any TileSpec, tiles.py:117-152):
+ * post-softmax _post_pooled (runner.py:148-152, fp64 sums) or pre-softmax
+ * _pre_pooled (runner.py:155-161). */
+int kscd_pool_tiles(const kscd_pool_tiles_params* p, void* stream);
 
 /* k_budget (tiles.py:81-89): min(max(floor(fraction*n), k_min), n). */
 int32_t kscd_k_budget(double fraction, int32_t k_min, int32_t n);

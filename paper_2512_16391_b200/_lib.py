@@ -78,6 +78,23 @@ class SelectPrefillParams(ctypes.Structure):
     ]
 
 
+class ProbsParams(ctypes.Structure):
+    _fields_ = [
+        ("num_q_heads", c_i32), ("num_kv_heads", c_i32), ("head_dim", c_i32), ("seq_len", c_i32),
+        ("causal", c_i32), ("q", c_vp), ("k", c_vp), ("q_stride_head", c_i64), ("kv_stride_head", c_i64),
+        ("softmax_scale", c_f32), ("lse", c_vp), ("probs", c_vp),
+    ]
+
+
+class PoolTilesParams(ctypes.Structure):
+    _fields_ = [
+        ("num_q_heads", c_i32), ("num_kv_heads", c_i32), ("head_dim", c_i32), ("seq_len", c_i32),
+        ("num_tiles", c_i32), ("tile_starts", c_vp), ("tile_ends", c_vp), ("pooling", c_i32),
+        ("all_heads", c_i32), ("probs", c_vp), ("q", c_vp), ("k", c_vp), ("q_stride_head", c_i64),
+        ("kv_stride_head", c_i64), ("pooled", c_vp), ("pooled_stride", c_i64), ("scratch", c_vp),
+    ]
+
+
 # entry point name -> params struct (None for non-struct signatures)
 ENTRY_POINTS = {
     "kscd_dense_decode": DecodeParams,
@@ -89,6 +106,8 @@ ENTRY_POINTS = {
     "kscd_anchor_lse_prefill": PrefillParams,
     "kscd_sparse_prefill": PrefillParams,
     "kscd_select_prefill": SelectPrefillParams,
+    "kscd_dense_probs": ProbsParams,
+    "kscd_pool_tiles": PoolTilesParams,
 }
 
 _lock = threading.Lock()

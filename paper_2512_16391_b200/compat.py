@@ -1,0 +1,369 @@
+"""The reference's trace-level API, executed by the B200 kernels.
+
+Same names, arguments, results and errors as ``kascade`` 0.1.0 so a caller
+can switch imports:
+
+    dense_attention(trace, layer, causal=True) -> (P, Y)      attention.py:106-144
+    oracle_topk_indices(p, k, kv_head=0, tile_id=0)          attention.py:147-174
+    topk_attention(trace, layer, selections, tiles, causal=True, dense_P=None)
+                                                              attention.py:185-253
+    run_dense(trace)                                          runner.py:132-137
+    run_kascade(trace, plan, phase="prefill") -> (outputs, RunReport)
+                                                              runner.py:228-297
+    compare(a, b) -> RunReport                                runner.py:321-344
+    softmax_row(scores)                                       attention.py:77-90
+
+Inputs are the reference's fp32 numpy traces; the engine computes in bf16
+(Q/K/V are rounded to bf16 on upload -- parity inputs are bf16-representable,
+SURVEY.md 8(c)) and returns fp32 numpy.  Prefill with 128-row tiles and
+post-softmax pooling runs the performance kernels (tcgen05 prefill, pass-B
+pooling, per-tile Top-k); any other TileSpec (decode phase, other tile
+sizes, pre-softmax pooling) runs reference-scale kernels: materialised P,
+pooled tile rows, and the decode sparse kernel with one query row per
+"sequence".  ``mass_recovered`` is exp(LSE_sparse - LSE_dense), which equals
+the reference's sum of dense P over the visible selected keys.
+"""
+
+from __future__ import annotations
+
+import math
+from typing import Dict, List, Mapping, Sequence, Tuple, Union
+
+import numpy as np
+import torch
+
+from . import _lib, ops
+from .exceptions import InvalidArgumentError, InvalidPlanError, NumericError, UnsupportedOperationError
+from .host_types import (DECODE, KIND_ANCHOR, KIND_ANCHOR0, KIND_REUSE, MODE_ALL_HEADS_POOLED, MODE_REMAPPED,
+                         POOL_POST, POOL_PRE, PREFILL, LayerReport, RunReport, TileSpec, TopkAttentionResult,
+                         TopKIndexSet, k_budget, make_tiles, validate_plan)
+
+MAX_P_SEQ = 8192        # materialised P is [Hq][N][N] fp32, like the reference
+
+
+def _dev():
+    if not torch.cuda.is_available():
+        raise UnsupportedOperationError("the B200 engine needs a CUDA device (there is no CPU path)")
+    return torch.device("cuda")
+
+
+def _layer(trace, layer: int):
+    if not 0 <= layer < trace.num_layers:
+        raise InvalidArgumentError(f"layer {layer} out of range [0, {trace.num_layers})")
+    if trace.head_dim != 128:
+        raise UnsupportedOperationError(f"head_dim {trace.head_dim} unsupported (engine is d=128)")
+    dev = _dev()
+    to = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev).to(torch.bfloat16)  # noqa
+    return to(trace.Q[layer]), to(trace.K[layer]), to(trace.V[layer])
+
+
+def _check_finite(Y: torch.Tensor, layer: int):
+    bad = ~torch.isfinite(Y).all(dim=-1)          # [Hq][N]
+    if bool(bad.any()):
+        h, r = (int(x) for x in torch.nonzero(bad)[0])
+        raise NumericError("non-finite attention intermediate", layer=layer, head=h, row=r)
+
+
+def _probs(q, k, lse, causal: bool) -> torch.Tensor:
+    Hq, N = q.shape[0], q.shape[1]
+    if N > MAX_P_SEQ:
+        raise UnsupportedOperationError(f"materialised P needs N <= {MAX_P_SEQ} (got {N})")
+    P = torch.empty(Hq, N, N, dtype=torch.float32, device=q.device)
+    p = _lib.ProbsParams(num_q_heads=Hq, num_kv_heads=k.shape[0], head_dim=128, seq_len=N,
+                         causal=1 if causal else 0, q=q.data_ptr(), k=k.data_ptr(), q_stride_head=q.stride(0),
+                         kv_stride_head=k.stride(0), lse=lse.data_ptr(), probs=P.data_ptr())
+    _lib.call("kscd_dense_probs", p, ops._stream())
+    return P
+
+
+def dense_attention(trace, layer: int, causal: bool = True) -> Tuple[np.ndarray, np.ndarray]:
+    """(P [Hq][N][N], Y [Hq][N][d]) of one layer; P is materialised only
+    because the reference returns it (N <= MAX_P_SEQ)."""
+    q, k, v = _layer(trace, layer)
+    out, lse = ops.dense_prefill(q, k, v, causal=causal)
+    Y = out.float()
+    _check_finite(Y, layer)
+    P = _probs(q, k, lse, causal)
+    return P.cpu().numpy(), Y.cpu().numpy()
+
+
+def softmax_row(scores) -> np.ndarray:
+    """attention.py:77-90: fp64 softmax of one score vector, fp32 result."""
+    s = np.asarray(scores)
+    if s.ndim != 1 or s.size == 0:
+        raise InvalidArgumentError("scores must be a non-empty vector")
+    if not np.isfinite(s).all():
+        raise InvalidArgumentError("scores must be finite")
+    t = torch.from_numpy(s.astype(np.float64)).to(_dev())
+    return torch.softmax(t, dim=0).to(torch.float32).cpu().numpy()
+
+
+def oracle_topk_indices(p, k: int, kv_head: int = 0, tile_id: int = 0) -> TopKIndexSet:
+    """The k largest weights, ties to the smaller position, ascending (the
+    exact radix-select kernel)."""
+    if k < 1:
+        raise InvalidArgumentError(f"k must be >= 1, got {k}")
+    positions = None
+    if hasattr(p, "weights") and hasattr(p, "key_positions"):
+        weights = np.asarray(p.weights)
+        positions = np.asarray(p.key_positions, dtype=np.int64)
+    else:
+        weights = np.asarray(p)
+    if weights.ndim != 1 or weights.size == 0:
+        raise InvalidArgumentError("p must be a non-empty vector")
+    vals = torch.from_numpy(weights.astype(np.float32)).to(_dev())[None]
+    idx, cnt = ops.topk(vals, int(k))
+    sel = idx[0, :int(cnt.item())].cpu().numpy().astype(np.int64)
+    if positions is not None:
+        sel = positions[sel]
+    return TopKIndexSet(kv_head=kv_head, tile_id=tile_id, indices=sel, k=k)
+
+
+def _sel_map(selections) -> Dict[Tuple[int, int], np.ndarray]:
+    if isinstance(selections, Mapping):
+        items = selections.items()
+    else:
+        items = (((s.kv_head, s.tile_id), s) for s in selections)
+    return {key: np.asarray(getattr(s, "indices", s), dtype=np.int64) for key, s in items}
+
+
+def _standard_prefill(tiles, N: int, Hkv: int) -> bool:
+    if tiles.phase != PREFILL or tiles.tile_size != ops.TILE:
+        return False
+    want = make_tiles(N, PREFILL, Hkv, Hkv, ops.TILE).tiles
+    return sorted((t.kv_head, t.tile_id, t.start, t.end) for t in tiles.tiles) == \
+        sorted((t.kv_head, t.tile_id, t.start, t.end) for t in want)
+
+
+def _sparse_any_tiles(q, k, v, tiles, sels, causal: bool):
+    """Sparse attention for an arbitrary TileSpec: every query row is one
+    'sequence' of the decode sparse kernel whose list is its tile's selection
+    truncated to the keys <= row (the staircase), K/V shared (batch stride 0).
+    Returns (Y [Hq][N][d] fp32, lse [Hq][N], vis [Hkv][N])."""
+    Hq, N = q.shape[0], q.shape[1]
+    Hkv = k.shape[0]
+    dev = q.device
+    kc = max(1, max((s.size for s in sels.values()), default=1))
+    idx = np.full((N, Hkv, kc), 2**31 - 1, np.int32)
+    vis = np.zeros((N, Hkv), np.int32)
+    for t in tiles.tiles:
+        sel = sels[(t.kv_head, t.tile_id)]
+        rows = np.arange(t.start, t.end)
+        idx[t.start:t.end, t.kv_head, :sel.size] = sel
+        vis[t.start:t.end, t.kv_head] = np.searchsorted(sel, rows, side="right") if causal else sel.size
+    q_rows = q.permute(1, 0, 2).contiguous()
+    kx = k.unsqueeze(0).expand(N, Hkv, N, 128)
+    vx = v.unsqueeze(0).expand(N, Hkv, N, 128)
+    lse = torch.empty(N, Hq, dtype=torch.float32, device=dev)
+    out = ops.sparse_decode(q_rows, kx, vx, N, torch.from_numpy(idx).to(dev), torch.from_numpy(vis).to(dev),
+                            None, lse=lse)
+    return out.permute(1, 0, 2).contiguous(), lse.t().contiguous(), vis.T
+
+
+def topk_attention(trace, layer: int, selections, tiles, causal: bool = True, dense_P=None) -> TopkAttentionResult:
+    """Sparse attention over per-(kv head, tile) selections; softmax
+    renormalised over the selected keys, row r sees the selected keys <= r,
+    rows with none fall back to V[g][r] and are flagged."""
+    sels = _sel_map(selections)
+    N, Hq, Hkv = trace.seq_len, trace.num_query_heads, trace.num_kv_heads
+    G = Hq // Hkv
+    for t in tiles.tiles:
+        key = (t.kv_head, t.tile_id)
+        if key not in sels:
+            raise InvalidArgumentError(f"no Top-k set for kv head {t.kv_head}, tile {t.tile_id}")
+        sel = sels[key]
+        if causal and sel.size and sel[-1] >= t.causal_bound:
+            raise InvalidArgumentError(f"selection for kv head {t.kv_head}, tile {t.tile_id} breaks the tile's "
+                                       f"causal bound {t.causal_bound}")
+    q, k, v = _layer(trace, layer)
+    dev = q.device
+    _, lse_d = ops.dense_prefill(q, k, v, causal=causal)
+    if causal and _standard_prefill(tiles, N, Hkv):
+        T = (N + ops.TILE - 1) // ops.TILE
+        kc = max(1, max(s.size for s in sels.values()))
+        idx = np.full((Hkv, T, kc), 2**31 - 1, np.int32)
+        cnt = np.zeros((Hkv, T), np.int32)
+        for (g, tid), sel in sels.items():
+            if g < Hkv and tid < T:
+                idx[g, tid, :sel.size] = sel
+                cnt[g, tid] = sel.size
+        lse_s = torch.empty(Hq, N, dtype=torch.float32, device=dev)
+        out, _ = ops.sparse_prefill(q, k, v, torch.from_numpy(idx).to(dev), torch.from_numpy(cnt).to(dev),
+                                    lse=lse_s)
+        Y = out.float()
+        rows = torch.arange(N, device=dev)
+        vis_np = np.zeros((Hkv, N), np.int64)
+        for t in tiles.tiles:
+            sel = sels[(t.kv_head, t.tile_id)]
+            vis_np[t.kv_head, t.start:t.end] = np.searchsorted(sel, np.arange(t.start, t.end), side="right")
+        del rows
+    else:
+        Y, lse_s, vis_np = _sparse_any_tiles(q, k, v, tiles, sels, causal)
+        # rows with no visible selected key: the diagonal fallback V[g][r]
+        dead = torch.from_numpy(vis_np == 0).to(dev)                     # [Hkv][N]
+        if bool(dead.any()):
+            dead_h = dead.repeat_interleave(G, dim=0)                    # [Hq][N]
+            vrows = v.float().repeat_interleave(G, dim=0)                # [Hq][N][d]
+            Y = torch.where(dead_h[..., None], vrows, Y)
+    mass = torch.exp(lse_s - lse_d)
+    mass = torch.where(torch.isfinite(lse_s), mass, torch.zeros_like(mass))
+    fallback: List[Tuple[int, int]] = []
+    for t in tiles.tiles:
+        rows = np.arange(t.start, t.end)
+        dead_rows = rows[vis_np[t.kv_head, t.start:t.end] == 0]
+        for h in range(t.kv_head * G, (t.kv_head + 1) * G):
+            fallback.extend((h, int(r)) for r in dead_rows)
+    return TopkAttentionResult(Y=Y.cpu().numpy(), mass_recovered=mass.float().cpu().numpy(), fallback_rows=fallback)
+
+
+def run_dense(trace) -> np.ndarray:
+    """Dense outputs of every layer: [L][Hq][N][d] fp32."""
+    outs = []
+    for layer in range(trace.num_layers):
+        q, k, v = _layer(trace, layer)
+        out, _ = ops.dense_prefill(q, k, v)
+        outs.append(out.float())
+    return torch.stack(outs).cpu().numpy()
+
+
+def _rel_l2(a: torch.Tensor, b: torch.Tensor) -> float:
+    num = torch.linalg.vector_norm((a.double() - b.double()).flatten()).item()
+    den = torch.linalg.vector_norm(b.double().flatten()).item()
+    if den == 0.0:
+        return 0.0 if num == 0.0 else float("inf")
+    return float(num / den)
+
+
+def _select_any_tiles(q, k, lse, tiles, plan, Hkv: int) -> Dict[Tuple[int, int], np.ndarray]:
+    """_anchor_selections (runner.py:164-207) for an arbitrary TileSpec via
+    materialised P (post) or the pre-softmax pooled rows."""
+    dev = q.device
+    Hq, N = q.shape[0], q.shape[1]
+    by_head: Dict[int, List] = {}
+    for t in tiles.tiles:
+        by_head.setdefault(t.kv_head, []).append(t)
+    tiles0 = sorted(by_head[0], key=lambda t: t.tile_id)
+    T = len(tiles0)
+    starts = torch.tensor([t.start for t in tiles0], dtype=torch.int32, device=dev)
+    ends = torch.tensor([t.end for t in tiles0], dtype=torch.int32, device=dev)
+    all_heads = plan.mode == MODE_ALL_HEADS_POOLED
+    stride = (N + 3) // 4 * 4
+    pre = plan.pooling == POOL_PRE
+    rows = Hkv
+    pooled = torch.zeros(rows, T, stride, dtype=torch.float32, device=dev)
+    pp = _lib.PoolTilesParams(num_q_heads=Hq, num_kv_heads=Hkv, head_dim=128, seq_len=N, num_tiles=T,
+                              tile_starts=starts.data_ptr(), tile_ends=ends.data_ptr(), pooling=1 if pre else 0,
+                              all_heads=0, q=q.data_ptr(), k=k.data_ptr(), q_stride_head=q.stride(0),
+                              kv_stride_head=k.stride(0), pooled=pooled.data_ptr(), pooled_stride=stride)
+    if pre:
+        scratch = torch.empty(Hkv, T, stride, dtype=torch.float64, device=dev)
+        pp.scratch = scratch.data_ptr()
+    else:
+        P = _probs(q, k, lse, True)
+        pp.probs = P.data_ptr()
+    _lib.call("kscd_pool_tiles", pp, ops._stream())
+    if all_heads:
+        # runner.py:188-196: np.mean over kv heads of the pooled vectors
+        pooled = pooled.double().mean(dim=0, keepdim=True).float()
+    lens = ends.long()
+    ks = torch.tensor([k_budget(plan.k_policy, t.end) for t in tiles0], dtype=torch.int32, device=dev)
+    nrow = pooled.shape[0]
+    idx, cnt = ops.topk(pooled.reshape(nrow * T, stride), ks.repeat(nrow),
+                        lengths=lens.to(torch.int32).repeat(nrow), k_cap=int(ks.max().item()))
+    idx, cnt = idx.cpu().numpy(), cnt.cpu().numpy()
+    out = {}
+    for g in range(Hkv):
+        r = 0 if all_heads else g
+        for i, t in enumerate(tiles0):
+            out[(g, t.tile_id)] = idx[r * T + i, :cnt[r * T + i]].astype(np.int64)
+    return out
+
+
+def run_kascade(trace, plan, phase: str = PREFILL) -> Tuple[np.ndarray, RunReport]:
+    """The anchor/reuse pipeline with the reference's report (runner.py:228-318):
+    layer 0 dense (+ selections), anchors select fresh sets and attend
+    sparsely, reuse layers route the latest anchor's sets through their head
+    map.  Fidelity (rel-L2 vs dense, recovered mass, fallback rows) per layer."""
+    try:
+        validate_plan(plan, trace)
+    except InvalidArgumentError as e:
+        raise InvalidPlanError(str(e)) from None
+    L, Hq, Hkv, N = trace.num_layers, trace.num_query_heads, trace.num_kv_heads, trace.seq_len
+    G = Hq // Hkv
+    tiles = make_tiles(N, phase, Hq, Hkv, plan.tile_size)
+    fast = phase == PREFILL and plan.tile_size == ops.TILE and plan.pooling == POOL_POST
+    anchors = set(plan.core.anchors)
+    outputs = np.empty((L, Hq, N, trace.head_dim), np.float32)
+    reports: List[LayerReport] = []
+    cur = None               # fast path: (idx, cnt) device tensors; else dict of sets
+    for layer in range(L):
+        q, k, v = _layer(trace, layer)
+        out_d, lse_d = ops.dense_prefill(q, k, v)
+        Yd = out_d.float()
+        _check_finite(Yd, layer)
+        is_anchor = layer == 0 or layer in anchors
+        if is_anchor:
+            if fast:
+                cur = ops.select_prefill(q, k, lse_d, plan.k_policy, all_heads=plan.mode == MODE_ALL_HEADS_POOLED)
+            else:
+                cur = _select_any_tiles(q, k, lse_d, tiles, plan, Hkv)
+        if layer == 0:
+            outputs[0] = Yd.cpu().numpy()
+            reports.append(LayerReport(0, KIND_ANCHOR0, 0.0, 1.0))
+            continue
+        kind = KIND_ANCHOR if layer in anchors else KIND_REUSE
+        if fast:
+            idx, cnt = cur
+            if plan.mode == MODE_ALL_HEADS_POOLED:
+                hmap = torch.zeros(Hkv, dtype=torch.int32, device=q.device)
+            elif kind == KIND_REUSE:
+                hmap = torch.tensor(plan.head_maps[layer].map, dtype=torch.int32, device=q.device)
+            else:
+                hmap = None
+            lse_s = torch.empty(Hq, N, dtype=torch.float32, device=q.device)
+            out, _ = ops.sparse_prefill(q, k, v, idx, cnt, hmap, lse=lse_s)
+            Y = out.float()
+            fb = int((~torch.isfinite(lse_s)).sum().item())
+        else:
+            if kind == KIND_REUSE and plan.mode == MODE_REMAPPED:
+                hm = plan.head_maps[layer].map
+                sels = {(g, tid): cur[(hm[g], tid)] for (g, tid) in cur}
+            else:
+                sels = cur
+            Y, lse_s, vis = _sparse_any_tiles(q, k, v, tiles, sels, True)
+            dead = torch.from_numpy(vis == 0).to(q.device)
+            if bool(dead.any()):
+                Y = torch.where(dead.repeat_interleave(G, dim=0)[..., None], v.float().repeat_interleave(G, dim=0), Y)
+            fb = int(dead.sum().item()) * G
+        mass = torch.where(torch.isfinite(lse_s), torch.exp(lse_s - lse_d), torch.zeros_like(lse_s))
+        outputs[layer] = Y.cpu().numpy()
+        reports.append(LayerReport(layer, kind, _rel_l2(Y, Yd), float(mass.double().mean().item()), fb))
+    errs = np.array([r.output_rel_err_l2 for r in reports])
+    masses = np.array([r.mass_recovered_mean for r in reports])
+    overall = {"mean_output_rel_err_l2": float(errs.mean()), "max_output_rel_err_l2": float(errs.max()),
+               "mean_mass_recovered": float(masses.mean()),
+               "fallback_rows": int(sum(r.fallback_rows for r in reports))}
+    for kind in (KIND_ANCHOR0, KIND_ANCHOR, KIND_REUSE):
+        sub = [r for r in reports if r.kind == kind]
+        if sub:
+            overall[f"{kind}_mean_rel_err"] = float(np.mean([r.output_rel_err_l2 for r in sub]))
+            overall[f"{kind}_mean_mass_recovered"] = float(np.mean([r.mass_recovered_mean for r in sub]))
+    config = {"plan": plan.digest() if hasattr(plan, "digest") else "", "prompt_id": trace.prompt_id,
+              "phase": phase, "mode": plan.mode, "pooling": plan.pooling, "engine": "b200"}
+    return outputs, RunReport(per_layer=reports, overall=overall, config=config)
+
+
+def compare(outputs_a, outputs_b) -> RunReport:
+    """Per-layer rel-L2 of a against reference b (runner.py:321-344)."""
+    a, b = np.asarray(outputs_a), np.asarray(outputs_b)
+    if a.shape != b.shape:
+        raise InvalidArgumentError(f"shape mismatch: {a.shape} vs {b.shape}")
+    rel = []
+    for i in range(a.shape[0]):
+        num = np.linalg.norm((a[i].astype(np.float64) - b[i].astype(np.float64)).ravel())
+        den = np.linalg.norm(b[i].astype(np.float64).ravel())
+        rel.append(0.0 if den == 0.0 and num == 0.0 else (float("inf") if den == 0.0 else float(num / den)))
+    reports = [LayerReport(i, "compare", r, float("nan")) for i, r in enumerate(rel)]
+    errs = np.array(rel)
+    return RunReport(per_layer=reports,
+                     overall={"mean_output_rel_err_l2": float(errs.mean()), "max_output_rel_err_l2": float(errs.max())})

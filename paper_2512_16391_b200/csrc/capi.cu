@@ -36,16 +36,25 @@ constexpr int kMaxSplits = 64;
 constexpr int kSmCount = 148;
 constexpr int kCtasPerSm = 2;
 
+// Largest split-K factor the planner may pick for `pairs` (b, g) pairs; the
+// workspace is sized by it, so it depends on the batch and heads only.
+int max_splits_for(int pairs) {
+  const int slots = kSmCount * kCtasPerSm;
+  const int want = std::max(1, (slots + pairs - 1) / pairs);
+  return std::min(4 * want, kMaxSplits);
+}
+
 // Split-K factor: enough CTAs to cover the SMs in whole waves, each CTA a
 // contiguous run of 64-key tiles of one (b, g).
 int plan_splits(int pairs, int keys, int requested) {
   const int tiles = (keys + kscd::decode_tile_keys() - 1) / kscd::decode_tile_keys();
-  if (requested > 0) return std::max(1, std::min({requested, kMaxSplits, std::max(tiles, 1)}));
+  const int cap = max_splits_for(pairs);
+  if (requested > 0) return std::max(1, std::min({requested, cap, std::max(tiles, 1)}));
   const int slots = kSmCount * kCtasPerSm;
   const int want = std::max(1, (slots + pairs - 1) / pairs);
   int best = 1;
   double best_eff = -1.0;
-  for (int s = want; s <= std::min(std::max(4 * want, want), kMaxSplits); ++s) {
+  for (int s = want; s <= cap; ++s) {
     if (s > tiles) break;
     const int tps = (tiles + s - 1) / s;
     const int used = (tiles + tps - 1) / tps;            // splits that get work
@@ -58,7 +67,7 @@ int plan_splits(int pairs, int keys, int requested) {
 
 size_t decode_ws_bytes(const kscd_decode_params* p) {
   const size_t bh = (size_t)p->batch * p->num_q_heads;
-  size_t bytes = bh * kMaxSplits * (kscd::kHeadDimC + 2) * sizeof(float);
+  size_t bytes = bh * max_splits_for(p->batch * p->num_kv_heads) * (kscd::kHeadDimC + 2) * sizeof(float);
   bytes = (bytes + 255) & ~(size_t)255;
   bytes += (size_t)p->batch * p->num_kv_heads * sizeof(int);
   return bytes;
@@ -126,7 +135,7 @@ kscd::DecodeArgs make_args(const kscd_decode_params* p, int keys) {
   const size_t bh = (size_t)a.B * a.Hq;
   a.part = (float*)p->workspace;
   a.part_ml = a.part + bh * a.splits * kscd::kHeadDimC;
-  size_t off = bh * kMaxSplits * (kscd::kHeadDimC + 2) * sizeof(float);
+  size_t off = bh * max_splits_for(a.B * a.Hkv) * (kscd::kHeadDimC + 2) * sizeof(float);
   off = (off + 255) & ~(size_t)255;
   a.counters = (int*)((char*)p->workspace + off);
   return a;
@@ -310,6 +319,60 @@ extern "C" int kscd_sparse_prefill(const kscd_prefill_params* p, void* stream) {
   if (!p->causal) return fail(KSCD_UNSUPPORTED, "sparse prefill is causal (runner.py:275)");
   return cuda_status(kscd::launch_prefill_attn(kscd::PMODE_SPARSE, make_prefill_args(p), (cudaStream_t)stream),
                      "kscd_sparse_prefill");
+}
+
+extern "C" int kscd_dense_probs(const kscd_probs_params* p, void* stream) {
+  if (!p) return fail(KSCD_INVALID_ARGUMENT, "params is NULL");
+  if (p->head_dim != 128) return fail(KSCD_UNSUPPORTED, "head_dim %d unsupported", p->head_dim);
+  if (p->num_q_heads < 1 || p->num_kv_heads < 1 || p->num_q_heads % p->num_kv_heads || p->seq_len < 1)
+    return fail(KSCD_INVALID_ARGUMENT, "bad shape");
+  if (!p->q || !p->k || !p->lse || !p->probs) return fail(KSCD_INVALID_ARGUMENT, "NULL buffer");
+  kscd::ProbsArgs a{};
+  a.Hq = p->num_q_heads;
+  a.Hkv = p->num_kv_heads;
+  a.G = a.Hq / a.Hkv;
+  a.N = p->seq_len;
+  a.causal = p->causal;
+  a.scale = p->softmax_scale > 0.f ? p->softmax_scale : (float)(1.0 / sqrt((double)p->head_dim));
+  a.q = (const __nv_bfloat16*)p->q;
+  a.k = (const __nv_bfloat16*)p->k;
+  a.q_sh = p->q_stride_head;
+  a.kv_sh = p->kv_stride_head;
+  a.lse = p->lse;
+  a.P = p->probs;
+  return cuda_status(kscd::launch_dense_probs(a, (cudaStream_t)stream), "kscd_dense_probs");
+}
+
+extern "C" int kscd_pool_tiles(const kscd_pool_tiles_params* p, void* stream) {
+  if (!p) return fail(KSCD_INVALID_ARGUMENT, "params is NULL");
+  if (p->head_dim != 128) return fail(KSCD_UNSUPPORTED, "head_dim %d unsupported", p->head_dim);
+  if (p->num_q_heads < 1 || p->num_kv_heads < 1 || p->num_q_heads % p->num_kv_heads || p->seq_len < 1 ||
+      p->num_tiles < 1)
+    return fail(KSCD_INVALID_ARGUMENT, "bad shape");
+  if (!p->tile_starts || !p->tile_ends || !p->pooled) return fail(KSCD_INVALID_ARGUMENT, "NULL buffer");
+  if (p->pooling == 0 && !p->probs) return fail(KSCD_INVALID_ARGUMENT, "post pooling needs probs");
+  if (p->pooling == 1 && (!p->q || !p->k || !p->scratch)) return fail(KSCD_INVALID_ARGUMENT, "pre pooling needs q/k/scratch");
+  if (p->pooling == 1 && p->all_heads) return fail(KSCD_INVALID_ARGUMENT, "pre pooling is per kv head");
+  if (p->pooled_stride < p->seq_len) return fail(KSCD_INVALID_ARGUMENT, "pooled_stride < seq_len");
+  kscd::PoolRowsArgs a{};
+  a.Hq = p->num_q_heads;
+  a.Hkv = p->num_kv_heads;
+  a.G = a.Hq / a.Hkv;
+  a.N = p->seq_len;
+  a.T = p->num_tiles;
+  a.starts = p->tile_starts;
+  a.ends = p->tile_ends;
+  a.pre = p->pooling == 1;
+  a.all_heads = p->all_heads;
+  a.P = p->probs;
+  a.q = (const __nv_bfloat16*)p->q;
+  a.k = (const __nv_bfloat16*)p->k;
+  a.q_sh = p->q_stride_head;
+  a.kv_sh = p->kv_stride_head;
+  a.pooled = p->pooled;
+  a.pool_stride = p->pooled_stride;
+  a.scratch = p->scratch;
+  return cuda_status(kscd::launch_pool_rows(a, (cudaStream_t)stream), "kscd_pool_tiles");
 }
 
 extern "C" int kscd_select_prefill(const kscd_select_prefill_params* p, void* stream) {

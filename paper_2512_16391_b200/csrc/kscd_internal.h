@@ -110,4 +110,31 @@ struct PoolPrefillArgs {
 };
 cudaError_t launch_pool_prefill(const PoolPrefillArgs& a, cudaStream_t st);
 
+// ------------------------------------------------------------ compat (small N)
+struct ProbsArgs {
+  int Hq, Hkv, G, N, causal;
+  float scale;                            // natural-log softmax scale
+  const __nv_bfloat16* q;
+  const __nv_bfloat16* k;
+  int64_t q_sh, kv_sh;
+  const float* lse;                       // [Hq][N] natural
+  float* P;                               // [Hq][N][N]
+};
+cudaError_t launch_dense_probs(const ProbsArgs& a, cudaStream_t st);
+
+struct PoolRowsArgs {
+  int Hq, Hkv, G, N, T;
+  const int* starts;                      // [T] tile row ranges
+  const int* ends;
+  int pre, all_heads;
+  const float* P;                         // post: [Hq][N][N]
+  const __nv_bfloat16* q;                 // pre
+  const __nv_bfloat16* k;
+  int64_t q_sh, kv_sh;
+  float* pooled;                          // [Hkv or 1][T][pool_stride]
+  int64_t pool_stride;
+  double* scratch;                        // pre: [Hkv][T][pool_stride]
+};
+cudaError_t launch_pool_rows(const PoolRowsArgs& a, cudaStream_t st);
+
 }  // namespace kscd

@@ -1,0 +1,157 @@
+"""Multi-GPU partitioning of the Kascade path.
+
+One process per GPU, ``torch.distributed`` for the plumbing.  The independent
+units are (sequence, kv head) in decode and (kv head, tile) in prefill --
+pooling and Top-k are per kv head and per tile (runner.py:199-206) -- so:
+
+* **Batch sharding** (decode, first choice): every rank owns whole
+  sequences with all heads and layers.  No data-path collective at all.
+* **KV-head sharding** (decode when B < #GPUs, 70B-style TP, and prefill):
+  rank r owns kv heads [g0, g1) and their G query heads.  The one real
+  exchange step is the head remap: a reuse kv head g borrows the anchor list
+  of head_map[g] (runner.py:220), which can live on another rank, so every
+  anchor layer all-gathers its index lists (B*Hkv*k*4 B -- 3.4 MB at b8/128K)
+  and reuse layers read the gathered lists locally.  Head-sharded outputs are
+  all-gathered only when the caller wants them reassembled.
+
+The collectives run on whatever backend the process group has (NCCL over
+NVLink on the GPU box, gloo in the CPU tests).
+"""
+
+from __future__ import annotations
+
+from typing import Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+from .exceptions import InvalidArgumentError
+
+
+def _world(group=None) -> Tuple[int, int]:
+    if not dist.is_available() or not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+def even_split(n: int, world: int, rank: int) -> Tuple[int, int]:
+    """[start, end) of rank's share of n units; shares differ by at most 1."""
+    if world < 1 or not 0 <= rank < world:
+        raise InvalidArgumentError(f"bad rank {rank} of world {world}")
+    base, extra = divmod(n, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def batch_shard(batch: int, group=None) -> Tuple[int, int]:
+    """Sequences owned by this rank under batch sharding."""
+    world, rank = _world(group)
+    return even_split(batch, world, rank)
+
+
+def kv_head_shard(num_kv_heads: int, group=None) -> Tuple[int, int]:
+    """kv heads [g0, g1) owned by this rank under kv-head sharding; requires
+    Hkv divisible by the world size so every rank holds whole groups."""
+    world, rank = _world(group)
+    if num_kv_heads % world:
+        raise InvalidArgumentError(f"{num_kv_heads} kv heads do not split over {world} ranks")
+    per = num_kv_heads // world
+    return rank * per, (rank + 1) * per
+
+
+def gather_index_lists(local_idx: torch.Tensor, local_cnt: torch.Tensor, group=None,
+                       head_dim: int = 1) -> Tuple[torch.Tensor, torch.Tensor]:
+    """All-gather per-kv-head index lists along ``head_dim`` so every rank
+    holds the anchor sets of ALL kv heads (the head-remap exchange).
+
+    decode: idx [B][Hloc][k_cap], cnt [B][Hloc]      (head_dim = 1)
+    prefill: idx [Hloc][T][k_cap], cnt [Hloc][T]     (head_dim = 0)
+    Ranks are concatenated in rank order, i.e. global kv head order."""
+    world, _ = _world(group)
+    if world == 1:
+        return local_idx, local_cnt
+
+    def cat(t: torch.Tensor) -> torch.Tensor:
+        moved = t.movedim(head_dim, 0).contiguous()
+        out = torch.empty((world * moved.shape[0],) + tuple(moved.shape[1:]), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(out, moved, group=group)
+        return out.movedim(0, head_dim).contiguous()
+
+    return cat(local_idx), cat(local_cnt)
+
+
+def gather_head_outputs(local_out: torch.Tensor, group=None, head_dim: int = 1) -> torch.Tensor:
+    """Reassemble head-sharded outputs (decode [B][Hq_loc][d], head_dim 1;
+    prefill [Hq_loc][N][d], head_dim 0)."""
+    world, _ = _world(group)
+    if world == 1:
+        return local_out
+    moved = local_out.movedim(head_dim, 0).contiguous()
+    out = torch.empty((world * moved.shape[0],) + tuple(moved.shape[1:]), dtype=moved.dtype, device=moved.device)
+    dist.all_gather_into_tensor(out, moved, group=group)
+    return out.movedim(0, head_dim)
+
+
+def local_head_map(head_map, g0: int, g1: int, device=None) -> torch.Tensor:
+    """The head-remap entries of this rank's kv heads.  Values stay GLOBAL
+    source heads: they index the gathered (all-heads) lists."""
+    m = [int(x) for x in head_map]
+    return torch.tensor(m[g0:g1], dtype=torch.int32, device=device)
+
+
+class ShardedKascadeDecoder:
+    """KV-head-sharded decode executor (one rank's share).
+
+    Anchor layers select on the local kv heads, then all-gather the index
+    lists; reuse layers gather through the GLOBAL head map from the gathered
+    lists.  q / caches passed to ``step`` are the rank's local head slices."""
+
+    def __init__(self, plan, num_layers: int, batch: int, num_q_heads: int, num_kv_heads: int,
+                 max_seq_len: int, group=None, device=None):
+        from . import engine
+        from .host_types import KIND_REUSE, MODE_ALL_HEADS_POOLED, k_budget, validate_plan
+        validate_plan(plan, num_layers, num_kv_heads)
+        if plan.mode == MODE_ALL_HEADS_POOLED:
+            raise InvalidArgumentError("all-heads-pooled mode needs the pooled vectors of every kv head; "
+                                       "use batch sharding (SURVEY.md 8(e) mode caveat)")
+        self.group = group
+        self.g0, self.g1 = kv_head_shard(num_kv_heads, group)
+        self.G = num_q_heads // num_kv_heads
+        self.Hkv, self.Hloc = num_kv_heads, self.g1 - self.g0
+        self.local = engine.KascadeDecoder(plan, num_layers, batch, self.Hloc * self.G, self.Hloc, max_seq_len,
+                                           device=device)
+        dev = self.local.device
+        self.kinds = self.local.kinds
+        self.maps = {l: local_head_map(plan.head_maps[l].map, self.g0, self.g1, dev)
+                     for l, kind in enumerate(self.kinds) if kind == KIND_REUSE}
+        self.own = torch.arange(self.g0, self.g1, dtype=torch.int32, device=dev)
+        kc = k_budget(plan.k_policy, max_seq_len)
+        self.full_idx = torch.empty(batch, num_kv_heads, kc, dtype=torch.int32, device=dev)
+        self.full_cnt = torch.zeros(batch, num_kv_heads, dtype=torch.int32, device=dev)
+
+    def step(self, q, k_caches, v_caches, seq_len: int) -> torch.Tensor:
+        from . import ops
+        from .host_types import KIND_ANCHOR, KIND_ANCHOR0, KIND_REUSE
+        loc = self.local
+        pol = loc.plan.k_policy
+        for l, kind in enumerate(self.kinds):
+            ql, kl, vl = q[l], k_caches[l], v_caches[l]
+            if kind == KIND_REUSE:
+                ops.sparse_decode(ql, kl, vl, seq_len, self.full_idx, self.full_cnt, self.maps[l], out=loc.out[l])
+                continue
+            if kind == KIND_ANCHOR0:
+                ops.dense_decode(ql, kl, vl, seq_len, out=loc.out[l], lse=loc.lse, scores=loc.scores)
+            else:
+                ops.anchor_scores_decode(ql, kl, seq_len, loc.scores, loc.lse)
+            ops.select_decode(loc.scores, loc.lse, seq_len, pol, self.Hloc, indices=loc.indices, counts=loc.counts,
+                              pooled=loc.pooled)
+            idx, cnt = gather_index_lists(loc.indices, loc.counts, self.group, head_dim=1)
+            self.full_idx[:, :, :idx.shape[2]].copy_(idx)
+            self.full_cnt.copy_(cnt)
+            if kind == KIND_ANCHOR:
+                ops.sparse_decode(ql, kl, vl, seq_len, self.full_idx, self.full_cnt, self.own, out=loc.out[l])
+        return loc.out
+
+    def gather_outputs(self) -> torch.Tensor:
+        """[L][B][Hq][d] reassembled from every rank's heads."""
+        return gather_head_outputs(self.local.out, self.group, head_dim=2)
