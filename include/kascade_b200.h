@@ -139,7 +139,8 @@ typedef struct kscd_select_prefill_params {
   int64_t q_stride_head, kv_stride_head;
   float softmax_scale;
   const float* lse;        /* fp32 [Hq][N] from kscd_dense_prefill / kscd_anchor_lse_prefill */
-  float* pooled;           /* scratch fp32 [Hkv][T][pooled_stride] (all-heads: [1][T][...]) */
+  float* pooled;           /* scratch fp32 [2][Hkv][T][pooled_stride] (all-heads: [2][1][T][...]):
+                              two partial-sum planes, the pooled row is plane0 + plane1 */
   int64_t pooled_stride;   /* >= N, multiple of 4 */
   double topk_fraction;
   int32_t k_min;

@@ -423,6 +423,7 @@ extern "C" int kscd_select_prefill(const kscd_select_prefill_params* p, void* st
   kscd::TopkArgs ta{};
   ta.rows = (p->all_heads ? 1 : p->num_kv_heads) * T;
   ta.vals = p->pooled;
+  ta.vals2 = p->pooled + (int64_t)ta.rows * p->pooled_stride;   // second warpgroup's partial plane
   ta.val_stride = p->pooled_stride;
   ta.len = p->seq_len;
   ta.k = kmax;

@@ -54,6 +54,7 @@ cudaError_t launch_pool_decode(const PoolDecodeArgs& a, cudaStream_t st);
 struct TopkArgs {
   int rows;
   const float* vals;                      // row r at vals + r*val_stride (+ row_offset)
+  const float* vals2;                     // optional second plane, same layout: value = vals + vals2
   int64_t val_stride;
   const int* lens;                        // per-row length (nullable => len)
   int len;

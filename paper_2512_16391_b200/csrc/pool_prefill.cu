@@ -15,10 +15,13 @@
 // break Top-k parity).  LSE comes from the dense / LSE pass of the same layer.
 //
 // CTA = (tile i, kv head g, head chunk of <= 4 heads).  Q of the chunk is
-// resident in shared memory ([half][rows][128 B], 128B-swizzled, so any
-// 256-row slice is one canonical UMMA operand); K blocks stream through a
-// 2-stage TMA ring.  The 512 TMEM columns hold S^T of rows 0-255 and
-// 256-511; two warpgroups each consume one half and ping-pong with the MMA.
+// resident in shared memory ([half][rows][128 B], 128B-swizzled, so each
+// head's 128 rows are one canonical UMMA operand); K blocks stream through a
+// 2-stage TMA ring.  The 512 TMEM columns hold one 128x128 S^T quarter per
+// head; warpgroup x owns quarters x and x+2, so the tensor core refills one
+// quarter while the warpgroup exponentiates the other (double buffering
+// without extra TMEM) and the two warpgroups run decoupled, each writing a
+// partial-sum plane that the Top-k reads as plane0 + plane1.
 #include "sm100.cuh"
 #include "kscd_internal.h"
 
@@ -37,6 +40,7 @@ constexpr int kOffRed = kOffLse + 512 * 4;         // float[2][128]
 constexpr int kOffBar = kOffRed + 2 * 128 * 4;
 constexpr int kOffTmem = kOffBar + 16 * 8;
 constexpr int kSmemBytes = kOffTmem + 16 + 1024;
+constexpr uint32_t kIdescQ = idesc_bf16(128, 128, false, false);   // S^T quarter: 128 keys x 128 rows
 }  // namespace pp
 
 struct PoolTmaps {
@@ -63,8 +67,6 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
   const int nb = (t1 + kBlock - 1) / kBlock;
   const int nh = a.nheads;                       // heads of this chunk (<= 4)
   const int hbase = g * a.G + a.head_begin;
-  const int nrows = nh * 128;
-  const int nhalves = (nrows + 255) / 256;
 
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
@@ -72,9 +74,9 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
       mbar_init(&bars[1 + s], 1);
       mbar_init(&bars[3 + s], 1);
     }
-    for (int x = 0; x < 2; ++x) {
-      mbar_init(&bars[5 + x], 1);
-      mbar_init(&bars[7 + x], 128);
+    for (int qq = 0; qq < 4; ++qq) {
+      mbar_init(&bars[5 + qq], 1);     // s_full[quarter]
+      mbar_init(&bars[9 + qq], 128);   // buf_free[quarter]
     }
     fence_barrier_init();
   }
@@ -113,22 +115,24 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
       const uint32_t qaddr = smem_u32(smem + kOffQ);
       const uint32_t kaddr = smem_u32(smem + kOffK);
       mbar_wait(&bars[0], 0);
+      // quarter qq = head qq of the chunk (128 rows) -> TMEM columns
+      // [128 qq, 128 qq + 128); issue order alternates the two warpgroups
       for (int j = 0; j < nb; ++j) {
         const int st = j % kStages;
         mbar_wait(&bars[1 + st], (j / kStages) & 1);
-        for (int x = 0; x < nhalves; ++x) {
-          if (j > 0) mbar_wait(&bars[7 + x], (j - 1) & 1);   // WG x has read block j-1
+        for (int oi = 0; oi < 4; ++oi) {
+          const int qq = (oi >> 1) | ((oi & 1) << 1);   // 0, 2, 1, 3
+          if (qq >= nh) continue;
+          if (j > 0) mbar_wait(&bars[9 + qq], (j - 1) & 1);   // quarter qq of block j-1 consumed
           tc_fence_after();
-          const int ncols = min(256, nrows - 256 * x);
-          const uint32_t idesc = idesc_bf16(128, ncols, false, false);
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks) {
             const uint32_t koff = (ks >> 2) * 16384 + (ks & 3) * 32;
-            const uint32_t qoff = (ks >> 2) * kHalfRows + x * 256 * 128 + (ks & 3) * 32;
-            mma_ss(tmem + 256 * x, sw128_desc(kaddr + st * 32768 + koff, 16, 1024),
-                   sw128_desc(qaddr + qoff, 16, 1024), idesc, ks > 0);
+            const uint32_t qoff = (ks >> 2) * kHalfRows + qq * 128 * 128 + (ks & 3) * 32;
+            mma_ss(tmem + 128 * qq, sw128_desc(kaddr + st * 32768 + koff, 16, 1024),
+                   sw128_desc(qaddr + qoff, 16, 1024), kIdescQ, ks > 0);
           }
-          mma_commit(&bars[5 + x]);
+          mma_commit(&bars[5 + qq]);
         }
         mma_commit(&bars[3 + st]);
       }
@@ -136,57 +140,54 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n");
     // --------------------------------------------------- column-sum warpgroups
-    const int x = (warp - 4) >> 2;                 // which 256-row half
+    // WG x owns quarters x and x + 2 (heads of the chunk); while it sums one,
+    // the tensor core refills the other's TMEM buffer for the next block.  Each
+    // WG writes its own partial plane (read back as plane0 + plane1 by the
+    // Top-k), so the warpgroups never wait for each other and the result is
+    // deterministic.
+    const int x = (warp - 4) >> 2;
     const int q = warp & 3;
     const int key_in_blk = q * 32 + lane;          // TMEM lane = key
-    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + 256 * x;
-    const int ncols = x < nhalves ? min(256, nrows - 256 * x) : 0;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    const int64_t plane = (int64_t)(a.g_fixed >= 0 ? 1 : a.Hkv) * T * a.pool_stride;
     // all-heads-pooled mode writes one row per tile (runner.py:180-197)
-    float* out_row = a.pooled + ((int64_t)(a.g_fixed >= 0 ? 0 : g) * T + ti) * a.pool_stride;
+    float* out_row = a.pooled + x * plane + ((int64_t)(a.g_fixed >= 0 ? 0 : g) * T + ti) * a.pool_stride;
+    const float2 sc2 = make_float2(a.scale_log2, a.scale_log2);
     for (int j = 0; j < nb; ++j) {
       const int key = j * kBlock + key_in_blk;
-      float acc = 0.f;
-      if (ncols > 0) {
-        mbar_wait(&bars[5 + x], j & 1);
+      const bool diag = (j == nb - 1);             // only the last block crosses the staircase
+      float2 acc2 = make_float2(0.f, 0.f);
+      for (int qq = x; qq < nh; qq += 2) {
+        mbar_wait(&bars[5 + qq], j & 1);
         tc_fence_after();
-        const bool diag = (j == nb - 1);           // only the last block crosses the staircase
-        const float2 sc2 = make_float2(a.scale_log2, a.scale_log2);
-        float2 acc2 = make_float2(0.f, 0.f);
-        for (int c0 = 0; c0 < ncols; c0 += 64) {
-          // two 32-column TMEM loads in flight per wait
-          uint32_t r[64];
-          tmem_ld32(lane_base + c0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-          tmem_ld32(lane_base + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-          tmem_ld_wait();
-          const float4* l4 = reinterpret_cast<const float4*>(lse2 + 256 * x + c0);
+        uint32_t r[128];
 #pragma unroll
-          for (int i = 0; i < 64; i += 4) {
-            const float4 lv = l4[i >> 2];          // broadcast read: same rows for every key
-            float2 e0 = __ffma2_rn(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sc2,
-                                   make_float2(-lv.x, -lv.y));
-            float2 e1 = __ffma2_rn(make_float2(__uint_as_float(r[i + 2]), __uint_as_float(r[i + 3])), sc2,
-                                   make_float2(-lv.z, -lv.w));
-            e0 = make_float2(fast_exp2(e0.x), fast_exp2(e0.y));
-            e1 = make_float2(fast_exp2(e1.x), fast_exp2(e1.y));
-            if (diag) {
-              const int rr = (c0 + i) & 127;       // row within the tile of column c0+i
-              if (key > r0 + rr) e0.x = 0.f;
-              if (key > r0 + rr + 1) e0.y = 0.f;
-              if (key > r0 + rr + 2) e1.x = 0.f;
-              if (key > r0 + rr + 3) e1.y = 0.f;
-            }
-            acc2 = __fadd2_rn(acc2, __fadd2_rn(e0, e1));
-          }
-        }
-        acc = acc2.x + acc2.y;
+        for (int c = 0; c < 4; ++c)
+          tmem_ld32(lane_base + 128 * qq + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&r[32 * c]));
+        tmem_ld_wait();
         tc_fence_before();
-        mbar_arrive(&bars[7 + x]);
+        mbar_arrive(&bars[9 + qq]);                // buffer free: the MMA may refill it
+        const float4* l4 = reinterpret_cast<const float4*>(lse2 + 128 * qq);
+#pragma unroll
+        for (int i = 0; i < 128; i += 4) {
+          const float4 lv = l4[i >> 2];            // broadcast read: same rows for every key
+          float2 e0 = __ffma2_rn(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sc2,
+                                 make_float2(-lv.x, -lv.y));
+          float2 e1 = __ffma2_rn(make_float2(__uint_as_float(r[i + 2]), __uint_as_float(r[i + 3])), sc2,
+                                 make_float2(-lv.z, -lv.w));
+          e0 = make_float2(fast_exp2(e0.x), fast_exp2(e0.y));
+          e1 = make_float2(fast_exp2(e1.x), fast_exp2(e1.y));
+          if (diag) {
+            if (key > r0 + i) e0.x = 0.f;
+            if (key > r0 + i + 1) e0.y = 0.f;
+            if (key > r0 + i + 2) e1.x = 0.f;
+            if (key > r0 + i + 3) e1.y = 0.f;
+          }
+          acc2 = __fadd2_rn(acc2, __fadd2_rn(e0, e1));
+        }
       }
-      // combine the two halves: WG1 parks its sums, WG0 adds and stores
-      if (x == 1) red[(j & 1) * 128 + key_in_blk] = acc;
-      named_bar_sync(2, 256);
-      if (x == 0 && key < t1) {
-        float v = acc + red[(j & 1) * 128 + key_in_blk];
+      if (key < t1) {
+        float v = acc2.x + acc2.y;
         if (a.accumulate) v += out_row[key];
         out_row[key] = v;
       }

@@ -101,10 +101,18 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
       mbar_init(&bars[3 + s], MODE == PMODE_SPARSE ? 96 : 1);
       mbar_init(&bars[5 + s], 1);
     }
-    for (int t = 0; t < 2; ++t) {
-      mbar_init(&bars[7 + t], 1);
-      mbar_init(&bars[9 + t], 128);
-      mbar_init(&bars[11 + t], 1);
+    if (MODE == PMODE_LSE) {
+      // no O: each tile double-buffers S; s_full(t,b) = 7+t+2b, p_full(t,b) = 11+t+2b
+      for (int i = 0; i < 4; ++i) {
+        mbar_init(&bars[7 + i], 1);
+        mbar_init(&bars[11 + i], 128);
+      }
+    } else {
+      for (int t = 0; t < 2; ++t) {
+        mbar_init(&bars[7 + t], 1);
+        mbar_init(&bars[9 + t], 128);
+        mbar_init(&bars[11 + t], 1);
+      }
     }
     fence_barrier_init();
   }
@@ -143,6 +151,29 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
           }
         };
         mbar_wait(&bars[0], 0);
+        if (MODE == PMODE_LSE) {
+          // S only: block j goes to buffer j&1 of each tile as soon as the
+          // softmax has drained that buffer (block j-2), so the tensor core
+          // runs a block ahead of the exponentials.
+          for (int j = 0; j < nb; ++j) {
+            const int st = j % kStages, b = j & 1;
+            mbar_wait(&bars[1 + st], (j / kStages) & 1);
+            for (int t = 0; t < nslots; ++t) {
+              if (j >= 2) mbar_wait(&bars[11 + t + 2 * b], ((j >> 1) - 1) & 1);
+              tc_fence_after();
+              const uint32_t d = tmem + t * 256 + b * 128;
+#pragma unroll
+              for (int ks = 0; ks < 8; ++ks) {
+                const uint32_t off = (ks >> 2) * kHalf + (ks & 3) * 32;
+                mma_ss(d, sw128_desc(qaddr + t * kTileBytes + off, 16, 1024),
+                       sw128_desc(kaddr + st * kTileBytes + off, 16, 1024), kIdescS, ks > 0);
+              }
+              mma_commit(&bars[7 + t + 2 * b]);
+            }
+            mma_commit(&bars[5 + st]);
+          }
+        }
+        if (MODE != PMODE_LSE) {
         mbar_wait(&bars[1], 0);
         tc_fence_after();
         for (int t = 0; t < nslots; ++t) issue_s(t, 0);
@@ -176,6 +207,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
           mma_commit(&bars[5 + st]);   // K/V stage free once everything so far retires
           if (more && nslots == 2) issue_s(1, st1);
         }
+        }  // MODE != PMODE_LSE
       }
     } else if (MODE != PMODE_SPARSE) {
       if (warp == 0 && lane == 0 && nb > 0) {
@@ -260,13 +292,16 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
       const int h = h0 + t;
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < nb; ++j) {
-        mbar_wait(&bars[7 + t], j & 1);
+        // LSE mode: S double-buffered (buffer j&1, its own barrier pair)
+        const int sb = MODE == PMODE_LSE ? 7 + t + 2 * (j & 1) : 7 + t;
+        const uint32_t s_off = MODE == PMODE_LSE ? 128 * (j & 1) : 0;
+        mbar_wait(&bars[sb], MODE == PMODE_LSE ? (j >> 1) & 1 : j & 1);
         tc_fence_after();
         // the whole 128-key row of S in one batch of TMEM loads, one wait
         float s[128];
 #pragma unroll
         for (int c = 0; c < 4; ++c)
-          tmem_ld32(lane_base + s_col + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]));
+          tmem_ld32(lane_base + s_col + s_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]));
         tmem_ld_wait();
         // masking on raw scores: keys past the end / after the row (causal) /
         // unselected.  Sorted selections only reach the tile's own rows in
@@ -351,7 +386,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
         }
         l += sum2.x + sum2.y;
         tc_fence_before();
-        mbar_arrive(&bars[9 + t]);
+        mbar_arrive(&bars[MODE == PMODE_LSE ? 11 + t + 2 * (j & 1) : 9 + t]);
       }
       // ---------------------------------------------------------- epilogue
       const bool live = row < a.N;

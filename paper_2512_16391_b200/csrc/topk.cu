@@ -103,6 +103,23 @@ KSCD_DEV uint32_t block_excl_scan(uint32_t v, uint32_t* warp_tot, uint32_t& tota
   return res;
 }
 
+// Four consecutive values of a row (plus the second partial plane when the
+// row is stored as two sums, see pool_prefill.cu); out-of-range -> 0.
+KSCD_DEV void load4(const float* vals, const float* vals2, int j, int end, bool vec, float (&v)[4]) {
+  if (vec && j + 3 < end) {
+    const float4 f = __ldcg(reinterpret_cast<const float4*>(vals + j));
+    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+    if (vals2) {
+      const float4 f2 = __ldcg(reinterpret_cast<const float4*>(vals2 + j));
+      v[0] += f2.x; v[1] += f2.y; v[2] += f2.z; v[3] += f2.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      v[i] = j + i < end ? __ldcg(vals + j + i) + (vals2 ? __ldcg(vals2 + j + i) : 0.f) : 0.f;
+  }
+}
+
 struct TopkShared {
   uint32_t hist[4096];
   uint32_t range_tot[16];     // per-CTA bin-range totals (valid in CTA 0)
@@ -129,6 +146,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
   }
   const int take = n < k ? n : k;
   const float* vals = a.vals + (int64_t)r * a.val_stride;
+  const float* vals2 = a.vals2 ? a.vals2 + (int64_t)r * a.val_stride : nullptr;
   int* out = a.idx + (int64_t)r * a.k_cap;
   // segment of this CTA (multiple of 8 elements so float4 loads stay aligned)
   const int seg_len = ((n + CL - 1) / CL + 7) & ~7;
@@ -157,13 +175,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
     for (int it = 0; it < iters; ++it) {
       const int j = seg0 + (it * kTopkThreads + tid) * 4;
       float v[4];
-      if (vec && j + 3 < seg1) {
-        const float4 f = __ldcg(reinterpret_cast<const float4*>(vals + j));
-        v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-      } else {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = j + i < seg1 ? __ldcg(vals + j + i) : 0.f;
-      }
+      load4(vals, vals2, j, seg1, vec, v);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const uint32_t key = order_key(v[i]);
@@ -263,13 +275,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
   for (int base = seg0; base < seg1; base += kTopkThreads * 4) {
     const int j = base + tid * 4;
     float v[4];
-    if (vec && j + 3 < seg1) {
-      const float4 f = __ldcg(reinterpret_cast<const float4*>(vals + j));
-      v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-    } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) v[i] = j + i < seg1 ? __ldcg(vals + j + i) : 0.f;
-    }
+    load4(vals, vals2, j, seg1, vec, v);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const uint32_t key = order_key(v[i]);
@@ -304,13 +310,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
     for (int h = 0; h < kTopkItems; h += 4) {
       float v[4];
       const int j = j0 + h;
-      if (vec && j + 3 < seg1) {
-        const float4 f = __ldcg(reinterpret_cast<const float4*>(vals + j));
-        v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-      } else {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = j + i < seg1 ? __ldcg(vals + j + i) : 0.f;
-      }
+      load4(vals, vals2, j, seg1, vec, v);
 #pragma unroll
       for (int i = 0; i < 4; ++i) keys[h + i] = order_key(v[i]);
     }

@@ -146,7 +146,7 @@ class KascadePrefill:
                 self.head_maps[l] = torch.tensor(m, dtype=torch.int32, device=dev)
         self.shared_map = torch.zeros(num_kv_heads, dtype=torch.int32, device=dev) if self.all_heads else None
         self.lse = torch.empty(num_q_heads, seq_len, dtype=torch.float32, device=dev)
-        self.pooled = torch.empty(rows, T, (seq_len + 3) // 4 * 4, dtype=torch.float32, device=dev)
+        self.pooled = torch.empty(2, rows, T, (seq_len + 3) // 4 * 4, dtype=torch.float32, device=dev)
         self.indices = torch.empty(rows, T, kc, dtype=torch.int32, device=dev)
         self.counts = torch.zeros(rows, T, dtype=torch.int32, device=dev)
         self.out = torch.empty(num_layers, num_q_heads, seq_len, 128, dtype=torch.bfloat16, device=dev)

@@ -334,7 +334,10 @@ def select_prefill(q, k, lse, policy: KBudgetPolicy, *, indices=None, counts=Non
     kc = prefill_k_cap(policy, N)
     dev = q.device
     if pooled is None:
-        pooled = torch.empty(rows, T, (N + 3) // 4 * 4, dtype=torch.float32, device=dev)
+        # two partial-sum planes (one per column-sum warpgroup), row = sum
+        pooled = torch.empty(2, rows, T, (N + 3) // 4 * 4, dtype=torch.float32, device=dev)
+    if pooled.dim() != 4 or pooled.shape[:3] != (2, rows, T) or pooled.shape[3] < N or not pooled.is_contiguous():
+        raise InvalidArgumentError(f"pooled scratch must be fp32 [2][{rows}][{T}][>=N] contiguous")
     if indices is None:
         indices = torch.empty(rows, T, kc, dtype=torch.int32, device=dev)
     if counts is None:
@@ -342,7 +345,7 @@ def select_prefill(q, k, lse, policy: KBudgetPolicy, *, indices=None, counts=Non
     p = _lib.SelectPrefillParams(
         num_q_heads=Hq, num_kv_heads=Hkv, head_dim=HEAD_DIM, seq_len=N, q=q.data_ptr(), k=k.data_ptr(),
         q_stride_head=q.stride(0), kv_stride_head=k.stride(0), softmax_scale=float(scale or 0.0),
-        lse=lse.data_ptr(), pooled=pooled.data_ptr(), pooled_stride=pooled.stride(1),
+        lse=lse.data_ptr(), pooled=pooled.data_ptr(), pooled_stride=pooled.stride(2),
         topk_fraction=float(policy.fraction), k_min=int(policy.k_min), all_heads=1 if all_heads else 0,
         indices=indices.data_ptr(), counts=counts.data_ptr(), k_cap=indices.shape[-1], tile_size=TILE)
     _lib.call("kscd_select_prefill", p, _stream())

@@ -45,7 +45,7 @@ def main():
     res["lse_pass_ms"] = t
     res["lse_pass_tflops"] = flops_dense / 2 / t / 1e9
     T = (N + 127) // 128
-    pooled = torch.empty(Hkv, T, (N + 3) // 4 * 4, dtype=torch.float32, device=dev)
+    pooled = torch.empty(2, Hkv, T, (N + 3) // 4 * 4, dtype=torch.float32, device=dev)
     idx = torch.empty(Hkv, T, ops.prefill_k_cap(pol, N), dtype=torch.int32, device=dev)
     cnt = torch.empty(Hkv, T, dtype=torch.int32, device=dev)
     t = timeit(lambda: ops.select_prefill(q, k, lse, pol, indices=idx, counts=cnt, pooled=pooled))
