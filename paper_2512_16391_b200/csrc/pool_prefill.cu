@@ -175,8 +175,8 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
                                  make_float2(-lv.x, -lv.y));
           float2 e1 = __ffma2_rn(make_float2(__uint_as_float(r[i + 2]), __uint_as_float(r[i + 3])), sc2,
                                  make_float2(-lv.z, -lv.w));
-          e0 = make_float2(fast_exp2(e0.x), fast_exp2(e0.y));
-          e1 = make_float2(fast_exp2(e1.x), fast_exp2(e1.y));
+          e0 = exp2_pair(e0, i >> 1);
+          e1 = exp2_pair(e1, (i >> 1) + 1);
           if (diag) {
             if (key > r0 + i) e0.x = 0.f;
             if (key > r0 + i + 1) e0.y = 0.f;

@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
 #pragma unroll
           for (int c = 0; c < 128; c += 2) {
             const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sc2, nm2);
-            sum2 = __fadd2_rn(sum2, make_float2(fast_exp2(x.x), fast_exp2(x.y)));
+            sum2 = __fadd2_rn(sum2, exp2_pair(x, c >> 1));
           }
         } else {
 #pragma unroll
@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const float2 x = __ffma2_rn(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sc2, nm2);
-              const float2 p = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+              const float2 p = exp2_pair(x, c * 16 + i);
               sum2 = __fadd2_rn(sum2, p);
               r[i] = pack_bf16(p.x, p.y);
             }
