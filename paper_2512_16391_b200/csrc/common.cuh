@@ -95,11 +95,15 @@ KSCD_DEV float2 exp2_poly2(float2 x) {
   return make_float2(x.x < -126.f ? 0.f : rx, x.y < -126.f ? 0.f : ry);
 }
 
-// exp2 of a pair: FMA-pipe polynomial for pair indices with (pair & 7) < 3
-// (3/8 of the pairs), MUFU for the rest.  `pair` is a compile-time constant
+// exp2 of a pair: FMA-pipe polynomial for pair indices with (pair & 7) <
+// kPolyPairsPer8, MUFU for the rest.  `pair` is a compile-time constant
 // inside the fully unrolled softmax loops, so the split costs nothing.
+// Measured on B200 (128K prefill): 3/8 polynomial made the dense / LSE /
+// pass-B kernels 10-16% SLOWER (extra issue slots + register spills), so the
+// split is off; the kernels are issue/latency bound, not MUFU bound.
+constexpr int kPolyPairsPer8 = 0;
 KSCD_DEV float2 exp2_pair(float2 x, int pair) {
-  if ((pair & 7) < 3) return exp2_poly2(x);
+  if ((pair & 7) < kPolyPairsPer8) return exp2_poly2(x);
   return make_float2(fast_exp2(x.x), fast_exp2(x.y));
 }
 
