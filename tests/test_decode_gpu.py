@@ -159,6 +159,26 @@ def test_topk_ties_and_padding(cuda_ok):
             assert (idx[r, ref.size:] == 2**31 - 1).all()
 
 
+@pytest.mark.parametrize("dist", ["lognormal", "heavy", "tied_block"])
+def test_topk_long_rows_exact(cuda_ok, dist):
+    # long rows take the sample-bracketed path; tied blocks force its exact fallback
+    from paper_2512_16391_b200 import ops
+    rng = np.random.default_rng(17)
+    n = 150001
+    if dist == "lognormal":
+        w = np.exp(rng.standard_normal((3, n)) * 2).astype(np.float32)
+    elif dist == "heavy":
+        w = (rng.pareto(1.5, (3, n)) + 1e-9).astype(np.float32)
+    else:
+        w = np.exp(rng.standard_normal((3, n))).astype(np.float32)
+        w[:, 1000:60000] = np.float32(1.5)          # a huge tie straddling the threshold
+    for k in (1, 128, 15000, 149999):
+        idx, cnt = ops.topk(_dev(w), k, k_cap=k)
+        idx = idx.cpu().numpy()
+        for r in range(3):
+            np.testing.assert_array_equal(idx[r, :cnt[r]], orc.topk_sorted(w[r], k))
+
+
 def test_select_decode_matches_oracle(cuda_ok):
     from paper_2512_16391_b200 import ops
     from paper_2512_16391_b200.host_types import KBudgetPolicy
