@@ -199,6 +199,43 @@ def run_reference(args, rank):
 
 
 # ------------------------------------------------------------------ prefill
+def cpu_prefill_sample(N, fraction, k_min, tiles=(0.25, 0.5, 0.75, 1.0)):
+    """CPU oracle (the reference algorithm) on a bounded sample of one 128K
+    prefill layer: per-tile drivers (oracle.prefill_tile_select /
+    sparse_tile) for ONE kv head (G = 4 heads) at 4 tile
+    positions, extrapolated to the layer with cost proportional to the
+    tile's causal bound (the reference itself cannot hold P at 128K)."""
+    from oracle import kascade_oracle as orc
+    rng = np.random.default_rng(1)
+    G, d = CFG["Hq"] // CFG["Hkv"], 128
+    Q = orc.bf16_round(rng.standard_normal((G, N, d)).astype(np.float32))
+    K = orc.bf16_round(rng.standard_normal((1, N, d)).astype(np.float32))
+    V = orc.bf16_round(rng.standard_normal((1, N, d)).astype(np.float32))
+    T = (N + 127) // 128
+    per_bound = {"dense": [], "anchor_select": [], "sparse": []}
+    for f in tiles:
+        i = max(0, int(f * T) - 1)
+        s, e = 128 * i, min(N, 128 * i + 128)
+        t0 = time.perf_counter()
+        Pt = orc.prefill_tile_rows(Q, K, 0, G, s, e)
+        _ = np.stack([Pt[j] @ V[0] for j in range(G)])
+        t1 = time.perf_counter()
+        sel, _ = orc.prefill_tile_select(Q, K, 0, G, s, e, fraction, k_min)
+        t2 = time.perf_counter()
+        orc.sparse_tile(Q, K, V, 0, G, s, e, sel)
+        t3 = time.perf_counter()
+        per_bound["dense"].append((t1 - t0) / e)
+        per_bound["anchor_select"].append((t2 - t1) / e)
+        per_bound["sparse"].append((t3 - t2) / e)
+    sum_bounds = sum(min(N, 128 * (i + 1)) for i in range(T)) * CFG["Hkv"]
+    est = {k: float(np.mean(v)) * sum_bounds for k, v in per_bound.items()}
+    layer = {"dense": est["dense"], "anchor0": est["dense"] + est["anchor_select"],
+             "anchor": est["anchor_select"] + est["sparse"], "reuse": est["sparse"]}
+    n_anchor, n_reuse = len(LLAMA_ANCHORS) - 1, CFG["layers"] - len(LLAMA_ANCHORS)
+    kascade = (layer["anchor0"] + n_anchor * layer["anchor"] + n_reuse * layer["reuse"]) / CFG["layers"]
+    return kascade, layer
+
+
 def bench_prefill(args, dev, world, dist):
     """Llama-3.1-8B prefill at 128K (batch 1 per GPU): the full 32-layer
     Kascade forward and the dense (Top-k = 100%) forward of the same engine,
@@ -280,6 +317,15 @@ def bench_prefill(args, dev, world, dist):
     weighted = (t_a0 + n_anchor * t_anchor + n_reuse * t_reuse) / L
     del qs, ks, vs, Q, K, V, eng
     torch.cuda.empty_cache()
+    cpu_prefill = None
+    if not args.no_cpu_baseline and world == 1:
+        kas_s, layer_s = cpu_prefill_sample(N, args.fraction, args.k_min)
+        cpu_prefill = {"value": round(kas_s * 1e3, 1), "unit": "ms/layer (extrapolated)", "cores": os.cpu_count(),
+                       "kind": "port",
+                       "sample": "per-tile oracle drivers for one kv head at 4 tile positions of a 128K layer, "
+                                 "extrapolated with cost proportional to each tile's causal bound; the full "
+                                 "reference cannot run at 128K (P alone is 512 GiB per layer)",
+                       "per_layer_s": {k_: round(v, 1) for k_, v in layer_s.items()}}
     return {
         "workload": f"llama8b-prefill-{N // 1024}k-b1-k{args.fraction:g}",
         "kascade_ms": round(ms_kas, 2), "kascade_ms_per_layer": round(ms_kas / L, 3),
@@ -296,6 +342,7 @@ def bench_prefill(args, dev, world, dist):
                      "peak_kind": kind,
                      "dense_prefill_frac": round(flops_dense / (t_dense * 1e-3) / 1e12 / tpk, 4)},
         "gpu_launches_per_step": 1 * 3 + n_anchor * 4 + n_reuse,
+        "cpu_baseline": cpu_prefill,
     }
 
 
