@@ -19,6 +19,8 @@
 // beyond the ring's.  Partial (m, l, O) of the 4 warps are merged in shared
 // memory; the last CTA of a (b, g) to finish merges the splits (warp-shuffle
 // LSE merge) and resets its arrival counter, so no extra launch is needed.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kscd_internal.h"
 
@@ -28,20 +30,24 @@ constexpr int kTileKeys = 64;
 constexpr int kThreads = 128;
 constexpr int kTileBytes = kTileKeys * kRowBytes;  // 16 KB
 
-template <int MODE>
+// STG = ring depth (0 = default: 3 with V, 5 K-only).  Rings of >= 5 stages
+// with V run one CTA per SM.
+template <int MODE, int STG = 0>
 struct DecodeCfg {
   static constexpr bool kHasV = MODE != MODE_SCORES;
-  static constexpr int kStages = kHasV ? 3 : 5;
+  static constexpr int kStages = STG ? STG : (kHasV ? 3 : 5);
   static constexpr int kStageBytes = kHasV ? 2 * kTileBytes : kTileBytes;
   static constexpr int kPipeBytes = kStages * kStageBytes;
   // merge scratch reuses the ring: 4 warps x 16 rows x (128 + 2) floats
   static constexpr int kMergeBytes = 4 * 16 * (kHeadDim + 2) * 4;
   static constexpr int kSmemBytes = kPipeBytes > kMergeBytes ? kPipeBytes : kMergeBytes;
+  static constexpr int kMinBlocks = (kHasV && kStages >= 5) ? 1 : 2;
 };
 
-template <int MODE, bool G16>
-__global__ void __launch_bounds__(kThreads, 2) decode_attn_kernel(const DecodeArgs a) {
-  using Cfg = DecodeCfg<MODE>;
+template <int MODE, bool G16, int STG>
+__global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
+    decode_attn_kernel(const DecodeArgs a) {
+  using Cfg = DecodeCfg<MODE, STG>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -327,27 +333,32 @@ __global__ void __launch_bounds__(kThreads, 2) decode_attn_kernel(const DecodeAr
   }
 }
 
-template <int MODE>
+template <int MODE, int STG = 0>
 static cudaError_t launch_mode(const DecodeArgs& a, cudaStream_t st) {
-  using Cfg = DecodeCfg<MODE>;
+  using Cfg = DecodeCfg<MODE, STG>;
   dim3 grid(a.splits, a.Hkv, a.B);
   const int smem = Cfg::kSmemBytes;
   // one-time opt-in to >48 KB dynamic shared memory per instantiation
   static const cudaError_t attr_hi = cudaFuncSetAttribute(
-      decode_attn_kernel<MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      decode_attn_kernel<MODE, true, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   static const cudaError_t attr_lo = cudaFuncSetAttribute(
-      decode_attn_kernel<MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      decode_attn_kernel<MODE, false, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (attr_hi != cudaSuccess) return attr_hi;
   if (attr_lo != cudaSuccess) return attr_lo;
-  if (a.G > 8) decode_attn_kernel<MODE, true><<<grid, kThreads, smem, st>>>(a);
-  else decode_attn_kernel<MODE, false><<<grid, kThreads, smem, st>>>(a);
+  if (a.G > 8) decode_attn_kernel<MODE, true, STG><<<grid, kThreads, smem, st>>>(a);
+  else decode_attn_kernel<MODE, false, STG><<<grid, kThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_decode_attn(int mode, const DecodeArgs& a, cudaStream_t st) {
+  // KSCD_SPARSE_STAGES (dev knob): ring depth of the gather kernel
+  static const int sparse_stages = getenv("KSCD_SPARSE_STAGES") ? atoi(getenv("KSCD_SPARSE_STAGES")) : 3;
   switch (mode) {
     case MODE_DENSE: return launch_mode<MODE_DENSE>(a, st);
-    case MODE_SPARSE: return launch_mode<MODE_SPARSE>(a, st);
+    case MODE_SPARSE:
+      if (sparse_stages == 6) return launch_mode<MODE_SPARSE, 6>(a, st);
+      if (sparse_stages == 4) return launch_mode<MODE_SPARSE, 4>(a, st);
+      return launch_mode<MODE_SPARSE>(a, st);
     default: return launch_mode<MODE_SCORES>(a, st);
   }
 }
