@@ -358,6 +358,7 @@ cudaError_t launch_decode_attn(int mode, const DecodeArgs& a, cudaStream_t st) {
     case MODE_SPARSE:
       if (sparse_stages == 6) return launch_mode<MODE_SPARSE, 6>(a, st);
       if (sparse_stages == 4) return launch_mode<MODE_SPARSE, 4>(a, st);
+      if (sparse_stages == 2) return launch_mode<MODE_SPARSE, 2>(a, st);
       return launch_mode<MODE_SPARSE>(a, st);
     default: return launch_mode<MODE_SCORES>(a, st);
   }
