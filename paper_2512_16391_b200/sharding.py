@@ -59,6 +59,17 @@ def kv_head_shard(num_kv_heads: int, group=None) -> Tuple[int, int]:
     return rank * per, (rank + 1) * per
 
 
+def _all_gather_dim0(x: torch.Tensor, world: int, group) -> torch.Tensor:
+    """all_gather_into_tensor along dim 0; CUDA tensors on a gloo group are
+    staged through host memory (gloo has no CUDA all-gather), which lets the
+    multi-process tests share one GPU."""
+    stage = x.is_cuda and dist.get_backend(group) == "gloo"
+    src = x.cpu() if stage else x
+    out = torch.empty((world * src.shape[0],) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+    dist.all_gather_into_tensor(out, src.contiguous(), group=group)
+    return out.to(x.device) if stage else out
+
+
 def gather_index_lists(local_idx: torch.Tensor, local_cnt: torch.Tensor, group=None,
                        head_dim: int = 1) -> Tuple[torch.Tensor, torch.Tensor]:
     """All-gather per-kv-head index lists along ``head_dim`` so every rank
@@ -72,10 +83,7 @@ def gather_index_lists(local_idx: torch.Tensor, local_cnt: torch.Tensor, group=N
         return local_idx, local_cnt
 
     def cat(t: torch.Tensor) -> torch.Tensor:
-        moved = t.movedim(head_dim, 0).contiguous()
-        out = torch.empty((world * moved.shape[0],) + tuple(moved.shape[1:]), dtype=t.dtype, device=t.device)
-        dist.all_gather_into_tensor(out, moved, group=group)
-        return out.movedim(0, head_dim).contiguous()
+        return _all_gather_dim0(t.movedim(head_dim, 0), world, group).movedim(0, head_dim).contiguous()
 
     return cat(local_idx), cat(local_cnt)
 
@@ -86,10 +94,7 @@ def gather_head_outputs(local_out: torch.Tensor, group=None, head_dim: int = 1) 
     world, _ = _world(group)
     if world == 1:
         return local_out
-    moved = local_out.movedim(head_dim, 0).contiguous()
-    out = torch.empty((world * moved.shape[0],) + tuple(moved.shape[1:]), dtype=moved.dtype, device=moved.device)
-    dist.all_gather_into_tensor(out, moved, group=group)
-    return out.movedim(0, head_dim)
+    return _all_gather_dim0(local_out.movedim(head_dim, 0), world, group).movedim(0, head_dim)
 
 
 def local_head_map(head_map, g0: int, g1: int, device=None) -> torch.Tensor:
@@ -155,3 +160,57 @@ class ShardedKascadeDecoder:
     def gather_outputs(self) -> torch.Tensor:
         """[L][B][Hq][d] reassembled from every rank's heads."""
         return gather_head_outputs(self.local.out, self.group, head_dim=2)
+
+
+class ShardedKascadePrefill:
+    """KV-head-sharded prefill executor (one rank's share; SURVEY.md 8(e)
+    prefill partitioning).  Each anchor layer selects on the local kv heads
+    and all-gathers its per-(kv head, tile) lists (<= 205 MiB per layer at
+    128K over 8 heads); reuse layers gather through the GLOBAL head map."""
+
+    def __init__(self, plan, num_layers: int, num_q_heads: int, num_kv_heads: int, seq_len: int, group=None,
+                 device=None):
+        from . import engine
+        from .host_types import KIND_REUSE, MODE_ALL_HEADS_POOLED, k_budget, validate_plan
+        validate_plan(plan, num_layers, num_kv_heads)
+        if plan.mode == MODE_ALL_HEADS_POOLED:
+            raise InvalidArgumentError("all-heads-pooled mode needs every kv head's pooled vectors; "
+                                       "use q-tile or batch partitioning (SURVEY.md 8(e) mode caveat)")
+        self.group = group
+        self.g0, self.g1 = kv_head_shard(num_kv_heads, group)
+        self.G = num_q_heads // num_kv_heads
+        self.Hkv, self.Hloc = num_kv_heads, self.g1 - self.g0
+        self.local = engine.KascadePrefill(plan, num_layers, self.Hloc * self.G, self.Hloc, seq_len, device=device)
+        dev = self.local.device
+        self.kinds = self.local.kinds
+        self.maps = {l: local_head_map(plan.head_maps[l].map, self.g0, self.g1, dev)
+                     for l, kind in enumerate(self.kinds) if kind == KIND_REUSE}
+        self.own = torch.arange(self.g0, self.g1, dtype=torch.int32, device=dev)
+        T = self.local.indices.shape[1]
+        kc = k_budget(plan.k_policy, seq_len)
+        self.full_idx = torch.empty(num_kv_heads, T, kc, dtype=torch.int32, device=dev)
+        self.full_cnt = torch.zeros(num_kv_heads, T, dtype=torch.int32, device=dev)
+
+    def forward(self, qs, ks, vs) -> torch.Tensor:
+        """qs/ks/vs: this rank's head slices per layer ([Hq_loc][N][128] and
+        [Hloc][N][128]).  Returns the local outputs [L][Hq_loc][N][128]."""
+        from . import ops
+        from .host_types import KIND_ANCHOR, KIND_ANCHOR0, KIND_REUSE
+        loc = self.local
+        pol = loc.plan.k_policy
+        for l, kind in enumerate(self.kinds):
+            q, k, v = qs[l], ks[l], vs[l]
+            if kind == KIND_REUSE:
+                ops.sparse_prefill(q, k, v, self.full_idx, self.full_cnt, self.maps[l], out=loc.out[l])
+                continue
+            if kind == KIND_ANCHOR0:
+                ops.dense_prefill(q, k, v, out=loc.out[l], lse=loc.lse)
+            else:
+                ops.anchor_lse_prefill(q, k, lse=loc.lse)
+            ops.select_prefill(q, k, loc.lse, pol, indices=loc.indices, counts=loc.counts, pooled=loc.pooled)
+            idx, cnt = gather_index_lists(loc.indices, loc.counts, self.group, head_dim=0)
+            self.full_idx.copy_(idx)
+            self.full_cnt.copy_(cnt)
+            if kind == KIND_ANCHOR:
+                ops.sparse_prefill(q, k, v, self.full_idx, self.full_cnt, self.own, out=loc.out[l])
+        return loc.out

@@ -1,0 +1,89 @@
+"""KV-head-sharded decode and prefill executors with a real 2-process group
+(gloo, both ranks on cuda:0): the anchor index lists cross ranks through the
+all-gather, reuse heads gather through the global head map, and the
+reassembled outputs match the unsharded engine.  Needs a B200."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, errq):
+    import torch.distributed as dist
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from oracle import kascade_oracle as orc
+        from paper_2512_16391_b200 import engine, sharding
+        from paper_2512_16391_b200.host_types import AnchorPlan, AnchorPlanCore, HeadMap, KBudgetPolicy
+        L, B, Hq, Hkv, n = 3, 2, 8, 4, 1200
+        G = Hq // Hkv
+        plan = AnchorPlan(AnchorPlanCore([0, 2], 2, 0.0), head_maps={1: HeadMap(1, 0, [2, 0, 3, 1])},
+                          k_policy=KBudgetPolicy(0.1, 64))
+        rng = np.random.default_rng(5)
+        q = orc.bf16_round((rng.standard_normal((L, B, Hq, 128)) * 2).astype(np.float32))
+        K = orc.bf16_round(rng.standard_normal((L, B, Hkv, n, 128)).astype(np.float32))
+        V = orc.bf16_round(rng.standard_normal((L, B, Hkv, n, 128)).astype(np.float32))
+        t = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)  # noqa: E731
+        g0, g1 = sharding.kv_head_shard(Hkv)
+        dec = sharding.ShardedKascadeDecoder(plan, L, B, Hq, Hkv, n)
+        dec.step(t(q[:, :, g0 * G:g1 * G]), [t(K[l][:, g0:g1]) for l in range(L)],
+                 [t(V[l][:, g0:g1]) for l in range(L)], n)
+        full = dec.gather_outputs().cpu().numpy()
+        if rank == 0:
+            ref = engine.KascadeDecoder(plan, L, B, Hq, Hkv, n)
+            want = ref.step(t(q), [t(K[l]) for l in range(L)], [t(V[l]) for l in range(L)], n).cpu().numpy()
+            err = np.abs(full - want).max()
+            assert err < 2e-3, f"sharded decode differs from unsharded by {err}"
+        # prefill: [L][H][N][d]
+        N = 600
+        Qp = orc.bf16_round(rng.standard_normal((L, Hq, N, 128)).astype(np.float32))
+        Kp = orc.bf16_round(rng.standard_normal((L, Hkv, N, 128)).astype(np.float32))
+        Vp = orc.bf16_round(rng.standard_normal((L, Hkv, N, 128)).astype(np.float32))
+        pf = sharding.ShardedKascadePrefill(plan, L, Hq, Hkv, N)
+        loc = pf.forward([t(Qp[l, g0 * G:g1 * G]) for l in range(L)], [t(Kp[l, g0:g1]) for l in range(L)],
+                         [t(Vp[l, g0:g1]) for l in range(L)])
+        allp = sharding.gather_head_outputs(loc, head_dim=1).float().cpu().numpy()
+        if rank == 0:
+            ref = engine.KascadePrefill(plan, L, Hq, Hkv, N)
+            want = ref.forward([t(Qp[l]) for l in range(L)], [t(Kp[l]) for l in range(L)],
+                               [t(Vp[l]) for l in range(L)]).float().cpu().numpy()
+            err = np.abs(allp - want).max()
+            assert err < 2e-2, f"sharded prefill differs from unsharded by {err}"
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # reported to the parent
+        errq.put(f"rank {rank}: {type(e).__name__}: {e}")
+        raise
+
+
+def test_kv_head_sharded_executors_match_unsharded(cuda_ok):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    errq = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, errq)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    msgs = []
+    while not errq.empty():
+        msgs.append(errq.get())
+    assert not msgs, msgs
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
