@@ -34,8 +34,9 @@ def layer_kinds(plan, num_layers: int) -> List[str]:
 
 class KascadeDecoder:
     def __init__(self, plan, num_layers: int, batch: int, num_q_heads: int, num_kv_heads: int,
-                 max_seq_len: int, device=None):
-        validate_plan(plan, num_layers, num_kv_heads)
+                 max_seq_len: int, device=None, validate: bool = True):
+        if validate:   # sharded executors validate against the GLOBAL head count themselves
+            validate_plan(plan, num_layers, num_kv_heads)
         if plan.pooling != POOL_POST:
             raise InvalidArgumentError("decode engine implements post-softmax pooling (the paper's mode)")
         self.plan = plan
@@ -124,8 +125,10 @@ class KascadePrefill:
 
     ``dense_forward`` is the Top-k = 100% baseline over the same layers."""
 
-    def __init__(self, plan, num_layers: int, num_q_heads: int, num_kv_heads: int, seq_len: int, device=None):
-        validate_plan(plan, num_layers, num_kv_heads)
+    def __init__(self, plan, num_layers: int, num_q_heads: int, num_kv_heads: int, seq_len: int, device=None,
+                 validate: bool = True):
+        if validate:   # sharded executors validate against the GLOBAL head count themselves
+            validate_plan(plan, num_layers, num_kv_heads)
         if plan.pooling != POOL_POST:
             raise InvalidArgumentError("prefill engine implements post-softmax pooling (the paper's mode)")
         if plan.tile_size != ops.TILE:

@@ -124,7 +124,7 @@ class ShardedKascadeDecoder:
         self.G = num_q_heads // num_kv_heads
         self.Hkv, self.Hloc = num_kv_heads, self.g1 - self.g0
         self.local = engine.KascadeDecoder(plan, num_layers, batch, self.Hloc * self.G, self.Hloc, max_seq_len,
-                                           device=device)
+                                           device=device, validate=False)
         dev = self.local.device
         self.kinds = self.local.kinds
         self.maps = {l: local_head_map(plan.head_maps[l].map, self.g0, self.g1, dev)
@@ -180,7 +180,8 @@ class ShardedKascadePrefill:
         self.g0, self.g1 = kv_head_shard(num_kv_heads, group)
         self.G = num_q_heads // num_kv_heads
         self.Hkv, self.Hloc = num_kv_heads, self.g1 - self.g0
-        self.local = engine.KascadePrefill(plan, num_layers, self.Hloc * self.G, self.Hloc, seq_len, device=device)
+        self.local = engine.KascadePrefill(plan, num_layers, self.Hloc * self.G, self.Hloc, seq_len, device=device,
+                                           validate=False)
         dev = self.local.device
         self.kinds = self.local.kinds
         self.maps = {l: local_head_map(plan.head_maps[l].map, self.g0, self.g1, dev)
