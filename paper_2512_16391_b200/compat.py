@@ -53,6 +53,8 @@ def _layer(trace, layer: int):
     if trace.head_dim != 128:
         raise UnsupportedOperationError(f"head_dim {trace.head_dim} unsupported (engine is d=128)")
     dev = _dev()
+    if hasattr(trace, "layer_device"):          # kscd_io.TraceFile: stream from the mmap
+        return trace.layer_device(layer, dev)
     to = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev).to(torch.bfloat16)  # noqa
     return to(trace.Q[layer]), to(trace.K[layer]), to(trace.V[layer])
 

@@ -207,6 +207,80 @@ def main():
                         pre_rel=np.array([r.output_rel_err_l2 for r in rep_p.per_layer]),
                         pre_mass=np.array([r.mass_recovered_mean for r in rep_p.per_layer]))
 
+    # 8. trace I/O and the `run` CLI (traceio.py:44-156, cli.py:216-233).
+    #    conformance_v1.kscd is the reference's own conformance trace
+    #    (test_traceio.py:39-40 pins its sha256); the CLI cases run the
+    #    reference `kascade run` on traces written by the reference writer and
+    #    freeze its report JSON and stdout.  The GPU tests regenerate the same
+    #    trace bytes with the oracle generator + our writer (sha-checked).
+    import contextlib
+    import io
+    import tempfile
+    from kascade import cli as ref_cli
+    from kascade import traceio as ref_io
+    cfg = ref.SynthConfig(num_layers=2, num_query_heads=2, num_kv_heads=1, head_dim=4, seq_len=3, seed=42,
+                          layer_correlation=0.5, include_xy=True, prompt_id="conformance-v1")
+    conf = os.path.join(HERE, "conformance_v1.kscd")
+    ref_io.write_trace(conf, ref.generate_synthetic(cfg))
+    with open(conf, "rb") as f:
+        meta["conformance_sha256"] = hashlib.sha256(f.read()).hexdigest()
+    # format-error messages and offsets of the reference reader on corrupted copies
+    with open(conf, "rb") as f:
+        good = f.read()
+    corrupt = {"magic": b"NOPE" + good[4:], "version": good[:4] + (999).to_bytes(2, "little") + good[6:],
+               "dtype": good[:26] + bytes([7]) + good[27:], "truncated": good[:-5], "header": b"KSCD\x01",
+               "trailing": good + b"xx", "heads": good[:10] + (3).to_bytes(4, "little") + good[14:],
+               "zero_dim": good[:6] + (0).to_bytes(4, "little") + good[10:],
+               "prompt_utf8": good[:28] + b"\xff" + good[29:]}
+    errs = {}
+    with tempfile.TemporaryDirectory() as td:
+        for name, blob in corrupt.items():
+            p = os.path.join(td, name + ".kscd")
+            with open(p, "wb") as f:
+                f.write(blob)
+            try:
+                ref_io.read_trace(p)
+                errs[name] = None
+            except ref.FormatError as e:
+                errs[name] = {"message": str(e), "offset": e.offset}
+        cli_cases = {}
+        c = dict(L=4, Hq=8, Hkv=2, d=128, N=512, seed=3, rho=0.9, perms=[[0, 1], [1, 0], [1, 0], [0, 1]])
+        g = ref.generate_synthetic(ref.SynthConfig(num_layers=c["L"], num_query_heads=c["Hq"],
+                                                   num_kv_heads=c["Hkv"], head_dim=c["d"], seq_len=c["N"],
+                                                   seed=c["seed"], layer_correlation=c["rho"],
+                                                   head_permutations=c["perms"], prompt_id="cli-small"))
+        t = trace_of(*(orc.bf16_round(x) for x in (g.Q, g.K, g.V)), pid="cli-small")
+        tpath = os.path.join(td, "t.kscd")
+        ref_io.write_trace(tpath, t)
+        with open(tpath, "rb") as f:
+            trace_sha = hashlib.sha256(f.read()).hexdigest()
+        anchors = [0, 2]
+        maps = ref.compute_head_maps(t, anchors, k=32)
+        for tile in (128, 32):
+            core = ref.AnchorPlanCore(anchors=anchors, budget=2, objective_value=0.0)
+            plan = ref.AnchorPlan(core=core, head_maps=maps, k_policy=ref.KBudgetPolicy(0.1, 16), tile_size=tile)
+            ppath = os.path.join(HERE, f"cli_plan_t{tile}.json")
+            ref_io.write_plan(ppath, plan)
+            for phase, mode in (("prefill", None), ("prefill", "all-heads-pooled"), ("decode", None)):
+                if tile == 32 and mode is not None:
+                    continue
+                rpath = os.path.join(td, "r.json")
+                argv = ["run", "--trace", tpath, "--plan", ppath, "--phase", phase, "--out", rpath]
+                if mode:
+                    argv += ["--mode", mode]
+                buf = io.StringIO()
+                with contextlib.redirect_stdout(buf):
+                    code = ref_cli.main(argv)
+                with open(rpath) as f:
+                    rep = json.load(f)
+                cli_cases[f"t{tile}_{phase}_{mode or 'remapped'}"] = {
+                    "plan": os.path.basename(ppath), "phase": phase, "mode": mode, "exit": code,
+                    "report": rep, "stdout": buf.getvalue()}
+    with open(os.path.join(HERE, "cli_cases.json"), "w") as f:
+        json.dump({"trace_args": c, "trace_prompt_id": "cli-small", "trace_sha256": trace_sha,
+                   "format_errors": errs, "cases": cli_cases}, f, indent=1, sort_keys=True)
+        f.write("\n")
+
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(meta, f, indent=1, sort_keys=True)
         f.write("\n")
