@@ -178,6 +178,18 @@ typedef struct kscd_pool_tiles_params {
   double* scratch;              /* pre: fp64 [Hkv][T][pooled_stride] */
 } kscd_pool_tiles_params;
 
+/* Decode-step KV append (engine plumbing for serving decode; the reference
+ * reads whole traces and has no cache): writes the step's new K/V rows of
+ * every layer at cache row `position` in one launch. */
+typedef struct kscd_append_kv_params {
+  int32_t num_layers, batch, num_kv_heads, head_dim;
+  int32_t position;             /* cache row written, < cache capacity */
+  const void* kv_new;           /* bf16 [L][2][B][Hkv][128], 16-byte aligned */
+  void* const* k_caches;        /* device array of L pointers, bf16 [B][Hkv][n_cap][128] */
+  void* const* v_caches;
+  int64_t kv_stride_batch, kv_stride_head;   /* elements, shared by every layer's cache */
+} kscd_append_kv_params;
+
 int kscd_abi_version(void);
 const char* kscd_last_error(void);
 
@@ -230,6 +242,8 @@ int kscd_dense_probs(const kscd_probs_params* p, void* stream);
  * post-softmax _post_pooled (runner.py:148-152, fp64 sums) or pre-softmax
  * _pre_pooled (runner.py:155-161). */
 int kscd_pool_tiles(const kscd_pool_tiles_params* p, void* stream);
+
+int kscd_append_kv(const kscd_append_kv_params* p, void* stream);
 
 /* k_budget (tiles.py:81-89): min(max(floor(fraction*n), k_min), n). */
 int32_t kscd_k_budget(double fraction, int32_t k_min, int32_t n);

@@ -95,6 +95,14 @@ class PoolTilesParams(ctypes.Structure):
     ]
 
 
+class AppendKvParams(ctypes.Structure):
+    _fields_ = [
+        ("num_layers", c_i32), ("batch", c_i32), ("num_kv_heads", c_i32), ("head_dim", c_i32),
+        ("position", c_i32), ("kv_new", c_vp), ("k_caches", c_vp), ("v_caches", c_vp),
+        ("kv_stride_batch", c_i64), ("kv_stride_head", c_i64),
+    ]
+
+
 # entry point name -> params struct (None for non-struct signatures)
 ENTRY_POINTS = {
     "kscd_dense_decode": DecodeParams,
@@ -108,6 +116,7 @@ ENTRY_POINTS = {
     "kscd_select_prefill": SelectPrefillParams,
     "kscd_dense_probs": ProbsParams,
     "kscd_pool_tiles": PoolTilesParams,
+    "kscd_append_kv": AppendKvParams,
 }
 
 _lock = threading.Lock()

@@ -438,3 +438,24 @@ extern "C" int kscd_select_prefill(const kscd_select_prefill_params* p, void* st
 }
 
 }  // extern "C"
+
+extern "C" int kscd_append_kv(const kscd_append_kv_params* p, void* stream) {
+  if (!p) return fail(KSCD_INVALID_ARGUMENT, "params is NULL");
+  if (p->head_dim != 128) return fail(KSCD_UNSUPPORTED, "head_dim %d unsupported", p->head_dim);
+  if (p->num_layers < 1 || p->batch < 1 || p->num_kv_heads < 1 || p->position < 0)
+    return fail(KSCD_INVALID_ARGUMENT, "bad shape");
+  if (!p->kv_new || !p->k_caches || !p->v_caches) return fail(KSCD_INVALID_ARGUMENT, "NULL buffer");
+  if (((uintptr_t)p->kv_new & 15) || (p->kv_stride_batch & 7) || (p->kv_stride_head & 7))
+    return fail(KSCD_INVALID_ARGUMENT, "kv_new and cache strides must be 16-byte aligned");
+  kscd::AppendKvArgs a{};
+  a.L = p->num_layers;
+  a.B = p->batch;
+  a.Hkv = p->num_kv_heads;
+  a.pos = p->position;
+  a.kv_new = (const __nv_bfloat16*)p->kv_new;
+  a.k_caches = (__nv_bfloat16* const*)p->k_caches;
+  a.v_caches = (__nv_bfloat16* const*)p->v_caches;
+  a.stride_b = p->kv_stride_batch;
+  a.stride_h = p->kv_stride_head;
+  return cuda_status(kscd::launch_append_kv(a, (cudaStream_t)stream), "kscd_append_kv");
+}

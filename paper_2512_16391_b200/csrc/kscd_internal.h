@@ -138,4 +138,13 @@ struct PoolRowsArgs {
 };
 cudaError_t launch_pool_rows(const PoolRowsArgs& a, cudaStream_t st);
 
+struct AppendKvArgs {
+  int L, B, Hkv, pos;
+  const __nv_bfloat16* kv_new;            // [L][2][B][Hkv][128]
+  __nv_bfloat16* const* k_caches;         // device [L] pointers, rows b*stride_b + h*stride_h + j*128
+  __nv_bfloat16* const* v_caches;
+  int64_t stride_b, stride_h;             // elements
+};
+cudaError_t launch_append_kv(const AppendKvArgs& a, cudaStream_t st);
+
 }  // namespace kscd

@@ -114,6 +114,36 @@ class KascadeDecoder:
         self._graphs[(seq_len, dense)] = g
         return g
 
+    def capture_host_step(self, q_host, kv_host, out_host, q, k_caches, v_caches, seq_len: int,
+                          dense: bool = False) -> torch.cuda.CUDAGraph:
+        """A whole serving decode step from and to pinned host memory as ONE
+        CUDA graph: H2D of the step's queries (``q_host`` [L][B][Hq][128]) and
+        new K/V rows (``kv_host`` [L][2][B][Hkv][128]), one append launch that
+        writes the rows at cache position ``seq_len - 1`` of every layer, the
+        layer loop, and D2H of the outputs into ``out_host`` [L][B][Hq][128]
+        fp32.  Replay, then synchronise the stream before reading out_host."""
+        for t, name in ((q_host, "q_host"), (kv_host, "kv_host"), (out_host, "out_host")):
+            if t.is_cuda or not t.is_pinned():
+                raise InvalidArgumentError(f"{name} must be pinned host memory")
+        kv_dev = torch.empty(kv_host.shape, dtype=torch.bfloat16, device=self.device)
+        tables = ops.cache_pointer_tables(k_caches, v_caches, self.device)
+        fn = self.dense_step if dense else self.step
+
+        def body():
+            q.copy_(q_host, non_blocking=True)
+            kv_dev.copy_(kv_host, non_blocking=True)
+            ops.append_kv(kv_dev, seq_len - 1, tables)
+            fn(q, k_caches, v_caches, seq_len)
+            out_host.copy_(self.out, non_blocking=True)
+
+        body()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            body()
+        self._graphs[("host", seq_len, dense)] = (g, kv_dev, tables)   # keep the staging alive
+        return g
+
 
 class KascadePrefill:
     """Prefill executor over every layer of a plan (batch 1, tiles of 128

@@ -263,6 +263,35 @@ def reuse_decode(q, k_cache, v_cache, seq_len, indices, counts, head_map=None, *
     return sparse_decode(q, k_cache, v_cache, seq_len, indices, counts, head_map, out=out)
 
 
+def cache_pointer_tables(k_caches, v_caches, device) -> Tuple[torch.Tensor, torch.Tensor, int, int]:
+    """Device pointer tables of per-layer caches for ``append_kv``; every
+    layer's cache must share one shape and stride layout."""
+    ref = k_caches[0]
+    for t in list(k_caches) + list(v_caches):
+        _need_cuda(t, "cache")
+        if t.dtype != torch.bfloat16 or t.shape != ref.shape or t.stride() != ref.stride() or t.stride(3) != 1 \
+                or t.stride(2) != HEAD_DIM:
+            raise InvalidArgumentError("caches must be bf16 [B][Hkv][n_cap][128] with one shared stride layout")
+    kp = torch.tensor([t.data_ptr() for t in k_caches], dtype=torch.int64, device=device)
+    vp = torch.tensor([t.data_ptr() for t in v_caches], dtype=torch.int64, device=device)
+    return kp, vp, ref.stride(0), ref.stride(1)
+
+
+def append_kv(kv_new: torch.Tensor, position: int, tables) -> None:
+    """Write the step's new rows (bf16 [L][2][B][Hkv][128], device) into
+    every layer's cache at row ``position`` with one launch."""
+    kp, vp, sb, sh = tables
+    _need_cuda(kv_new, "kv_new")
+    if kv_new.dtype != torch.bfloat16 or kv_new.dim() != 5 or kv_new.shape[1] != 2 or kv_new.shape[4] != HEAD_DIM \
+            or not kv_new.is_contiguous() or kv_new.shape[0] != kp.numel():
+        raise InvalidArgumentError("kv_new must be contiguous bf16 [L][2][B][Hkv][128]")
+    L, _, B, Hkv, _ = kv_new.shape
+    p = _lib.AppendKvParams(num_layers=L, batch=B, num_kv_heads=Hkv, head_dim=HEAD_DIM, position=position,
+                            kv_new=kv_new.data_ptr(), k_caches=kp.data_ptr(), v_caches=vp.data_ptr(),
+                            kv_stride_batch=sb, kv_stride_head=sh)
+    _lib.call("kscd_append_kv", p, _stream())
+
+
 def default_scale() -> float:
     return 1.0 / math.sqrt(HEAD_DIM)
 

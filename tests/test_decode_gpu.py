@@ -256,3 +256,37 @@ def test_decode_engine_llama_shapes_vs_oracle(cuda_ok):
     for b in range(B):
         Y, _, _ = orc.decode_step(q[:, b], K[:, b], V[:, b], [0, 2], {1: hm}, 0.025, 128, want_mass=False)
         assert_outputs_close(out[:, b], Y)
+
+
+def test_host_step_graph_appends_and_matches_step(cuda_ok):
+    """capture_host_step (pinned H2D + one-launch KV append + layer loop +
+    D2H as one CUDA graph) equals appending by hand and running step(); the
+    appended rows land bit-exactly at position n-1 of every layer."""
+    from paper_2512_16391_b200 import engine
+    from paper_2512_16391_b200.host_types import AnchorPlan, AnchorPlanCore, HeadMap, KBudgetPolicy
+    L, B, Hq, Hkv, n, n_cap = 3, 2, 8, 2, 700, 768
+    plan = AnchorPlan(AnchorPlanCore([0, 2], 2, 0.0), head_maps={1: HeadMap(1, 0, [1, 0])},
+                      k_policy=KBudgetPolicy(0.1, 16))
+    g = torch.Generator(device="cuda").manual_seed(5)
+    Ks = [torch.randn(B, Hkv, n_cap, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(L)]
+    Vs = [torch.randn(B, Hkv, n_cap, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(L)]
+    q_host = torch.randn(L, B, Hq, 128).to(torch.bfloat16).pin_memory()
+    kv_host = torch.randn(L, 2, B, Hkv, 128).to(torch.bfloat16).pin_memory()
+    out_host = torch.zeros(L, B, Hq, 128).pin_memory()
+    Kr = [x.clone() for x in Ks]
+    Vr = [x.clone() for x in Vs]
+    dec = engine.KascadeDecoder(plan, L, B, Hq, Hkv, n_cap)
+    q = torch.empty(L, B, Hq, 128, dtype=torch.bfloat16, device="cuda")
+    graph = dec.capture_host_step(q_host, kv_host, out_host, q, Ks, Vs, n)
+    out_host.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    for l in range(L):
+        assert torch.equal(Ks[l][:, :, n - 1].cpu(), kv_host[l, 0]) and torch.equal(Vs[l][:, :, n - 1].cpu(), kv_host[l, 1])
+        assert torch.equal(Ks[l][:, :, :n - 1], Kr[l][:, :, :n - 1])
+        assert torch.equal(Ks[l][:, :, n:], Kr[l][:, :, n:])
+        Kr[l][:, :, n - 1] = kv_host[l, 0].cuda()
+        Vr[l][:, :, n - 1] = kv_host[l, 1].cuda()
+    ref = engine.KascadeDecoder(plan, L, B, Hq, Hkv, n_cap)
+    want = ref.step(q_host.cuda(), Kr, Vr, n).cpu()
+    assert torch.equal(out_host, want)
