@@ -452,3 +452,156 @@ def prefill_tile_select(Ql, Kl, g: int, G: int, start: int, end: int, fraction: 
     else:
         pooled = pooled_pre(Ql, Kl, g, G, start, end)
     return topk_sorted(pooled, k_budget(fraction, k_min, end)), pooled
+
+
+# --------------------------------------------------------------------------
+# offline calibration: head similarity / head maps (heads.py:50-143,
+# pipeline.py:31-73) and the layer similarity matrix (metrics.py:105-335)
+# --------------------------------------------------------------------------
+
+def group_mean(P: np.ndarray, G: int) -> np.ndarray:
+    """heads.py:50-59: per-kv-head distributions, the fp64 mean of the
+    group's G query-head rows, stored as fp32 -> [Hkv][N][N]."""
+    Hq, N, M = P.shape
+    return P.reshape(Hq // G, G, N, M).mean(axis=1, dtype=np.float64).astype(np.float32)
+
+
+def token_sets(D: np.ndarray, k: int):
+    """Per-token Top-k of causal rows (ranking.py:14-25 + the row-r support
+    mask of heads.py:92-94 / metrics.py:133-149): positions ordered by
+    (value desc, index asc), the first min(k, r+1) valid.  D [..][N][N] ->
+    (idx [..][N][take], valid [N][take])."""
+    N = D.shape[-1]
+    take = min(k, N)
+    idx = np.argsort(-D, axis=-1, kind="stable")[..., :take]
+    valid = np.arange(take)[None, :] < np.minimum(np.arange(N) + 1, take)[:, None]
+    return idx, valid
+
+
+def masked_mass(D: np.ndarray, idx: np.ndarray, valid: np.ndarray) -> np.ndarray:
+    """fp64 sum of D[row][idx[row][t]] over valid t: [..][N][N] -> [..][N]."""
+    got = np.take_along_axis(D.astype(np.float64), np.where(valid, idx, 0), axis=-1)
+    return np.where(valid, got, 0.0).sum(axis=-1)
+
+
+def _agg(scores: np.ndarray, how: str) -> float:
+    if scores.size == 0:
+        return 0.0
+    return float(scores.mean(dtype=np.float64)) if how == "mean" else float(scores.min())
+
+
+def head_similarity_dists(idx_a: np.ndarray, Db: np.ndarray, k: int, how: str = "mean") -> np.ndarray:
+    """heads.py:67-108: hs[i][j] = token aggregate of mass(Db_j on anchor
+    head i's per-token sets) / mass(Db_j on its own sets), fp32 per token."""
+    Hkv = Db.shape[0]
+    idx_b, valid = token_sets(Db, k)
+    hs = np.zeros((Hkv, Hkv), np.float64)
+    for j in range(Hkv):
+        den = masked_mass(Db[j], idx_b[j], valid)
+        ok = den != 0.0
+        for i in range(Hkv):
+            num = masked_mass(Db[j], idx_a[i], valid)
+            hs[i, j] = _agg((num[ok] / den[ok]).astype(np.float32), how)
+    return hs
+
+
+def layer_group_dists(Q, K, V, layer: int) -> np.ndarray:
+    P, _ = dense_layer(Q[layer], K[layer], V[layer])
+    return group_mean(P, Q.shape[1] // K.shape[1])
+
+
+def head_similarity(Q, K, V, a: int, b: int, k: int = 64, how: str = "mean") -> np.ndarray:
+    """heads.py:111-126 for one trace."""
+    Da = layer_group_dists(Q, K, V, a)
+    Db = Da if a == b else layer_group_dists(Q, K, V, b)
+    return head_similarity_dists(token_sets(Da, k)[0], Db, k, how)
+
+
+def head_maps(Q, K, V, anchors: Sequence[int], k: int = 64) -> Dict[int, List[int]]:
+    """pipeline.py:31-73 (remapped mode): for each reuse layer, argmax over
+    anchor heads (first maximum) of its similarity column against the most
+    recent anchor.  Returns {layer: map}."""
+    L = Q.shape[0]
+    anchors = sorted(set(anchors))
+    out = {}
+    for n, a in enumerate(anchors):
+        end = anchors[n + 1] if n + 1 < len(anchors) else L
+        if a + 1 >= end:
+            continue
+        idx_a = token_sets(layer_group_dists(Q, K, V, a), k)[0]
+        for b in range(a + 1, end):
+            hs = head_similarity_dists(idx_a, layer_group_dists(Q, K, V, b), k)
+            out[b] = [int(x) for x in hs.argmax(axis=0)]
+    return out
+
+
+def planning_matrix(Q, K, V, k: int = 64, how: str = "mean", tile: int = 128, phase: str = "prefill"):
+    """metrics.py:226-295: per-(kv head, tile) pooled distributions (fp64)
+    and their Top-k sets per layer; S[a][b] aggregates, over tiles, the mean
+    over reuse heads j of mass(b, j on a's set of head map[j]) / mass(b, j on
+    its own set), the head map maximising the tile-mean per-head score.
+    Returns (S fp32 [L][L], undefined count)."""
+    L, Hq = Q.shape[0], Q.shape[1]
+    Hkv, N = K.shape[1], Q.shape[2]
+    G = Hq // Hkv
+    tiles = prefill_tiles(N, tile) if phase == "prefill" else decode_tiles(N)
+    dist, sets, den = [], [], []
+    for layer in range(L):
+        P, _ = dense_layer(Q[layer], K[layer], V[layer])
+        dl, sl, nl = {}, {}, {}
+        for g in range(Hkv):
+            for s, e, t in tiles:
+                w = pooled_post(P, g, G, s, e)
+                chosen = np.argsort(-w, kind="stable")[:min(k, e)]
+                dl[(g, t)], sl[(g, t)], nl[(g, t)] = w, np.sort(chosen), float(w[chosen].sum())
+        dist.append(dl), sets.append(sl), den.append(nl)
+    tids = [t for _, _, t in tiles]
+
+    def score(i, a, j, b, t):
+        d = den[b][(j, t)]
+        return None if d == 0.0 else float(np.float32(float(dist[b][(j, t)][sets[a][(i, t)]].sum()) / d))
+
+    S = np.zeros((L, L), np.float32)
+    undefined = 0
+    for b in range(L):
+        for a in range(b + 1):
+            hs = np.zeros((Hkv, Hkv))
+            for i in range(Hkv):
+                for j in range(Hkv):
+                    v = [x for x in (score(i, a, j, b, t) for t in tids) if x is not None]
+                    hs[i, j] = np.mean(v) if v else 0.0
+            hm = hs.argmax(axis=0)
+            per_tile = []
+            for t in tids:
+                v = [score(int(hm[j]), a, j, b, t) for j in range(Hkv)]
+                kept = [x for x in v if x is not None]
+                undefined += len(v) - len(kept)
+                if kept:
+                    per_tile.append(float(np.mean(kept)))
+            if per_tile:
+                S[a, b] = np.float32(np.mean(per_tile) if how == "mean" else np.min(per_tile))
+    return S, undefined
+
+
+def diagnostic_matrix(Q, K, V, k: int = 64, how: str = "mean"):
+    """metrics.py:205-223: per-token distributions averaged over ALL query
+    heads; S[a][b] aggregates mass(b on a's sets) / mass(b on b's sets)."""
+    L = Q.shape[0]
+    S = np.zeros((L, L), np.float32)
+    undefined = 0
+    kept_sets = []
+    for b in range(L):
+        P, _ = dense_layer(Q[b], K[b], V[b])
+        Db = P.mean(axis=0, dtype=np.float64).astype(np.float32)
+        idx_b, valid = token_sets(Db, k)
+        den = masked_mass(Db, idx_b, valid)
+        kept_sets.append(idx_b)
+        ok = den != 0.0
+        for a in range(b + 1):
+            num = masked_mass(Db, kept_sets[a], valid)
+            sc = np.zeros_like(num)
+            sc[ok] = num[ok] / den[ok]
+            sc = sc.astype(np.float32)
+            undefined += int((~ok).sum())
+            S[a, b] = np.float32(_agg(sc[ok], how)) if how == "mean" else _agg(sc[ok], how)
+    return S, undefined

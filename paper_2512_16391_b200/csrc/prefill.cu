@@ -46,8 +46,9 @@ constexpr int kHalf = 16384;           // one 64-column 128B-swizzled half tile
 constexpr int kOffQ = 0;                                   // 2 tiles
 constexpr int kOffK = kOffQ + 2 * kTileBytes;              // stages
 constexpr int kOffV = kOffK + kStages * kTileBytes;
-constexpr int kOffPos = kOffV + kStages * kTileBytes;      // int[stages][128]
-constexpr int kOffBar = kOffPos + kStages * 128 * 4;
+constexpr int kPosBufs = 4;                               // sparse: positions of blocks j..j+3
+constexpr int kOffPos = kOffV + kStages * kTileBytes;      // int[kPosBufs][128]
+constexpr int kOffBar = kOffPos + kPosBufs * 128 * 4;
 constexpr int kNumBars = 16;
 constexpr int kOffTmem = kOffBar + kNumBars * 8;
 constexpr int kSmemBytes = kOffTmem + 16 + 1024;           // + alignment slack
@@ -61,7 +62,9 @@ struct PrefillTmaps {
 };
 
 // bars: 0 q_full | 1-2 k_full[s] | 3-4 v_full[s] | 5-6 kv_empty[s] |
-//       7-8 s_full[t] | 9-10 p_full[t] | 11-12 o_done[t]
+//       7-8 s_full[t] | 9-10 p_full[t] | 11-12 o_done[t] |
+//       13-14 k_empty[s] (sparse: the K half of a stage frees once S of
+//       both tiles retired, long before PV frees the V half)
 template <int MODE>
 __global__ void __launch_bounds__(pf::kThreads, 1)
     prefill_attn_kernel(const __grid_constant__ PrefillTmaps tm, const PrefillArgs a) {
@@ -100,6 +103,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
       mbar_init(&bars[1 + s], MODE == PMODE_SPARSE ? 96 : 1);
       mbar_init(&bars[3 + s], MODE == PMODE_SPARSE ? 96 : 1);
       mbar_init(&bars[5 + s], 1);
+      if (MODE == PMODE_SPARSE) mbar_init(&bars[13 + s], 1);
     }
     if (MODE == PMODE_LSE) {
       // no O: each tile double-buffers S; s_full(t,b) = 7+t+2b, p_full(t,b) = 11+t+2b
@@ -177,6 +181,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
         mbar_wait(&bars[1], 0);
         tc_fence_after();
         for (int t = 0; t < nslots; ++t) issue_s(t, 0);
+        if (MODE == PMODE_SPARSE) mma_commit(&bars[13]);
         for (int j = 0; j < nb; ++j) {
           const int st = j % kStages;
           const uint32_t ph = (j / kStages) & 1;
@@ -206,6 +211,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
           }
           mma_commit(&bars[5 + st]);   // K/V stage free once everything so far retires
           if (more && nslots == 2) issue_s(1, st1);
+          if (MODE == PMODE_SPARSE && more) mma_commit(&bars[13 + st1]);   // K_{j+1} consumed by both S
         }
         }  // MODE != PMODE_LSE
       }
@@ -249,34 +255,56 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
       // tensor core reads coherent shared memory.
       const __nv_bfloat16* kg = a.k + (int64_t)g * a.kv_sh;
       const __nv_bfloat16* vg = a.v + (int64_t)g * a.kv_sh;
-      for (int j = 0; j < nb; ++j) {
-        const int st = j % kStages;
-        if (j >= kStages) mbar_wait(&bars[5 + st], ((j / kStages) - 1) & 1);
-        int* pos = posbuf + st * 128;
-        for (int r = pt; r < 128; r += 96) {
-          const int e = j * kBlockN + r;
-          pos[r] = e < count ? __ldg(sel + e) : 0x7fffffff;
-        }
-        named_bar_sync(1, 96);
-        const uint32_t kdst = smem_u32(smem + kOffK + st * kTileBytes);
-        const uint32_t vdst = smem_u32(smem + kOffV + st * kTileBytes);
+      // The selection entries of block j+1 are loaded into registers while
+      // block j's rows are in flight, so the dependent index load never sits
+      // on the stage-free -> gather -> publish critical path.
+      const int r1 = pt + 96;                       // second row of threads 0..31
+      auto load_sel = [&](int j, int& p0, int& p1) {
+        const int e0 = j * kBlockN + pt, e1 = j * kBlockN + r1;
+        p0 = e0 < count ? __ldg(sel + e0) : 0x7fffffff;
+        p1 = (r1 < kBlockN && e1 < count) ? __ldg(sel + e1) : 0x7fffffff;
+      };
+      int p0 = 0x7fffffff, p1 = 0x7fffffff;
+      if (nb > 0) load_sel(0, p0, p1);
+      // Cp.async groups retire in order K_0, V_0, K_1, V_1, ...: K_j is
+      // gathered as soon as S_{j-2} released its half-stage and is published
+      // first; V_{j-1} is published while K_j is in flight.
+      auto gather = [&](uint32_t dst, const __nv_bfloat16* src, const int* pos) {
+#pragma unroll 2
         for (int c = pt; c < 128 * 16; c += 96) {
           const int r = c >> 4, ch = c & 15;
           const int p = pos[r];
           const bool valid = p != 0x7fffffff;
           const uint32_t off = (ch >> 3) * kHalf + r * 128 + (((ch & 7) ^ (r & 7)) << 4);
-          const int64_t src = (int64_t)(valid ? p : 0) * 128 + ch * 8;
-          cp_async16_zfill(kdst + off, kg + src, valid);
-          cp_async16_zfill(vdst + off, vg + src, valid);
+          cp_async16_zfill(dst + off, src + (int64_t)(valid ? p : 0) * 128 + ch * 8, valid);
         }
-        // Publish block j before touching block j+1: the MMA warp releases
-        // stage j-1 only after K_j has landed (it issues S_j first), so
-        // holding block j back would deadlock the 2-stage ring.
         cp_async_commit();
-        cp_async_wait<0>();
+      };
+      for (int j = 0; j < nb; ++j) {
+        const int st = j % kStages;
+        const uint32_t ph_free = ((j / kStages) - 1) & 1;
+        if (j >= kStages) mbar_wait(&bars[13 + st], ph_free);    // K half of the stage free
+        int* pos = posbuf + (j % kPosBufs) * 128;
+        pos[pt] = p0;
+        if (r1 < kBlockN) pos[r1] = p1;
+        if (j + 1 < nb) load_sel(j + 1, p0, p1);
+        named_bar_sync(1, 96);
+        gather(smem_u32(smem + kOffK + st * kTileBytes), kg, pos);
+        if (j > 0) {                                              // V_{j-1} landed
+          cp_async_wait<1>();
+          fence_proxy_async_smem();
+          mbar_arrive(&bars[3 + (j - 1) % kStages]);
+        }
+        if (j >= kStages) mbar_wait(&bars[5 + st], ph_free);     // V half free (PV_{j-2} retired)
+        gather(smem_u32(smem + kOffV + st * kTileBytes), vg, pos);
+        cp_async_wait<1>();                                       // K_j landed
         fence_proxy_async_smem();
         mbar_arrive(&bars[1 + st]);
-        mbar_arrive(&bars[3 + st]);
+      }
+      if (nb > 0) {
+        cp_async_wait<0>();
+        fence_proxy_async_smem();
+        mbar_arrive(&bars[3 + (nb - 1) % kStages]);
       }
     }
   } else {
@@ -307,7 +335,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
         // unselected.  Sorted selections only reach the tile's own rows in
         // their last block(s), so earlier blocks skip the per-key test.
         if (MODE == PMODE_SPARSE) {
-          const int* pos = posbuf + (j % kStages) * 128;
+          const int* pos = posbuf + (j % kPosBufs) * 128;
           if (pos[127] > r0) {
 #pragma unroll
             for (int c = 0; c < 128; c += 4) {

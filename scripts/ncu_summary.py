@@ -33,7 +33,7 @@ def main():
     for k in KEYS:
         if k in d:
             print(f"  {k:92s} {d[k]:>20s} {u.get(k, '')}")
-    t_us = float(d["gpu__time_duration.sum"]) * (1e-3 if u["gpu__time_duration.sum"] == "ns" else 1.0)
+    t_us = float(d["gpu__time_duration.sum"]) * {"ns": 1e-3, "us": 1.0, "ms": 1e3}.get(u["gpu__time_duration.sum"], 1.0)
     rd = float(d["dram__bytes_read.sum"]) * (1e6 if u["dram__bytes_read.sum"] == "Mbyte" else
                                               1e9 if u["dram__bytes_read.sum"] == "Gbyte" else 1e3)
     wr = float(d["dram__bytes_write.sum"]) * (1e6 if u["dram__bytes_write.sum"] == "Mbyte" else

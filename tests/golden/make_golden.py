@@ -281,6 +281,41 @@ def main():
                    "format_errors": errs, "cases": cli_cases}, f, indent=1, sort_keys=True)
         f.write("\n")
 
+    # 9. offline calibration: head similarity and head
+    #    maps (heads.py:67-143, pipeline.py:31-73) and the layer similarity
+    #    matrix in both modes (metrics.py:205-335), on the kascade_prefill
+    #    trace (section 5) and on config 1 (section 7).
+    import time
+    from kascade import metrics as ref_metrics
+    from kascade import heads as ref_heads
+    z5 = np.load(os.path.join(HERE, "kascade_prefill.npz"))
+    tA = trace_of(*(orc.from_bf16_bits(z5[n]) for n in ("Q", "K", "V")))
+    cal = {}
+    for agg in ("mean", "min"):
+        for a, b in ((0, 1), (0, 3), (2, 3), (1, 1)):
+            cal[f"hs_{agg}_{a}_{b}"] = ref_heads.head_similarity(tA, a, b, k=16, token_agg=agg)
+        for mode, extra in (("planning", dict(tile_size=64)), ("diagnostic", {})):
+            S = ref_metrics.similarity_matrix(tA, k=16, token_agg=agg, mode=mode, **extra)
+            cal[f"S_{mode}_{agg}"] = S.S
+            cal[f"und_{mode}_{agg}"] = np.array(S.undefined_scores)
+    S = ref_metrics.similarity_matrix(tA, k=16, token_agg="min", mode="planning", tile_size=64, phase="decode")
+    cal["S_planning_decode_min"], cal["und_planning_decode_min"] = S.S, np.array(S.undefined_scores)
+    maps = ref.compute_head_maps(tA, [0, 2], k=16)
+    cal["maps_A"] = np.array([maps[l].map if l in maps else [-1, -1] for l in range(4)], np.int32)
+    # config 1: the BASELINE planning pass (k=64, tile 128, min over tiles)
+    t1 = trace_of(*(orc.bf16_round(x) for x in orc.synth_qkv(c1["L"], c1["Hq"], c1["Hkv"], c1["d"], c1["N"],
+                                                             seed=c1["seed"], rho=c1["rho"])), "config1")
+    t0 = time.perf_counter()
+    S1 = ref_metrics.similarity_matrix(t1, k=64, token_agg="min", mode="planning", tile_size=128)
+    meta["ref_seconds_config1_planning_matrix"] = round(time.perf_counter() - t0, 2)
+    t0 = time.perf_counter()
+    maps1 = ref.compute_head_maps(t1, [0, 2], k=64)
+    meta["ref_seconds_config1_head_maps"] = round(time.perf_counter() - t0, 2)
+    cal["S1_planning_min"], cal["und1"] = S1.S, np.array(S1.undefined_scores)
+    cal["maps1"] = np.array([maps1[l].map if l in maps1 else [-1, -1] for l in range(4)], np.int32)
+    cal["hs1_0_1"] = ref_heads.head_similarity(t1, 0, 1, k=64)
+    np.savez_compressed(os.path.join(HERE, "calibration.npz"), **cal)
+
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(meta, f, indent=1, sort_keys=True)
         f.write("\n")
