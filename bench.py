@@ -78,6 +78,16 @@ def make_plan(L, Hkv, anchors, fraction, k_min):
                       k_policy=KBudgetPolicy(fraction, k_min))
 
 
+def load_traffic(key):
+    """Per-launch DRAM bytes of a roofline kernel from the committed ncu capture
+    (profiles/traffic.json), or None when the bench shape has none."""
+    p = os.path.join(REPO, "profiles", "traffic.json")
+    try:
+        return json.load(open(p))[key]["bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def load_peaks():
     p = os.path.join(REPO, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -338,7 +348,8 @@ def bench_prefill(args, dev, world, dist):
         "paper_h100_ms_per_layer": {"fa3": 215.76, "tilelang_dense": 262.21, "kascade": 98.55},
         "roofline": {"kernel": "kscd sparse_prefill (reuse layer)", "bound": "tensor",
                      "achieved": round(flops_reuse / (t_reuse * 1e-3) / 1e12, 1), "peak": tpk, "unit": "TFLOP/s",
-                     "frac": round(flops_reuse / (t_reuse * 1e-3) / 1e12 / tpk, 4), "traffic": None,
+                     "frac": round(flops_reuse / (t_reuse * 1e-3) / 1e12 / tpk, 4),
+                     "traffic": load_traffic(f"sparse_prefill_{N // 1024}k"),
                      "peak_kind": kind,
                      "dense_prefill_frac": round(flops_dense / (t_dense * 1e-3) / 1e12 / tpk, 4)},
         "gpu_launches_per_step": 1 * 3 + n_anchor * 4 + n_reuse,
@@ -543,7 +554,8 @@ def main():
         "paper_h100_us_per_token": 1415,
         "roofline": {"kernel": "kscd sparse_decode (reuse layer)", "bound": "hbm",
                      "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                     "frac": round(achieved / hbm, 4), "traffic": None, "peak_kind": peaks_kind,
+                     "frac": round(achieved / hbm, 4), "traffic": load_traffic(f"sparse_decode_{n // 1024}k_b{B}"),
+                     "peak_kind": peaks_kind,
                      "bytes_per_launch": reuse_bytes, "launch_ms": round(reuse_ms, 4),
                      "dense_decode_frac": round(dense_bytes / (dense_ms_launch * 1e-3) / 1e9 / hbm, 4)},
         "clocks": clk,
