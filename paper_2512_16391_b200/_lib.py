@@ -12,7 +12,7 @@ import threading
 from .exceptions import InvalidArgumentError, KascadeError, UnsupportedOperationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkascade_b200.so")
+LIB_PATH = os.environ.get("KSCD_LIB_PATH") or os.path.join(_HERE, "libkascade_b200.so")  # dev override: variant builds
 
 KSCD_OK, KSCD_INVALID_ARGUMENT, KSCD_UNSUPPORTED, KSCD_CUDA_ERROR = 0, 1, 2, 3
 

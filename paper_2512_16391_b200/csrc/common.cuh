@@ -101,10 +101,60 @@ KSCD_DEV float2 exp2_poly2(float2 x) {
 // Measured on B200 (128K prefill): 3/8 polynomial made the dense / LSE /
 // pass-B kernels 10-16% SLOWER (extra issue slots + register spills), so the
 // split is off; the kernels are issue/latency bound, not MUFU bound.
+#ifdef KSCD_POLY
+constexpr int kPolyPairsPer8 = KSCD_POLY;
+#else
 constexpr int kPolyPairsPer8 = 0;
+#endif
+// Share of the exponentials of the two anchor passes (row sums of pass A,
+// column sums of pass B) that go to the FMA-pipe polynomial.  Measured on
+// B200 (same box, A/B alternated): at 32K, 1/8-2/8 cut pass A by 6-13%
+// (pass B within noise); at 128K every split is within +-1% of MUFU-only --
+// the long launches run under sw_power_cap, so offloaded exponentials buy
+// no clock cycles.  1/8 is kept as the smallest deviation from MUFU.EX2.
+#ifndef KSCD_PB_POLY
+#define KSCD_PB_POLY 1      // pass B column sums: polynomial pairs per 8
+#endif
+#ifndef KSCD_LSE_POLY
+#define KSCD_LSE_POLY 1     // pass A row sums: polynomial pairs per 8
+#endif
 KSCD_DEV float2 exp2_pair(float2 x, int pair) {
   if ((pair & 7) < kPolyPairsPer8) return exp2_poly2(x);
   return make_float2(fast_exp2(x.x), fast_exp2(x.y));
+}
+
+// exp2 of a pair on the FMA pipe for inputs that never need an exact zero
+// (anchor pass A row sums, pass B column sums): Cody-Waite split + degree-5
+// minimax of 2^f on [-0.5, 0.5] (max rel. error 2.3e-7 in fp32, the same
+// class as MUFU.EX2's 2^-22).  Inputs below -126 (incl. -inf) return
+// 2^-126 instead of 0 -- harmless inside a sum of terms >= 2^-126 * count.
+KSCD_DEV float2 exp2_poly5(float2 x) {
+  const float2 xc = make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f));
+  const float2 t = __fadd2_rn(xc, make_float2(12582912.f, 12582912.f));      // round to integer
+  const float2 n = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __ffma2_rn(n, make_float2(-1.f, -1.f), xc);               // f = x - n
+  float2 p = make_float2(0.00132764654699713f, 0.00132764654699713f);
+  p = __ffma2_rn(p, f, make_float2(0.009675540961325169f, 0.009675540961325169f));
+  p = __ffma2_rn(p, f, make_float2(0.05550713464617729f, 0.05550713464617729f));
+  p = __ffma2_rn(p, f, make_float2(0.24022120237350464f, 0.24022120237350464f));
+  p = __ffma2_rn(p, f, make_float2(0.6931469440460205f, 0.6931469440460205f));
+  p = __ffma2_rn(p, f, make_float2(1.0000001192092896f, 1.0000001192092896f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
+// exp2 of a pair for sums: FMA-pipe polynomial for pair indices with
+// (pair & 7) < POLY, MUFU for the rest (POLY is a compile-time split).
+template <int POLY>
+KSCD_DEV float2 exp2_pair_sum(float2 x, int pair) {
+  if ((pair & 7) < POLY) return exp2_poly5(x);
+  return make_float2(fast_exp2(x.x), fast_exp2(x.y));
+}
+
+KSCD_DEV float4 lds_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
 }
 
 template <typename T>

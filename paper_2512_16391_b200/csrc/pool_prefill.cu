@@ -56,7 +56,6 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmem);
   float* lse2 = reinterpret_cast<float*>(smem + kOffLse);
-  float* red = reinterpret_cast<float*>(smem + kOffRed);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int T = (a.N + 127) / 128;
@@ -167,16 +166,16 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&bars[9 + qq]);                // buffer free: the MMA may refill it
-        const float4* l4 = reinterpret_cast<const float4*>(lse2 + 128 * qq);
+        const uint32_t l4 = smem_u32(lse2 + 128 * qq);
 #pragma unroll
         for (int i = 0; i < 128; i += 4) {
-          const float4 lv = l4[i >> 2];            // broadcast read: same rows for every key
+          const float4 lv = lds_f4(l4 + i * 4);    // broadcast read: same rows for every key
           float2 e0 = __ffma2_rn(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sc2,
                                  make_float2(-lv.x, -lv.y));
           float2 e1 = __ffma2_rn(make_float2(__uint_as_float(r[i + 2]), __uint_as_float(r[i + 3])), sc2,
                                  make_float2(-lv.z, -lv.w));
-          e0 = exp2_pair(e0, i >> 1);
-          e1 = exp2_pair(e1, (i >> 1) + 1);
+          e0 = exp2_pair_sum<KSCD_PB_POLY>(e0, i >> 1);
+          e1 = exp2_pair_sum<KSCD_PB_POLY>(e1, (i >> 1) + 1);
           if (diag) {
             if (key > r0 + i) e0.x = 0.f;
             if (key > r0 + i + 1) e0.y = 0.f;

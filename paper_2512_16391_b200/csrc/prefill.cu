@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
 #pragma unroll
           for (int c = 0; c < 128; c += 2) {
             const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sc2, nm2);
-            sum2 = __fadd2_rn(sum2, exp2_pair(x, c >> 1));
+            sum2 = __fadd2_rn(sum2, exp2_pair_sum<KSCD_LSE_POLY>(x, c >> 1));
           }
         } else {
 #pragma unroll

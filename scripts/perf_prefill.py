@@ -44,6 +44,10 @@ def main():
     t = timeit(lambda: ops.anchor_lse_prefill(q, k, lse=lse))
     res["lse_pass_ms"] = t
     res["lse_pass_tflops"] = flops_dense / 2 / t / 1e9
+    if len(sys.argv) > 2 and sys.argv[2] == "dense-only":
+        res["lib"] = os.environ.get("KSCD_LIB_PATH", "default")
+        print(json.dumps({k_: (round(v_, 3) if isinstance(v_, float) else v_) for k_, v_ in res.items()}))
+        return
     T = (N + 127) // 128
     pooled = torch.empty(2, Hkv, T, (N + 3) // 4 * 4, dtype=torch.float32, device=dev)
     idx = torch.empty(Hkv, T, ops.prefill_k_cap(pol, N), dtype=torch.int32, device=dev)
