@@ -48,7 +48,8 @@ def parse():
     ap.add_argument("--k-min", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--extra", action="store_true", help="also time configs[1] (32K, k=2.5%%)")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the BASELINE.json configs[1..4] section")
     ap.add_argument("--best-of", action="store_true", help="report the better of two timed regions")
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--prefill-ctx", type=int, default=131072)
@@ -57,24 +58,30 @@ def parse():
     return ap.parse_args()
 
 
-def head_maps_for(L, Hkv, anchors, seed=1234):
-    """Deterministic non-identity head maps (a fixed permutation per reuse
-    layer), standing in for offline calibration so the bench exercises the
-    cross-head gather."""
-    rng = np.random.default_rng(seed)
-    maps = {}
-    for l in range(L):
-        if l in anchors:
-            continue
-        maps[l] = rng.permutation(Hkv).tolist()
-    return maps
+PLANS = os.path.join(REPO, "plans")
 
 
-def make_plan(L, Hkv, anchors, fraction, k_min):
+def make_plan(L, Hkv, anchors, fraction, k_min, name="llama8b"):
+    """The committed plan built by the reference's own offline planner
+    (plans/make_plans.py: published anchors + compute_head_maps on a
+    head-permuted synthetic trace, so the remaps are non-identity), with the
+    bench's Top-k budget."""
+    from paper_2512_16391_b200.host_types import KBudgetPolicy, read_plan
+    plan = read_plan(os.path.join(PLANS, f"{name}.json"))
+    assert plan.anchors == list(anchors), (name, plan.anchors, anchors)
+    assert all(len(m.map) == Hkv for m in plan.head_maps.values())
+    plan.k_policy = KBudgetPolicy(fraction, k_min)
+    plan.validate(L, Hkv)
+    return plan
+
+
+def shard_plan(plan, fraction, k_min):
+    """One kv head of an 8-way kv-head-sharded plan: same anchors, the head
+    maps reduced to the shard's own head (the cross-shard routing is the
+    index-list all-gather, timed separately)."""
     from paper_2512_16391_b200.host_types import AnchorPlan, AnchorPlanCore, HeadMap, KBudgetPolicy
-    maps = head_maps_for(L, Hkv, anchors)
-    hm = {l: HeadMap(l, max(a for a in anchors if a <= l), m) for l, m in maps.items()}
-    return AnchorPlan(AnchorPlanCore(anchors, len(anchors), 0.0), head_maps=hm,
+    maps = {l: HeadMap(l, m.anchor_layer, [0]) for l, m in plan.head_maps.items()}
+    return AnchorPlan(AnchorPlanCore(plan.anchors, len(plan.anchors), 0.0), head_maps=maps,
                       k_policy=KBudgetPolicy(fraction, k_min))
 
 
@@ -357,6 +364,146 @@ def bench_prefill(args, dev, world, dist):
     }
 
 
+# ------------------------------------------------------ BASELINE configs
+def _timed(fn, steps, warm, world, dist, dev):
+    """CUDA-event time of `steps` calls after `warm` untimed ones, max over
+    ranks (ms per call)."""
+    import torch
+    for _ in range(warm):
+        fn()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
+def _decode_config(dev, world, dist, plan, L, B, Hq, Hkv, n, steps, warm, seed):
+    """One decode step (all L layers, CUDA graph) of the Kascade plan and of
+    the dense mode on the same per-layer KV caches (distinct per layer when
+    they fit in HBM, else a pool of distinct buffers cycled over the layers;
+    each layer's KV is far larger than L2 either way)."""
+    import torch
+    from paper_2512_16391_b200 import engine
+    per_layer = 2 * B * Hkv * n * 128 * 2
+    free, _ = torch.cuda.mem_get_info(dev)
+    n_distinct = int(max(2, min(L, (free - 16 * 2**30) // per_layer)))
+    gen = torch.Generator(device=dev)
+    Kc, Vc = [], []
+    for i in range(n_distinct):
+        gen.manual_seed(seed + i)
+        Kc.append(torch.randn(B, Hkv, n, 128, device=dev, dtype=torch.bfloat16, generator=gen))
+        Vc.append(torch.randn(B, Hkv, n, 128, device=dev, dtype=torch.bfloat16, generator=gen))
+    Ks = [Kc[l % n_distinct] for l in range(L)]
+    Vs = [Vc[l % n_distinct] for l in range(L)]
+    q = (torch.randn(L, B, Hq, 128, device=dev, generator=gen) * 2.0).to(torch.bfloat16)
+    dec = engine.KascadeDecoder(plan, L, B, Hq, Hkv, n, device=dev)
+    ga = dec.capture(q, Ks, Vs, n)
+    gd = dec.capture(q, Ks, Vs, n, dense=True)
+    m_a = _timed(ga.replay, steps, warm, world, dist, dev)
+    m_d = _timed(gd.replay, steps, warm, world, dist, dev)
+    del ga, gd, dec, Kc, Vc, Ks, Vs, q
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return m_a, m_d, n_distinct
+
+
+def _prefill_config(dev, world, dist, plan, L, Hq, Hkv, N, steps, warm, seed):
+    """The full L-layer Kascade prefill forward and the dense forward of the
+    same engine (batch 1)."""
+    import torch
+    from paper_2512_16391_b200 import engine
+    per_layer = (Hq + 2 * Hkv) * N * 128 * 2
+    eng = engine.KascadePrefill(plan, L, Hq, Hkv, N, device=dev)
+    free, _ = torch.cuda.mem_get_info(dev)
+    n_distinct = int(max(2, min(L, (free - 16 * 2**30) // per_layer)))
+    gen = torch.Generator(device=dev)
+    qs, ks, vs = [], [], []
+    for i in range(n_distinct):
+        gen.manual_seed(seed + i)
+        qs.append(torch.randn(Hq, N, 128, device=dev, generator=gen, dtype=torch.bfloat16))
+        ks.append(torch.randn(Hkv, N, 128, device=dev, generator=gen, dtype=torch.bfloat16))
+        vs.append(torch.randn(Hkv, N, 128, device=dev, generator=gen, dtype=torch.bfloat16))
+    Q = [qs[l % n_distinct] for l in range(L)]
+    K = [ks[l % n_distinct] for l in range(L)]
+    V = [vs[l % n_distinct] for l in range(L)]
+    m_a = _timed(lambda: eng.forward(Q, K, V), steps, warm, world, dist, dev)
+    m_d = _timed(lambda: eng.dense_forward(Q, K, V), steps, warm, world, dist, dev)
+    del eng, qs, ks, vs, Q, K, V
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return m_a, m_d, n_distinct
+
+
+def bench_configs(args, dev, world, dist):
+    """BASELINE.json configs[1..4] at their own shapes and plans (configs[0]
+    is the reference's CPU case; it is a parity test, tests/golden).  Each
+    rank runs the per-GPU share of the config (weak scaling): configs[3]'s
+    batch of 32 is split over the ranks, configs[4] is one kv head of the
+    8-way kv-head-sharded 70B model (1 KV + 8 Q heads, 80 layers) -- the
+    work each of the 8 GPUs does between index-list all-gathers."""
+    rank_seed = 97 * int(os.environ.get("RANK", "0"))
+    out = []
+    steps, warm = max(3, args.steps // 2), max(3, args.warmup)
+
+    # configs[1]: Llama-3.1-8B decode, 32K, batch 8, Top-k 2.5 %
+    L, Hq, Hkv = CFG["layers"], CFG["Hq"], CFG["Hkv"]
+    plan = make_plan(L, Hkv, LLAMA_ANCHORS, 0.025, args.k_min)
+    m_a, m_d, nd = _decode_config(dev, world, dist, plan, L, 8, Hq, Hkv, 32768, steps, warm, 11000 + rank_seed)
+    out.append({"config": 1, "workload": "llama8b-decode-32k-b8-k2.5%", "plan": "plans/llama8b.json",
+                "kascade_us_per_token": round(m_a * 1e3 / 8, 2), "dense_us_per_token": round(m_d * 1e3 / 8, 2),
+                "speedup_vs_dense": round(m_d / m_a, 3), "batch_per_gpu": 8, "kv_layers_distinct": nd})
+
+    # configs[2]: Llama-3.1-8B prefill, 64K, tile-level Top-k 10 % + head remap
+    plan = make_plan(L, Hkv, LLAMA_ANCHORS, args.fraction, args.k_min)
+    m_a, m_d, nd = _prefill_config(dev, world, dist, plan, L, Hq, Hkv, 65536, 1, 1, 12000 + rank_seed)
+    out.append({"config": 2, "workload": "llama8b-prefill-64k-b1-k0.1", "plan": "plans/llama8b.json",
+                "kascade_ms_per_layer": round(m_a / L, 3), "dense_ms_per_layer": round(m_d / L, 3),
+                "kascade_ms": round(m_a, 2), "dense_ms": round(m_d, 2), "speedup_vs_dense": round(m_d / m_a, 3),
+                "layers_distinct": nd})
+
+    # configs[3]: Qwen3-8B-shaped decode, 128K, batch 32 split over the ranks
+    Lq = 36
+    B3 = max(1, 32 // world)
+    plan = make_plan(Lq, Hkv, [0, 2, 7, 14, 23], args.fraction, args.k_min, name="qwen3_8b")
+    m_a, m_d, nd = _decode_config(dev, world, dist, plan, Lq, B3, Hq, Hkv, 131072, steps, warm, 13000 + rank_seed)
+    out.append({"config": 3, "workload": f"qwen3-8b-decode-128k-b32-k0.1 (batch {B3} per GPU x {world})",
+                "plan": "plans/qwen3_8b.json", "kascade_us_per_token": round(m_a * 1e3 / (B3 * world), 2),
+                "dense_us_per_token": round(m_d * 1e3 / (B3 * world), 2), "speedup_vs_dense": round(m_d / m_a, 3),
+                "batch_per_gpu": B3, "kv_layers_distinct": nd,
+                "note": "KV of 32 sequences x 36 layers is 618 GB: layers cycle over the distinct buffers that "
+                        "fit (each layer's KV >> L2)"})
+
+    # configs[4]: Llama-3.1-70B, one kv head of 8-way kv-head sharding, 128K
+    from paper_2512_16391_b200.host_types import read_plan
+    p70 = read_plan(os.path.join(PLANS, "llama70b.json"))
+    shard = shard_plan(p70, args.fraction, args.k_min)
+    L7, Hq7 = 80, 8
+    m_pa, m_pd, nd_p = _prefill_config(dev, world, dist, shard, L7, Hq7, 1, 131072, 1, 1, 14000 + rank_seed)
+    m_da, m_dd, nd_d = _decode_config(dev, world, dist, shard, L7, 8, Hq7, 1, 131072, steps, warm, 15000 + rank_seed)
+    out.append({"config": 4, "workload": "llama70b-128k-kv-head-shard (1 KV + 8 Q heads per GPU, 80 layers, k0.1)",
+                "plan": "plans/llama70b.json (reference build_plan, budget 12)", "anchors": p70.anchors,
+                "prefill_kascade_ms_per_layer": round(m_pa / L7, 3), "prefill_dense_ms_per_layer": round(m_pd / L7, 3),
+                "prefill_speedup_vs_dense": round(m_pd / m_pa, 3),
+                "decode_kascade_us_per_token": round(m_da * 1e3 / 8, 2),
+                "decode_dense_us_per_token": round(m_dd * 1e3 / 8, 2),
+                "decode_speedup_vs_dense": round(m_dd / m_da, 3), "decode_batch": 8,
+                "layers_distinct": {"prefill": nd_p, "decode": nd_d},
+                "note": "per-GPU work of the 8-way job; the index-list all-gather after each of the 12 anchor "
+                        "layers (<= 54 MB per GPU at 128K prefill) is not in this single-GPU timing"})
+    return out
+
+
 # ------------------------------------------------------------------ GPU arm
 def main():
     args = parse()
@@ -496,31 +643,17 @@ def main():
                        "and new K/V rows, one append launch into the 32 layers' caches, the layer loop, D2H "
                        "of all 32 layers' outputs; host-synchronised every step"}
 
-    # ---- secondary config: configs[1] 32K, k = 2.5 % -----------------------
-    extra = None
-    if args.extra and n >= 32768:
-        n2 = 32768
-        plan2 = make_plan(L, Hkv, LLAMA_ANCHORS, 0.025, args.k_min)
-        K2 = [x[:, :, :n2] for x in Ks]
-        V2 = [x[:, :, :n2] for x in Vs]
-        dec2 = engine.KascadeDecoder(plan2, L, B, Hq, Hkv, n2, device=dev)
-        ga = dec2.capture(q, K2, V2, n2)
-        gd = dec2.capture(q, K2, V2, n2, dense=True)
-        m_a, m_d = timed(ga, args.steps), timed(gd, args.steps)
-        extra = {"workload": "configs[1] llama8b-decode-32k-b8-k2.5%", "kascade_us_per_token":
-                 round(m_a * 1e3 / (B * world), 2), "dense_us_per_token": round(m_d * 1e3 / (B * world), 2),
-                 "speedup_vs_dense": round(m_d / m_a, 3)}
-        del dec2, ga, gd
-
     # ---- prefill at 128K (secondary metric of the same line) -------------
     del g_kas, g_den, dec, Kc, Vc, Ks, Vs, q
-    if extra is not None:
-        del K2, V2
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     prefill = None
     if not args.no_prefill:
         prefill = bench_prefill(args, dev, world, dist)
+        torch.cuda.empty_cache()
+    configs = None
+    if not args.no_configs:
+        configs = bench_configs(args, dev, world, dist)
 
     # ---- CPU baseline (rank 0 only at N=1) -------------------------------
     cpu = None
@@ -563,10 +696,10 @@ def main():
         "cpu_baseline": cpu,
         "e2e": e2e,
     }
-    if extra:
-        line["extra"] = extra
     if prefill:
         line["prefill"] = prefill
+    if configs:
+        line["configs"] = configs
     del out_kas
     if rank == 0:
         print(json.dumps(line), flush=True)
