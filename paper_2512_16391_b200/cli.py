@@ -1,8 +1,12 @@
-"""``python -m paper_2512_16391_b200 run``: the reference CLI's ``run``
-subcommand (cli.py:80-89,216-233) on the B200 engine.
+"""``python -m paper_2512_16391_b200 run|cost``: the reference CLI's ``run``
+subcommand (cli.py:80-89,216-233) on the B200 engine, and its ``cost``
+subcommand (cli.py:90-105,236-300) over the B200 presets (costmodel.py).
 
     python -m paper_2512_16391_b200 run --trace t.kscd --plan p.json \\
         [--phase prefill|decode] [--mode remapped|all-heads-pooled] [--out report.json] [--fail-above X]
+    python -m paper_2512_16391_b200 cost [--preset b200-decode-131072-k10 ...] [--list-presets]
+        [--ratios a0,a,r | --predict] [--phase] [--fraction] [--seq-len] [--layers] [--anchors]
+        [--baseline-time] [--csv] [--out results.json]
 
 Exit codes follow the reference (cli.py:20-23): 0 ok, 1 usage, 2 data or
 format error, 3 threshold exceeded.
@@ -33,7 +37,83 @@ def build_parser():
     run.add_argument("--fail-above", type=float, default=None)
     run.add_argument("--engine", choices=["b200"], default="b200",
                      help="accepted for parity with `kascade run --engine b200`; there is no other engine")
+    cost = sub.add_parser("cost", help="weighted-average pipeline time and speedup (B200 presets)")
+    cost.add_argument("--preset", action="append", default=None,
+                      help="B200 preset name (repeatable); see --list-presets")
+    cost.add_argument("--list-presets", action="store_true")
+    cost.add_argument("--ratios", default=None, help="anchor0,anchor,reuse per-layer times")
+    cost.add_argument("--predict", action="store_true", help="use the ratio model fitted on the B200 rows")
+    cost.add_argument("--phase", choices=["decode", "prefill"], default="decode")
+    cost.add_argument("--fraction", type=float, default=0.1)
+    cost.add_argument("--seq-len", type=int, default=131072)
+    cost.add_argument("--layers", type=int, default=32)
+    cost.add_argument("--anchors", type=int, default=5)
+    cost.add_argument("--baseline-time", type=float, default=1.0)
+    cost.add_argument("--csv", action="store_true", help="emit CSV instead of text")
+    cost.add_argument("--out", default=None, help="write JSON results here")
     return p
+
+
+def _cost_rows(args):
+    """cli.py:236-273 over the B200 presets."""
+    from . import costmodel
+    from .exceptions import KascadeError
+    rows = []
+    if args.preset:
+        for name in args.preset:
+            rows.append((name, costmodel.report_from_preset(name), costmodel.get_preset(name)))
+    elif args.ratios:
+        parts = [float(x) for x in args.ratios.split(",")]
+        if len(parts) != 3:
+            raise KascadeError("--ratios needs anchor0,anchor,reuse")
+        params = costmodel.CostParams(phase=args.phase, num_layers=args.layers, num_anchors=args.anchors,
+                                      topk_fraction=args.fraction, seq_len=args.seq_len,
+                                      baseline_layer_time=args.baseline_time)
+        rows.append(("custom", costmodel.weighted_pipeline_time(
+            params, {"anchor0": parts[0], "anchor": parts[1], "reuse": parts[2]}), None))
+    elif args.predict:
+        rep = costmodel.predict_report(args.phase, args.fraction, args.seq_len, num_layers=args.layers,
+                                       num_anchors=args.anchors, baseline_layer_time=args.baseline_time)
+        rows.append((f"predict-b200-{args.phase}-{args.seq_len}-k{args.fraction}", rep, None))
+    else:
+        for name in costmodel.preset_names():
+            rows.append((name, costmodel.report_from_preset(name), costmodel.get_preset(name)))
+    return rows
+
+
+def cmd_cost(args) -> int:
+    """cli.py:276-320; the reference's "published" columns are the
+    measured B200 pipeline time / speedup of the preset row."""
+    import json
+    from . import costmodel
+    if args.list_presets:
+        for name in costmodel.preset_names():
+            print(name)
+        return EXIT_OK
+    rows = _cost_rows(args)
+    if args.csv:
+        print("name,kascade_time,baseline_time,speedup,measured_time,measured_speedup")
+        for name, rep, row in rows:
+            mt = f"{row.kascade_ms:.6g}" if row else ""
+            ms = f"{row.speedup:.6g}" if row else ""
+            print(f"{name},{rep.kascade_time:.6g},{rep.baseline_time:.6g},{rep.speedup:.6g},{mt},{ms}")
+    else:
+        for name, rep, row in rows:
+            line = f"{name}: time={rep.kascade_time:.4g} baseline={rep.baseline_time:.4g} speedup={rep.speedup:.3f}"
+            if row:
+                line += f" (measured B200 time={row.kascade_ms:.4g} speedup={row.speedup:.3f})"
+            if not rep.valid:
+                line += f" [!] {rep.note}"
+            print(line)
+    if args.out:
+        payload = [{"name": name, "kascade_time": rep.kascade_time, "baseline_time": rep.baseline_time,
+                    "speedup": rep.speedup, "per_kind": rep.per_kind, "valid": rep.valid,
+                    "measured_time": row.kascade_ms if row else None,
+                    "measured_speedup": row.speedup if row else None} for name, rep, row in rows]
+        with open(args.out, "w", encoding="utf-8") as f:
+            json.dump(payload, f, indent=2)
+            f.write("\n")
+    return EXIT_OK
 
 
 def cmd_run(args) -> int:
@@ -65,7 +145,7 @@ def main(argv=None) -> int:
     except SystemExit as e:
         return int(e.code or 0)
     try:
-        return cmd_run(args)
+        return cmd_cost(args) if args.command == "cost" else cmd_run(args)
     except (KascadeError, OSError) as e:
         sys.stderr.write(f"{build_parser().prog}: {e}\n")
         return EXIT_DATA
