@@ -245,6 +245,25 @@ int kscd_pool_tiles(const kscd_pool_tiles_params* p, void* stream);
 
 int kscd_append_kv(const kscd_append_kv_params* p, void* stream);
 
+/* Offline calibration gather-sum: mass[i][j][r] =
+ * fp64 sum over t < counts[i][r] of dist[j][r][indices[i][r][t]] -- the
+ * num / den terms of head_similarity_from_dists (heads.py:96-108) and of the
+ * planning matrix's pair_score (metrics.py:254-260). */
+typedef struct kscd_masked_mass_params {
+  int32_t num_sets;             /* I: index-set heads */
+  int32_t num_dists;            /* J: distribution heads */
+  int32_t rows;                 /* tokens or tiles */
+  const float* dist;            /* fp32; row r of head j at dist + j*dist_stride_head + r*dist_stride_row */
+  int64_t dist_stride_head, dist_stride_row;
+  int32_t dist_len;             /* valid columns of a row (indices must be < dist_len) */
+  const int32_t* indices;       /* [I][rows][k_cap], entries < dist_len */
+  const int32_t* counts;        /* [I][rows], <= k_cap */
+  int32_t k_cap;
+  double* mass;                 /* [I][J][rows] */
+} kscd_masked_mass_params;
+
+int kscd_masked_mass(const kscd_masked_mass_params* p, void* stream);
+
 /* k_budget (tiles.py:81-89): min(max(floor(fraction*n), k_min), n). */
 int32_t kscd_k_budget(double fraction, int32_t k_min, int32_t n);
 

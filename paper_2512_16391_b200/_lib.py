@@ -104,6 +104,15 @@ class AppendKvParams(ctypes.Structure):
 
 
 # entry point name -> params struct (None for non-struct signatures)
+class MaskedMassParams(ctypes.Structure):
+    _fields_ = [
+        ("num_sets", c_i32), ("num_dists", c_i32), ("rows", c_i32),
+        ("dist", c_vp), ("dist_stride_head", c_i64), ("dist_stride_row", c_i64), ("dist_len", c_i32),
+        ("indices", c_vp), ("counts", c_vp), ("k_cap", c_i32),
+        ("mass", c_vp),
+    ]
+
+
 ENTRY_POINTS = {
     "kscd_dense_decode": DecodeParams,
     "kscd_anchor_scores_decode": DecodeParams,
@@ -117,6 +126,7 @@ ENTRY_POINTS = {
     "kscd_dense_probs": ProbsParams,
     "kscd_pool_tiles": PoolTilesParams,
     "kscd_append_kv": AppendKvParams,
+    "kscd_masked_mass": MaskedMassParams,
 }
 
 _lock = threading.Lock()

@@ -459,3 +459,25 @@ extern "C" int kscd_append_kv(const kscd_append_kv_params* p, void* stream) {
   a.stride_h = p->kv_stride_head;
   return cuda_status(kscd::launch_append_kv(a, (cudaStream_t)stream), "kscd_append_kv");
 }
+
+int kscd_masked_mass(const kscd_masked_mass_params* p, void* stream) {
+  if (!p) return fail(KSCD_INVALID_ARGUMENT, "params is NULL");
+  if (p->num_sets < 0 || p->num_dists < 0 || p->rows < 0)
+    return fail(KSCD_INVALID_ARGUMENT, "negative size");
+  if (p->k_cap < 1) return fail(KSCD_INVALID_ARGUMENT, "k_cap must be >= 1, got %d", p->k_cap);
+  if (p->dist_len < 1) return fail(KSCD_INVALID_ARGUMENT, "dist_len must be >= 1");
+  if (p->dist_stride_row < p->dist_len) return fail(KSCD_INVALID_ARGUMENT, "dist rows overlap");
+  if (!p->dist || !p->indices || !p->counts || !p->mass) return fail(KSCD_INVALID_ARGUMENT, "NULL buffer");
+  kscd::MaskedMassArgs a{};
+  a.I = p->num_sets;
+  a.J = p->num_dists;
+  a.rows = p->rows;
+  a.k_cap = p->k_cap;
+  a.dist = p->dist;
+  a.dist_head_stride = p->dist_stride_head;
+  a.dist_row_stride = p->dist_stride_row;
+  a.idx = p->indices;
+  a.counts = p->counts;
+  a.mass = p->mass;
+  return cuda_status(kscd::launch_masked_mass(a, (cudaStream_t)stream), "kscd_masked_mass");
+}

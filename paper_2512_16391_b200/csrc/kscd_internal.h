@@ -111,6 +111,17 @@ struct PoolPrefillArgs {
 };
 cudaError_t launch_pool_prefill(const PoolPrefillArgs& a, cudaStream_t st);
 
+// ------------------------------------------------------- calibration (calib.cu)
+struct MaskedMassArgs {
+  int I, J, rows, k_cap;
+  const float* dist;                      // [J] heads, row r at + j*dist_head_stride + r*dist_row_stride
+  int64_t dist_head_stride, dist_row_stride;
+  const int* idx;                         // [I][rows][k_cap]
+  const int* counts;                      // [I][rows]
+  double* mass;                           // [I][J][rows]
+};
+cudaError_t launch_masked_mass(const MaskedMassArgs& a, cudaStream_t st);
+
 // ------------------------------------------------------------ compat (small N)
 struct ProbsArgs {
   int Hq, Hkv, G, N, causal;

@@ -149,3 +149,49 @@ def test_prefill_tile_driver_matches_reference(config1):
                 continue
             y, _, _ = orc.sparse_tile(Q[l], K[l], V[l], g, 4, N - tile, N, sel)
             np.testing.assert_allclose(y, z["pre_last_tile"][l, g * 4:(g + 1) * 4], rtol=0, atol=1e-6)
+
+
+# ---------------------------------------------------------------- calibration
+# Offline calibration: head similarity, head maps and
+# the layer similarity matrix in both modes, frozen from the reference
+# (heads.py:67-143, pipeline.py:31-73, metrics.py:205-335) by make_golden.py.
+
+@pytest.fixture(scope="module")
+def calib():
+    z5 = golden("kascade_prefill")
+    qkv = tuple(bf16(z5[n]) for n in ("Q", "K", "V"))
+    return qkv, golden("calibration")
+
+
+@pytest.mark.parametrize("agg", ["mean", "min"])
+def test_head_similarity_matches_reference(calib, agg):
+    (Q, K, V), z = calib
+    for a, b in ((0, 1), (0, 3), (2, 3), (1, 1)):
+        np.testing.assert_allclose(orc.head_similarity(Q, K, V, a, b, k=16, how=agg), z[f"hs_{agg}_{a}_{b}"],
+                                   rtol=0, atol=1e-6)
+
+
+def test_head_maps_match_reference(calib, config1):
+    (Q, K, V), z = calib
+    maps = orc.head_maps(Q, K, V, [0, 2], k=16)
+    got = np.array([maps.get(l, [-1, -1]) for l in range(4)], np.int32)
+    np.testing.assert_array_equal(got, z["maps_A"])
+    (Q1, K1, V1), _ = config1
+    maps1 = orc.head_maps(Q1, K1, V1, [0, 2], k=64)
+    np.testing.assert_array_equal(np.array([maps1.get(l, [-1, -1]) for l in range(4)], np.int32), z["maps1"])
+    np.testing.assert_allclose(orc.head_similarity(Q1, K1, V1, 0, 1, k=64), z["hs1_0_1"], rtol=0, atol=1e-6)
+
+
+@pytest.mark.parametrize("agg", ["mean", "min"])
+def test_similarity_matrices_match_reference(calib, agg):
+    (Q, K, V), z = calib
+    S, und = orc.planning_matrix(Q, K, V, k=16, how=agg, tile=64)
+    np.testing.assert_allclose(S, z[f"S_planning_{agg}"], rtol=0, atol=1e-6)
+    assert und == int(z[f"und_planning_{agg}"])
+    S, und = orc.diagnostic_matrix(Q, K, V, k=16, how=agg)
+    np.testing.assert_allclose(S, z[f"S_diagnostic_{agg}"], rtol=0, atol=1e-6)
+    assert und == int(z[f"und_diagnostic_{agg}"])
+    if agg == "min":
+        S, und = orc.planning_matrix(Q, K, V, k=16, how="min", tile=64, phase="decode")
+        np.testing.assert_allclose(S, z["S_planning_decode_min"], rtol=0, atol=1e-6)
+        assert und == int(z["und_planning_decode_min"])
