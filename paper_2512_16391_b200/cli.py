@@ -1,9 +1,14 @@
-"""``python -m paper_2512_16391_b200 run|cost``: the reference CLI's ``run``
-subcommand (cli.py:80-89,216-233) on the B200 engine, and its ``cost``
-subcommand (cli.py:90-105,236-300) over the B200 presets (costmodel.py).
+"""``python -m paper_2512_16391_b200 run|plan|cost``: the reference CLI's
+``run`` subcommand (cli.py:80-89,216-233) on the B200 engine, its ``plan``
+subcommand (cli.py:66-78,195-213) on the GPU calibration (calibration.py),
+and its ``cost`` subcommand (cli.py:90-105,236-300) over the B200 presets
+(costmodel.py).
 
     python -m paper_2512_16391_b200 run --trace t.kscd --plan p.json \\
         [--phase prefill|decode] [--mode remapped|all-heads-pooled] [--out report.json] [--fail-above X]
+    python -m paper_2512_16391_b200 plan --trace a.kscd [b.kscd ...] --out plan.json [--budget 5] [--k 64]
+        [--token-agg min|mean] [--tile-size 128] [--pooling post|pre] [--mode remapped|all-heads-pooled]
+        [--fraction 0.1] [--k-min 128] [--no-importance]
     python -m paper_2512_16391_b200 cost [--preset b200-decode-131072-k10 ...] [--list-presets]
         [--ratios a0,a,r | --predict] [--phase] [--fraction] [--seq-len] [--layers] [--anchors]
         [--baseline-time] [--csv] [--out results.json]
@@ -37,6 +42,19 @@ def build_parser():
     run.add_argument("--fail-above", type=float, default=None)
     run.add_argument("--engine", choices=["b200"], default="b200",
                      help="accepted for parity with `kascade run --engine b200`; there is no other engine")
+    plan = sub.add_parser("plan", help="select anchors and head maps on the GPU, write a plan file")
+    plan.add_argument("--trace", nargs="+", required=True)
+    plan.add_argument("--budget", type=int, default=5)
+    plan.add_argument("--k", type=int, default=64)
+    plan.add_argument("--token-agg", choices=["mean", "min"], default="min")
+    plan.add_argument("--tile-size", type=int, default=128)
+    plan.add_argument("--pooling", choices=["post", "pre"], default="post")
+    plan.add_argument("--mode", choices=["remapped", "all-heads-pooled"], default="remapped")
+    plan.add_argument("--fraction", type=float, default=0.1)
+    plan.add_argument("--k-min", type=int, default=128)
+    plan.add_argument("--no-importance", action="store_true",
+                      help="skip importance weighting even when X/Y are present")
+    plan.add_argument("--out", required=True)
     cost = sub.add_parser("cost", help="weighted-average pipeline time and speedup (B200 presets)")
     cost.add_argument("--preset", action="append", default=None,
                       help="B200 preset name (repeatable); see --list-presets")
@@ -116,6 +134,22 @@ def cmd_cost(args) -> int:
     return EXIT_OK
 
 
+def cmd_plan(args) -> int:
+    """cli.py:195-213 with the similarity matrix and head maps on the GPU."""
+    from . import calibration, kscd_io
+    from .host_types import KBudgetPolicy, write_plan
+    traces = [kscd_io.TraceFile(p) for p in args.trace]
+    plan = calibration.build_plan(traces, budget=args.budget, k=args.k, token_agg=args.token_agg,
+                                  tile_size=args.tile_size, pooling=args.pooling,
+                                  mode=args.mode.replace("-", "_"),
+                                  k_policy=KBudgetPolicy(args.fraction, args.k_min),
+                                  use_importance=not args.no_importance)
+    write_plan(args.out, plan)
+    print(f"anchors={plan.core.anchors} objective={plan.core.objective_value:.6g} "
+          f"mode={plan.mode} pooling={plan.pooling} -> {args.out}")
+    return EXIT_OK
+
+
 def cmd_run(args) -> int:
     from . import compat, kscd_io
     from .host_types import read_plan
@@ -145,7 +179,7 @@ def main(argv=None) -> int:
     except SystemExit as e:
         return int(e.code or 0)
     try:
-        return cmd_cost(args) if args.command == "cost" else cmd_run(args)
+        return {"cost": cmd_cost, "plan": cmd_plan, "run": cmd_run}[args.command](args)
     except (KascadeError, OSError) as e:
         sys.stderr.write(f"{build_parser().prog}: {e}\n")
         return EXIT_DATA

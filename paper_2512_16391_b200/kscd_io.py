@@ -103,6 +103,18 @@ class TraceFile:
     head_dim = property(lambda self: self.d)
     seq_len = property(lambda self: self.N)
 
+    @property
+    def X(self):
+        """Zero-copy [L][N][model_dim] fp32 view of the attention inputs (None without X/Y)."""
+        return self._view(self.off_end, (self.L, self.N, self.model_dim)) if self.has_xy else None
+
+    @property
+    def Y(self):
+        """Zero-copy [L][N][model_dim] fp32 view of the attention outputs (None without X/Y)."""
+        if not self.has_xy:
+            return None
+        return self._view(self.off_end + self.L * self.N * self.model_dim * 4, (self.L, self.N, self.model_dim))
+
     def layer_device(self, layer: int, device="cuda"):
         """One layer as bf16 CUDA tensors (Q [Hq][N][d], K/V [Hkv][N][d]):
         mmap slice -> reused pinned staging buffer -> async H2D on the

@@ -50,6 +50,32 @@ def main():
     np.savez_compressed(os.path.join(HERE, "calib_plan.npz"), **out)
     print("anchors", plan.anchors, "maps", out["maps"].tolist())
 
+    # `kascade plan` (cli.py:195-213) on the CLI golden trace (cli_cases.json)
+    import contextlib
+    import io
+    import json
+    import tempfile
+    from kascade import cli as ref_cli
+    from kascade import traceio as ref_io
+    c = json.load(open(os.path.join(HERE, "cli_cases.json")))
+    a = c["trace_args"]
+    Q, K, V = orc.synth_qkv(a["L"], a["Hq"], a["Hkv"], a["d"], a["N"], seed=a["seed"], rho=a["rho"], perms=a["perms"])
+    Q, K, V = (orc.bf16_round(x) for x in (Q, K, V))
+    tc = AttentionTrace(num_layers=a["L"], num_query_heads=a["Hq"], num_kv_heads=a["Hkv"], head_dim=a["d"],
+                        seq_len=a["N"], Q=Q, K=K, V=V, prompt_id=c["trace_prompt_id"])
+    with tempfile.TemporaryDirectory() as td:
+        tpath, ppath = os.path.join(td, "t.kscd"), os.path.join(HERE, "cli_plan_built.json")
+        ref_io.write_trace(tpath, tc)
+        argv = ["plan", "--trace", tpath, "--budget", "2", "--k", "32", "--tile-size", "64", "--fraction", "0.1",
+                "--k-min", "16", "--out", ppath]
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            code = ref_cli.main(argv)
+        assert code == 0
+        meta = {"argv": argv[3:], "stdout": buf.getvalue().replace(ppath, "OUT")}
+        json.dump(meta, open(os.path.join(HERE, "cli_plan_built_meta.json"), "w"), indent=1)
+        print(buf.getvalue())
+
 
 if __name__ == "__main__":
     main()

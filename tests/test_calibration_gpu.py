@@ -127,3 +127,21 @@ def test_calibration_errors(cuda_ok, tA):
         cal.compute_head_maps(tA, [0, 2], head_map_mode="bogus")
     with pytest.raises(InvalidArgumentError):
         cal.compute_head_map(np.zeros((2, 3)))
+
+
+def test_plan_cli_matches_reference_cli(cuda_ok, tmp_path, capsys):
+    """`python -m paper_2512_16391_b200 plan` vs the reference's `kascade
+    plan` on the CLI golden trace (same arguments, streamed from the KSCD
+    file): identical anchors, head maps and policy; objective to 1e-4."""
+    from paper_2512_16391_b200 import cli
+    from test_kscd_io import cli_trace
+    path, _ = cli_trace(tmp_path)
+    meta = json.load(open(os.path.join(GOLDEN, "cli_plan_built_meta.json")))
+    out = tmp_path / "plan.json"
+    assert cli.main(["plan", "--trace", str(path), *meta["argv"], "--out", str(out)]) == 0
+    text = capsys.readouterr().out
+    assert text.split(" -> ")[0].split(" objective=")[0] == meta["stdout"].split(" objective=")[0]
+    got, want = json.load(open(out)), json.load(open(os.path.join(GOLDEN, "cli_plan_built.json")))
+    assert abs(got.pop("objective_value") - want.pop("objective_value")) < 1e-4
+    got.pop("source_digest", None), want.pop("source_digest", None)
+    assert got == want
