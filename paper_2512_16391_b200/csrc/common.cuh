@@ -157,6 +157,23 @@ KSCD_DEV float4 lds_f4(uint32_t addr) {
   return v;
 }
 
+// Max of N register values as 8 independent FMNMX3 chains and a short
+// combine (a single running max is a 64-deep dependent chain at N = 128).
+template <int N>
+KSCD_DEV float max_tree(const float* s) {
+  static_assert(N % 16 == 0, "N must be a multiple of 16");
+  float m[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) m[k] = fmaxf(s[2 * k], s[2 * k + 1]);
+#pragma unroll
+  for (int c = 16; c < N; c += 16)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m[k] = fmaxf(m[k], fmaxf(s[c + 2 * k], s[c + 2 * k + 1]));
+  const float a = fmaxf(m[0], fmaxf(m[1], m[2]));
+  const float b = fmaxf(m[3], fmaxf(m[4], m[5]));
+  return fmaxf(fmaxf(a, b), fmaxf(m[6], m[7]));
+}
+
 template <typename T>
 KSCD_DEV T warp_max(T v) {
 #pragma unroll

@@ -29,6 +29,8 @@
 //           none falls back to V[r]: topk_attention, attention.py:185-253,
 //           _routed_selections, runner.py:210-225.  O, LSE
 //   LSE     QK^T + online softmax statistics only (anchor pass A)
+#include <stdlib.h>
+
 #include "sm100.cuh"
 #include "kscd_internal.h"
 
@@ -148,6 +150,8 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
         auto issue_pv = [&](int t, int st, int j) {
           const uint32_t d = tmem + t * 256 + 128;
           const uint32_t p = tmem + t * 256;
+          mbar_wait(&bars[9 + t], j & 1);          // P_t(j) written
+          tc_fence_after();
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks) {
             mma_ts(d, p + ks * 8, sw128_desc(vaddr + st * kTileBytes + ks * 2048, kHalf, 1024), kIdescPV,
@@ -190,8 +194,6 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
           const uint32_t ph1 = ((j + 1) / kStages) & 1;
           if (MODE != PMODE_LSE) mbar_wait(&bars[3 + st], ph);
           // tile 0: PV_j, then S_{j+1}
-          mbar_wait(&bars[9], j & 1);
-          tc_fence_after();
           if (MODE != PMODE_LSE) {
             issue_pv(0, st, j);
             if (j == nb - 1) mma_commit(&bars[11]);
@@ -202,8 +204,6 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
             issue_s(0, st1);
           }
           if (nslots == 2) {
-            mbar_wait(&bars[10], j & 1);
-            tc_fence_after();
             if (MODE != PMODE_LSE) {
               issue_pv(1, st, j);
               if (j == nb - 1) mma_commit(&bars[12]);
@@ -355,9 +355,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
               if (k0 + c > lim) s[c] = -INFINITY;
           }
         }
-        float mx_raw = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < 128; ++c) mx_raw = fmaxf(mx_raw, s[c]);
+        const float mx_raw = max_tree<128>(s);
         const float mx = mx_raw * a.scale_log2;   // scale > 0: max commutes
         // Lazy rescale: a row moves its reference max only when the block max
         // exceeds it by > 2^8.  tcgen05.ld/st are warp-collective, so the O
@@ -384,12 +382,13 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
         const float mu = m_used == -INFINITY ? 0.f : m_used;
         const float2 sc2 = make_float2(a.scale_log2, a.scale_log2);
         const float2 nm2 = make_float2(-mu, -mu);
-        float2 sum2 = make_float2(0.f, 0.f);
+        float2 sum4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                          make_float2(0.f, 0.f)};   // 4 independent FADD2 chains
         if (MODE == PMODE_LSE) {
 #pragma unroll
           for (int c = 0; c < 128; c += 2) {
             const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sc2, nm2);
-            sum2 = __fadd2_rn(sum2, exp2_pair_sum<KSCD_LSE_POLY>(x, c >> 1));
+            sum4[(c >> 1) & 3] = __fadd2_rn(sum4[(c >> 1) & 3], exp2_pair_sum<KSCD_LSE_POLY>(x, c >> 1));
           }
         } else {
 #pragma unroll
@@ -399,7 +398,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
             for (int i = 0; i < 16; ++i) {
               const float2 x = __ffma2_rn(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sc2, nm2);
               const float2 p = exp2_pair(x, c * 16 + i);
-              sum2 = __fadd2_rn(sum2, p);
+              sum4[i & 3] = __fadd2_rn(sum4[i & 3], p);
               r[i] = pack_bf16(p.x, p.y);
             }
             // 16 packed columns: the key pairs of this 32-key chunk
@@ -412,6 +411,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
           }
           tmem_st_wait();
         }
+        const float2 sum2 = __fadd2_rn(__fadd2_rn(sum4[0], sum4[1]), __fadd2_rn(sum4[2], sum4[3]));
         l += sum2.x + sum2.y;
         tc_fence_before();
         mbar_arrive(&bars[MODE == PMODE_LSE ? 11 + t + 2 * (j & 1) : 9 + t]);
@@ -484,14 +484,20 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
+bool make_prefill_map_box(CUtensorMap* m, const void* base, int heads, int rows, int64_t head_stride, int box_rows);
+
 // [heads][rows][128] bf16 with row stride 128 and head stride `head_stride`
 // elements, box {64, 128, 1}, 128B swizzle.
 bool make_prefill_map(CUtensorMap* m, const void* base, int heads, int rows, int64_t head_stride) {
+  return make_prefill_map_box(m, base, heads, rows, head_stride, 128);
+}
+
+bool make_prefill_map_box(CUtensorMap* m, const void* base, int heads, int rows, int64_t head_stride, int box_rows) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {128, (cuuint64_t)rows, (cuuint64_t)heads};
   cuuint64_t strides[2] = {256, (cuuint64_t)head_stride * 2};
-  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -513,7 +519,14 @@ static cudaError_t launch_prefill_mode(const PrefillArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+bool prefill_pair_supported(int mode, const PrefillArgs& a);
+cudaError_t launch_prefill_pair(int mode, const PrefillArgs& a, cudaStream_t st);
+
 cudaError_t launch_prefill_attn(int mode, const PrefillArgs& a, cudaStream_t st) {
+  // CTA pairs (prefill_pair.cu, 2-SM UMMA) are opt-in (KSCD_PREFILL_PAIR=1):
+  // measured slower than the single-CTA ping-pong.
+  static const char* knob = getenv("KSCD_PREFILL_PAIR");
+  if (knob && knob[0] == '1' && prefill_pair_supported(mode, a)) return launch_prefill_pair(mode, a, st);
   switch (mode) {
     case PMODE_DENSE: return launch_prefill_mode<PMODE_DENSE>(a, st);
     case PMODE_SPARSE: return launch_prefill_mode<PMODE_SPARSE>(a, st);

@@ -2,8 +2,8 @@ import sys, torch
 sys.path.insert(0, "/root/repo")
 from paper_2512_16391_b200 import ops
 torch.manual_seed(0)
-for N in (64, 128, 192, 256, 300):
-    for Hq, Hkv in ((2, 1), (4, 2)):
+for N in (64, 128, 192, 256, 300, 1000):
+    for Hq, Hkv in ((4, 1), (8, 2), (16, 2)):
         q = torch.randn(Hq, N, 128, device="cuda").bfloat16()
         k = torch.randn(Hkv, N, 128, device="cuda").bfloat16()
         v = torch.randn(Hkv, N, 128, device="cuda").bfloat16()
