@@ -641,7 +641,8 @@ def main():
                "d2h_bytes_per_step": out_host.numel() * 4,
                "note": "KascadeDecoder.capture_host_step: one CUDA graph per step = pinned H2D of the step's q "
                        "and new K/V rows, one append launch into the 32 layers' caches, the layer loop, D2H "
-                       "of all 32 layers' outputs; host-synchronised every step"}
+                       "of all 32 layers' outputs (copies pipelined against the layers on two graph branches); "
+                       "host-synchronised every step"}
 
     # ---- prefill at 128K (secondary metric of the same line) -------------
     del g_kas, g_den, dec, Kc, Vc, Ks, Vs, q

@@ -74,31 +74,34 @@ class KascadeDecoder:
         Returns the preallocated fp32 outputs [L][B][Hq][128]."""
         if seq_len > self.n_max:
             raise InvalidArgumentError(f"seq_len {seq_len} exceeds max_seq_len {self.n_max}")
-        pol = self.plan.k_policy
-        k = k_budget(pol, seq_len)
-        idx = self.indices[:, :, :k]
-        for l, kind in enumerate(self.kinds):
-            ql, kl, vl = q[l], k_caches[l], v_caches[l]
-            if kind == KIND_REUSE:
-                ops.sparse_decode(ql, kl, vl, seq_len, self.indices, self.counts, self.head_maps[l],
-                                  out=self.out[l])
-                continue
-            if kind == KIND_ANCHOR0:
-                ops.dense_decode(ql, kl, vl, seq_len, out=self.out[l], lse=self.lse, scores=self.scores)
-            else:
-                ops.anchor_scores_decode(ql, kl, seq_len, self.scores, self.lse)
-            ops.select_decode(self.scores, self.lse, seq_len, pol, self.Hkv, indices=self.indices,
-                              counts=self.counts, pooled=self.pooled, all_heads=self.all_heads)
-            if kind == KIND_ANCHOR:
-                ops.sparse_decode(ql, kl, vl, seq_len, self.indices, self.counts, self.shared_map,
-                                  out=self.out[l])
-        del idx
+        for l in range(self.L):
+            self._layer(l, q, k_caches, v_caches, seq_len)
         return self.out
+
+    def _layer(self, l: int, q, k_caches, v_caches, seq_len: int) -> None:
+        """The kernels of layer l (runner.py:250-275 for one decode token)."""
+        pol = self.plan.k_policy
+        kind = self.kinds[l]
+        ql, kl, vl = q[l], k_caches[l], v_caches[l]
+        if kind == KIND_REUSE:
+            ops.sparse_decode(ql, kl, vl, seq_len, self.indices, self.counts, self.head_maps[l], out=self.out[l])
+            return
+        if kind == KIND_ANCHOR0:
+            ops.dense_decode(ql, kl, vl, seq_len, out=self.out[l], lse=self.lse, scores=self.scores)
+        else:
+            ops.anchor_scores_decode(ql, kl, seq_len, self.scores, self.lse)
+        ops.select_decode(self.scores, self.lse, seq_len, pol, self.Hkv, indices=self.indices,
+                          counts=self.counts, pooled=self.pooled, all_heads=self.all_heads)
+        if kind == KIND_ANCHOR:
+            ops.sparse_decode(ql, kl, vl, seq_len, self.indices, self.counts, self.shared_map, out=self.out[l])
+
+    def _dense_layer(self, l: int, q, k_caches, v_caches, seq_len: int) -> None:
+        ops.dense_decode(q[l], k_caches[l], v_caches[l], seq_len, out=self.out[l], lse=self.lse)
 
     def dense_step(self, q, k_caches, v_caches, seq_len: int) -> torch.Tensor:
         """Top-k = 100% baseline: dense attention on every layer."""
         for l in range(self.L):
-            ops.dense_decode(q[l], k_caches[l], v_caches[l], seq_len, out=self.out[l], lse=self.lse)
+            self._dense_layer(l, q, k_caches, v_caches, seq_len)
         return self.out
 
     # -------------------------------------------------------------- graphs
@@ -127,21 +130,47 @@ class KascadeDecoder:
                 raise InvalidArgumentError(f"{name} must be pinned host memory")
         kv_dev = torch.empty(kv_host.shape, dtype=torch.bfloat16, device=self.device)
         tables = ops.cache_pointer_tables(k_caches, v_caches, self.device)
-        fn = self.dense_step if dense else self.step
+        layer = self._dense_layer if dense else self._layer
+        # The copies are pipelined against the layer loop on two side streams
+        # (graph branches): the new K/V rows and layer 0's queries arrive
+        # first, the other layers' queries stream in behind layer 0, and each
+        # layer's output leaves as soon as that layer is done -- only the
+        # first H2D and the last layer's D2H stay on the critical path.
+        h2d, d2h = torch.cuda.Stream(device=self.device), torch.cuda.Stream(device=self.device)
+        ev_first = torch.cuda.Event()
+        ev_q = [torch.cuda.Event() for _ in range(self.L)]
+        ev_done = [torch.cuda.Event() for _ in range(self.L)]
 
         def body():
-            q.copy_(q_host, non_blocking=True)
-            kv_dev.copy_(kv_host, non_blocking=True)
+            main = torch.cuda.current_stream()
+            h2d.wait_stream(main)
+            d2h.wait_stream(main)
+            with torch.cuda.stream(h2d):
+                kv_dev.copy_(kv_host, non_blocking=True)
+                q[0].copy_(q_host[0], non_blocking=True)
+                ev_first.record(h2d)
+                for l in range(1, self.L):
+                    q[l].copy_(q_host[l], non_blocking=True)
+                    ev_q[l].record(h2d)
+            main.wait_event(ev_first)
             ops.append_kv(kv_dev, seq_len - 1, tables)
-            fn(q, k_caches, v_caches, seq_len)
-            out_host.copy_(self.out, non_blocking=True)
+            for l in range(self.L):
+                if l > 0:
+                    main.wait_event(ev_q[l])
+                layer(l, q, k_caches, v_caches, seq_len)
+                ev_done[l].record(main)
+                with torch.cuda.stream(d2h):
+                    d2h.wait_event(ev_done[l])
+                    out_host[l].copy_(self.out[l], non_blocking=True)
+            main.wait_stream(h2d)
+            main.wait_stream(d2h)
 
         body()
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             body()
-        self._graphs[("host", seq_len, dense)] = (g, kv_dev, tables)   # keep the staging alive
+        self._graphs[("host", seq_len, dense)] = (g, kv_dev, tables, h2d, d2h)   # keep the staging alive
         return g
 
 
