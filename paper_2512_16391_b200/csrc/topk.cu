@@ -577,6 +577,11 @@ static cudaError_t launch_topk_cl(const TopkArgs& a, cudaStream_t st) {
     topk_kernel<1, AGG><<<a.rows, kTopkThreads, 0, st>>>(a);
     return cudaGetLastError();
   }
+  if (CL > 8) {
+    static const cudaError_t np = cudaFuncSetAttribute(topk_kernel<CL, AGG>,
+                                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (np != cudaSuccess) return np;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.rows * CL);
   cfg.blockDim = dim3(kTopkThreads);
@@ -610,14 +615,16 @@ cudaError_t launch_topk(const TopkArgs& a, cudaStream_t st) {
     return cudaGetLastError();
   }
   if (forced && forced[0]) {
-    cl = forced[0] == '8' ? 8 : (forced[0] == '4' ? 4 : (forced[0] == '2' ? 2 : 1));
+    cl = forced[0] == 'g' ? 16 : forced[0] == '8' ? 8 : (forced[0] == '4' ? 4 : (forced[0] == '2' ? 2 : 1));
     agg = forced[1] == '1';
   } else {
-    // Few long rows (decode: batch x kv heads) -> a cluster of 4 CTAs per row.
-    // Measured on B200 (64 rows x 128K): 1 CTA 141 us, 2: 83, 4: 65, 8: 85;
-    // match_any aggregation costs more than the atomics it saves.
-    cl = (a.rows * 4 <= 4 * 148 && a.len >= 8192) ? 4 : 1;
+    // Few long rows (decode: batch x kv heads) -> a cluster of CTAs per row.
+    // Measured on B200 at 128K: 64 rows: 1 CTA 141 us, 2: 83, 4: 65, 8: 85;
+    // 16 rows: 4: 64, 8: 54; 8 rows: 4: 62, 8: 44.  match_any aggregation
+    // costs more than the atomics it saves.
+    cl = a.len < 8192 ? 1 : (a.rows * 8 <= 148 ? 8 : (a.rows <= 148 ? 4 : 1));
   }
+  if (cl == 16) return agg ? launch_topk_cl<16, 1>(a, st) : launch_topk_cl<16, 0>(a, st);
   if (cl == 8) return agg ? launch_topk_cl<8, 1>(a, st) : launch_topk_cl<8, 0>(a, st);
   if (cl == 4) return agg ? launch_topk_cl<4, 1>(a, st) : launch_topk_cl<4, 0>(a, st);
   if (cl == 2) return agg ? launch_topk_cl<2, 1>(a, st) : launch_topk_cl<2, 0>(a, st);

@@ -159,9 +159,10 @@ def test_topk_ties_and_padding(cuda_ok):
             assert (idx[r, ref.size:] == 2**31 - 1).all()
 
 
-@pytest.mark.parametrize("dist", ["lognormal", "heavy", "tied_block"])
+@pytest.mark.parametrize("dist", ["lognormal", "heavy", "tied_block", "aliased"])
 def test_topk_long_rows_exact(cuda_ok, dist):
-    # long rows take the sample-bracketed path; tied blocks force its exact fallback
+    # long rows take the sample-banded first radix digit; tied blocks and a
+    # pattern aliased with the sample stride force its exact fallback
     from paper_2512_16391_b200 import ops
     rng = np.random.default_rng(17)
     n = 150001
@@ -169,9 +170,12 @@ def test_topk_long_rows_exact(cuda_ok, dist):
         w = np.exp(rng.standard_normal((3, n)) * 2).astype(np.float32)
     elif dist == "heavy":
         w = (rng.pareto(1.5, (3, n)) + 1e-9).astype(np.float32)
-    else:
+    elif dist == "tied_block":
         w = np.exp(rng.standard_normal((3, n))).astype(np.float32)
         w[:, 1000:60000] = np.float32(1.5)          # a huge tie straddling the threshold
+    else:
+        w = rng.random((3, n)).astype(np.float32)
+        w[:, ::16] += np.float32(10.0)              # every sampled key is large: the band misses
     for k in (1, 128, 15000, 149999):
         idx, cnt = ops.topk(_dev(w), k, k_cap=k)
         idx = idx.cpu().numpy()
