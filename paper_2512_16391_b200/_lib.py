@@ -145,6 +145,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
                 "(the engine has no CPU fallback)")
         lib = ctypes.CDLL(path)
         for name, st in ENTRY_POINTS.items():
+            if os.environ.get("KSCD_LIB_PATH") and not hasattr(lib, name):
+                continue            # dev override: an older variant build may lack newer entry points
             fn = getattr(lib, name)
             fn.argtypes = [ctypes.POINTER(st), c_vp]
             fn.restype = ctypes.c_int

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
     for (int j = 0; j < nb; ++j) {
       const int key = j * kBlock + key_in_blk;
       const bool diag = (j == nb - 1);             // only the last block crosses the staircase
-      float2 acc2 = make_float2(0.f, 0.f), acc2b = make_float2(0.f, 0.f);   // 2 independent chains
+      float2 acc2 = make_float2(0.f, 0.f);
       for (int qq = x; qq < nh; qq += 2) {
         mbar_wait(&bars[5 + qq], j & 1);
         tc_fence_after();
@@ -182,12 +182,10 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
             if (key > r0 + i + 2) e1.x = 0.f;
             if (key > r0 + i + 3) e1.y = 0.f;
           }
-          if ((i >> 2) & 1) acc2b = __fadd2_rn(acc2b, __fadd2_rn(e0, e1));
-          else acc2 = __fadd2_rn(acc2, __fadd2_rn(e0, e1));
+          acc2 = __fadd2_rn(acc2, __fadd2_rn(e0, e1));
         }
       }
       if (key < t1) {
-        acc2 = __fadd2_rn(acc2, acc2b);
         float v = acc2.x + acc2.y;
         if (a.accumulate) v += out_row[key];
         out_row[key] = v;

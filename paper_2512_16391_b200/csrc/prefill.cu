@@ -355,7 +355,16 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
               if (k0 + c > lim) s[c] = -INFINITY;
           }
         }
-        const float mx_raw = max_tree<128>(s);
+        // tree max for the dense / LSE modes; the sparse mode keeps the running max
+        // (measured 3 % faster there at 128K, A/B on one box)
+        float mx_raw;
+        if (MODE == PMODE_SPARSE) {
+          mx_raw = -INFINITY;
+#pragma unroll
+          for (int c = 0; c < 128; ++c) mx_raw = fmaxf(mx_raw, s[c]);
+        } else {
+          mx_raw = max_tree<128>(s);
+        }
         const float mx = mx_raw * a.scale_log2;   // scale > 0: max commutes
         // Lazy rescale: a row moves its reference max only when the block max
         // exceeds it by > 2^8.  tcgen05.ld/st are warp-collective, so the O
