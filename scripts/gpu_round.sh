@@ -18,7 +18,7 @@ for s in $STEPS; do
       echo "bench rc=$?"; tail -c 600 $O/bench_$TAG.json ;;
     launches)
       timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-        --log-file $O/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline \
+        --log-file $O/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-configs \
         > $O/launches_$TAG.out 2>&1
       echo "launches rc=$?" ;;
     full)
