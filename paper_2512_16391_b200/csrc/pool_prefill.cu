@@ -47,6 +47,32 @@ struct PoolTmaps {
   CUtensorMap q, k;
 };
 
+// Sum over the 128 (head, row) columns of one S^T quarter held by this
+// thread (its key): exp2(s * scale * log2e - lse2[row]), rows after the key
+// zeroed on the diagonal block (the causal zeros of _post_pooled).
+template <bool DIAG>
+KSCD_DEV float2 pool_colsum(const uint32_t (&r)[128], uint32_t l4, float2 sc2, int key, int r0) {
+  float2 acc2 = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < 128; i += 4) {
+    const float4 lv = lds_f4(l4 + i * 4);    // broadcast read: same rows for every key
+    float2 e0 = __ffma2_rn(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sc2,
+                           make_float2(-lv.x, -lv.y));
+    float2 e1 = __ffma2_rn(make_float2(__uint_as_float(r[i + 2]), __uint_as_float(r[i + 3])), sc2,
+                           make_float2(-lv.z, -lv.w));
+    e0 = exp2_pair_sum<KSCD_PB_POLY>(e0, i >> 1);
+    e1 = exp2_pair_sum<KSCD_PB_POLY>(e1, (i >> 1) + 1);
+    if (DIAG) {
+      if (key > r0 + i) e0.x = 0.f;
+      if (key > r0 + i + 1) e0.y = 0.f;
+      if (key > r0 + i + 2) e1.x = 0.f;
+      if (key > r0 + i + 3) e1.y = 0.f;
+    }
+    acc2 = __fadd2_rn(acc2, __fadd2_rn(e0, e1));
+  }
+  return acc2;
+}
+
 // bars: 0 q_full | 1-2 k_full[s] | 3-4 k_empty[s] | 5-6 s_full[x] | 7-8 buf_free[x]
 __global__ void __launch_bounds__(pp::kThreads, 1)
     pool_prefill_kernel(const __grid_constant__ PoolTmaps tm, const PoolPrefillArgs a) {
@@ -167,23 +193,9 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
         tc_fence_before();
         mbar_arrive(&bars[9 + qq]);                // buffer free: the MMA may refill it
         const uint32_t l4 = smem_u32(lse2 + 128 * qq);
-#pragma unroll
-        for (int i = 0; i < 128; i += 4) {
-          const float4 lv = lds_f4(l4 + i * 4);    // broadcast read: same rows for every key
-          float2 e0 = __ffma2_rn(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sc2,
-                                 make_float2(-lv.x, -lv.y));
-          float2 e1 = __ffma2_rn(make_float2(__uint_as_float(r[i + 2]), __uint_as_float(r[i + 3])), sc2,
-                                 make_float2(-lv.z, -lv.w));
-          e0 = exp2_pair_sum<KSCD_PB_POLY>(e0, i >> 1);
-          e1 = exp2_pair_sum<KSCD_PB_POLY>(e1, (i >> 1) + 1);
-          if (diag) {
-            if (key > r0 + i) e0.x = 0.f;
-            if (key > r0 + i + 1) e0.y = 0.f;
-            if (key > r0 + i + 2) e1.x = 0.f;
-            if (key > r0 + i + 3) e1.y = 0.f;
-          }
-          acc2 = __fadd2_rn(acc2, __fadd2_rn(e0, e1));
-        }
+        // separate instantiations: the staircase mask costs 2 ALU ops per
+        // element, and only the last block needs it
+        acc2 = __fadd2_rn(acc2, diag ? pool_colsum<true>(r, l4, sc2, key, r0) : pool_colsum<false>(r, l4, sc2, key, r0));
       }
       if (key < t1) {
         float v = acc2.x + acc2.y;
