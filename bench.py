@@ -328,6 +328,13 @@ def bench_prefill(args, dev, world, dist):
     G = Hq // Hkv
     flops_reuse = 4.0 * d * G * float((cnt * rows[None, :]).sum())
     flops_dense = 2.0 * d * Hq * N * (N + 1)
+    # K/V bytes the sparse kernel gathers: every CTA (two q heads of a kv
+    # group) gathers its tile's selected rows (256 B of K + 256 B of V each)
+    gather_bytes = float(cnt.sum()) * 512.0 * (Hq // 2) / Hkv
+    try:
+        gather_peak = float(json.load(open(os.path.join(REPO, "profiles", "gather_ceiling.json")))["l2_resident_32MB_GBs"])
+    except (OSError, KeyError, ValueError):
+        gather_peak = None
     peaks, kind = load_peaks()
     tpk = float(peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"]))
     n_anchor, n_reuse = len(LLAMA_ANCHORS) - 1, L - len(LLAMA_ANCHORS)
@@ -358,7 +365,12 @@ def bench_prefill(args, dev, world, dist):
                      "frac": round(flops_reuse / (t_reuse * 1e-3) / 1e12 / tpk, 4),
                      "traffic": load_traffic(f"sparse_prefill_{N // 1024}k"),
                      "peak_kind": kind,
-                     "dense_prefill_frac": round(flops_dense / (t_dense * 1e-3) / 1e12 / tpk, 4)},
+                     "dense_prefill_frac": round(flops_dense / (t_dense * 1e-3) / 1e12 / tpk, 4),
+                     "gather": {"bound": "l2_gather", "bytes_per_launch": int(gather_bytes),
+                                "achieved": round(gather_bytes / (t_reuse * 1e-3) / 1e9, 1), "peak": gather_peak,
+                                "unit": "GB/s", "peak_kind": "measured (scripts/micro/gather_bench.cu)",
+                                "frac": round(gather_bytes / (t_reuse * 1e-3) / 1e9 / gather_peak, 4)
+                                if gather_peak else None}},
         "gpu_launches_per_step": 1 * 3 + n_anchor * 4 + n_reuse,
         "cpu_baseline": cpu_prefill,
     }

@@ -89,7 +89,7 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 int main(int argc, char** argv) {
-  const int nrows = 131072;                       // one kv head at 128K: 32 MB
+  const int nrows = argc > 3 ? atoi(argv[3]) : 131072;   // 131072 rows = 32 MB (L2-resident); 16M rows = 4 GB (HBM)
   const int nblocks = argc > 1 ? atoi(argv[1]) : 50;
   const int grid = argc > 2 ? atoi(argv[2]) : 148;
   const int npos = 200000;
@@ -102,7 +102,7 @@ int main(int argc, char** argv) {
   srand(1);
   for (int i = 0; i < npos; i += kRows) {     // sorted random selections per block, like Top-k lists
     std::vector<int> blk(kRows);
-    for (int r = 0; r < kRows; ++r) blk[r] = rand() % nrows;
+    for (int r = 0; r < kRows; ++r) blk[r] = (int)(((long long)rand() * 32768 + rand()) % nrows);
     std::sort(blk.begin(), blk.end());
     for (int r = 0; r < kRows && i + r < npos; ++r) hp[i + r] = blk[r];
   }
@@ -127,7 +127,7 @@ int main(int argc, char** argv) {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  for (int mode = 0; mode < 2; ++mode) {
+  for (int mode = 0; mode < (argc > 4 ? atoi(argv[4]) : 2); ++mode) {
     for (int it = 0; it < 3; ++it) {
       cudaEventRecord(a);
       if (mode == 0) gather_kernel<0><<<grid, 128, smem>>>(tm, k, pos, nblocks, npos, sink);
