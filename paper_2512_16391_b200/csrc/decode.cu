@@ -57,6 +57,15 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
   const __nv_bfloat16* kbase = a.k + (int64_t)b * a.kv_sb + (int64_t)g * a.kv_sh;
   const __nv_bfloat16* vbase = a.v + (int64_t)b * a.kv_sb + (int64_t)g * a.kv_sh;
   const int* sel = nullptr;
+  // Programmatic dependent launch (consecutive decode layers): let the next
+  // layer's kernel start filling SMs as ours retire.  Our inputs are all
+  // complete when we start -- q and the caches are static within a step, the
+  // index lists come from a select launch that never triggers early, and no
+  // decode launch ever directly follows the pooling kernel that reads the
+  // score buffer we may stream into -- so only the merge below (its
+  // workspace and counters are shared with the previous layer's kernel, and
+  // it writes out / lse) waits for the previous grid.
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   int count = a.n;
   if (MODE == MODE_SPARSE) {
     const int src = a.head_map ? __ldg(a.head_map + g) : g;
@@ -234,6 +243,7 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
   }
   cp_async_wait<0>();
   __syncthreads();
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
 
   // ---- merge the 4 warps of the CTA in shared memory --------------------
 #pragma unroll
@@ -345,9 +355,21 @@ static cudaError_t launch_mode(const DecodeArgs& a, cudaStream_t st) {
       decode_attn_kernel<MODE, false, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (attr_hi != cudaSuccess) return attr_hi;
   if (attr_lo != cudaSuccess) return attr_lo;
-  if (a.G > 8) decode_attn_kernel<MODE, true, STG><<<grid, kThreads, smem, st>>>(a);
-  else decode_attn_kernel<MODE, false, STG><<<grid, kThreads, smem, st>>>(a);
-  return cudaGetLastError();
+  // programmatic stream serialization (see the kernel's PDL note);
+  // KSCD_NO_PDL=1 (dev knob) launches with plain stream order
+  static const bool pdl = !getenv("KSCD_NO_PDL");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  if (a.G > 8) return cudaLaunchKernelEx(&cfg, decode_attn_kernel<MODE, true, STG>, a);
+  return cudaLaunchKernelEx(&cfg, decode_attn_kernel<MODE, false, STG>, a);
 }
 
 cudaError_t launch_decode_attn(int mode, const DecodeArgs& a, cudaStream_t st) {

@@ -133,13 +133,14 @@ class KascadeDecoder:
         layer = self._dense_layer if dense else self._layer
         # The copies are pipelined against the layer loop on two side streams
         # (graph branches): the new K/V rows and layer 0's queries arrive
-        # first, the other layers' queries stream in behind layer 0, and each
-        # layer's output leaves as soon as that layer is done -- only the
-        # first H2D and the last layer's D2H stay on the critical path.
+        # first, the other layers' queries stream in (one copy) behind layer
+        # 0, and the outputs leave in chunks of 8 layers as they complete.
+        # Few cross-stream edges keep consecutive reuse-layer kernels chained
+        # by programmatic dependent launch (decode.cu).
         h2d, d2h = torch.cuda.Stream(device=self.device), torch.cuda.Stream(device=self.device)
-        ev_first = torch.cuda.Event()
-        ev_q = [torch.cuda.Event() for _ in range(self.L)]
-        ev_done = [torch.cuda.Event() for _ in range(self.L)]
+        ev_first, ev_rest = torch.cuda.Event(), torch.cuda.Event()
+        chunk = 8
+        ev_done = [torch.cuda.Event() for _ in range(0, self.L, chunk)]
 
         def body():
             main = torch.cuda.current_stream()
@@ -149,19 +150,21 @@ class KascadeDecoder:
                 kv_dev.copy_(kv_host, non_blocking=True)
                 q[0].copy_(q_host[0], non_blocking=True)
                 ev_first.record(h2d)
-                for l in range(1, self.L):
-                    q[l].copy_(q_host[l], non_blocking=True)
-                    ev_q[l].record(h2d)
+                if self.L > 1:
+                    q[1:].copy_(q_host[1:], non_blocking=True)
+                ev_rest.record(h2d)
             main.wait_event(ev_first)
             ops.append_kv(kv_dev, seq_len - 1, tables)
             for l in range(self.L):
-                if l > 0:
-                    main.wait_event(ev_q[l])
+                if l == 1:
+                    main.wait_event(ev_rest)
                 layer(l, q, k_caches, v_caches, seq_len)
-                ev_done[l].record(main)
-                with torch.cuda.stream(d2h):
-                    d2h.wait_event(ev_done[l])
-                    out_host[l].copy_(self.out[l], non_blocking=True)
+                if (l + 1) % chunk == 0 or l == self.L - 1:
+                    c = l // chunk
+                    ev_done[c].record(main)
+                    with torch.cuda.stream(d2h):
+                        d2h.wait_event(ev_done[c])
+                        out_host[c * chunk:l + 1].copy_(self.out[c * chunk:l + 1], non_blocking=True)
             main.wait_stream(h2d)
             main.wait_stream(d2h)
 
