@@ -90,6 +90,12 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
   const int* sel = nullptr;
   int nb;
   if (MODE == PMODE_SPARSE) {
+    // Programmatic dependent launch between consecutive reuse layers: the
+    // next layer's CTAs may take SMs as ours retire.  Inputs are complete at
+    // launch (per-layer Q/K/V; index lists from a select launch that never
+    // triggers early) and each layer writes its own output, so only the
+    // optional LSE side output (shared) waits for the previous grid.
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     const int src = a.head_map ? __ldg(a.head_map + g) : g;
     sel = a.idx + (int64_t)src * a.idx_sg + (int64_t)ti * a.idx_st;
     count = min(__ldg(a.cnt + (int64_t)src * a.cnt_sg + ti), a.k_cap);
@@ -466,6 +472,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
           }
         }
       }
+      if (MODE == PMODE_SPARSE && a.lse) asm volatile("griddepcontrol.wait;\n" ::: "memory");
       if (live && a.lse) a.lse[(int64_t)h * a.N + row] = l > 0.f ? (m_used + __log2f(l)) * kLn2 : -INFINITY;
     }
   }
@@ -524,8 +531,22 @@ static cudaError_t launch_prefill_mode(const PrefillArgs& a, cudaStream_t st) {
   if (attr != cudaSuccess) return attr;
   const int tiles = (a.N + pf::kTileM - 1) / pf::kTileM;
   dim3 grid(tiles, a.Hq / a.slots);
-  prefill_attn_kernel<MODE><<<grid, pf::kThreads, pf::kSmemBytes, st>>>(tm, a);
-  return cudaGetLastError();
+  if (MODE != PMODE_SPARSE) {
+    prefill_attn_kernel<MODE><<<grid, pf::kThreads, pf::kSmemBytes, st>>>(tm, a);
+    return cudaGetLastError();
+  }
+  static const bool pdl = !getenv("KSCD_NO_PDL");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(pf::kThreads);
+  cfg.dynamicSmemBytes = pf::kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, prefill_attn_kernel<MODE>, tm, a);
 }
 
 bool prefill_pair_supported(int mode, const PrefillArgs& a);
