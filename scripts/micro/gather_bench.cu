@@ -24,23 +24,24 @@ KSCD_DEV void gather4(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, 
       : "memory");
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(128, 1) gather_kernel(const __grid_constant__ CUtensorMap tm, const __nv_bfloat16* k,
+template <int MODE_, int NPROD = 96>
+__global__ void __launch_bounds__(NPROD + 32, 1) gather_kernel_t(const __grid_constant__ CUtensorMap tm, const __nv_bfloat16* k,
                                                         const int* pos_all, int nblocks, int npos, float* sink) {
+  constexpr int MODE = MODE_;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * 2 * kTile + 65536);   // full[2], empty[2]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&bars[s], MODE == 0 ? 96 : 1);
+      mbar_init(&bars[s], (MODE == 0 || MODE == 4) ? NPROD : 1);
       mbar_init(&bars[2 + s], 1);
     }
     fence_barrier_init();
   }
   __syncthreads();
   const int* pos0 = pos_all + (((size_t)blockIdx.x * 7919 % (npos - nblocks * kRows)) & ~(size_t)3);
-  if (warp == 3) {
+  if (warp == NPROD / 32) {
     float acc = 0.f;
     for (int j = 0; j < nblocks; ++j) {
       const int st = j & 1;
@@ -57,12 +58,26 @@ __global__ void __launch_bounds__(128, 1) gather_kernel(const __grid_constant__ 
     if (j >= 2) mbar_wait(&bars[2 + st], ((j >> 1) - 1) & 1);
     const int* pos = pos0 + j * kRows;
     uint8_t* kd = smem + st * 2 * kTile;      // K then V (same rows: stands in for both)
-    if (MODE == 0) {
+    if (MODE == 4) {
       const uint32_t dst0 = smem_u32(kd);
-      for (int rep = 0; rep < 2; ++rep) {
-        for (int c = threadIdx.x; c < kRows * 16; c += 96) {
+      for (int rep = 0; rep < 2; ++rep)
+        for (int c = threadIdx.x; c < kRows * 16; c += NPROD) {
           const int r = c >> 4, ch = c & 15;
           const int p = __ldg(pos + r);
+          const uint32_t off = rep * kTile + (ch >> 3) * kHalf + r * 128 + (((ch & 7) ^ (r & 7)) << 4);
+          cp_async16_zfill(dst0 + off, k + (int64_t)p * 128 + ch * 8, true);
+        }
+      cp_async_mbar_arrive(&bars[st]);     // arrives when this thread's copies land; no blocking wait
+    } else if (MODE == 0) {
+      const uint32_t dst0 = smem_u32(kd);
+      // positions staged in shared memory first (as the prefill producer does)
+      int* spos = reinterpret_cast<int*>(smem + 2 * 2 * kTile + 65536 + 64);
+      for (int r = threadIdx.x; r < kRows; r += NPROD) spos[r] = __ldg(pos + r);
+      asm volatile("bar.sync 1, %0;\n" ::"r"(NPROD));
+      for (int rep = 0; rep < 2; ++rep) {
+        for (int c = threadIdx.x; c < kRows * 16; c += NPROD) {
+          const int r = c >> 4, ch = c & 15;
+          const int p = spos[r];
           const uint32_t off = rep * kTile + (ch >> 3) * kHalf + r * 128 + (((ch & 7) ^ (r & 7)) << 4);
           cp_async16_zfill(dst0 + off, k + (int64_t)p * 128 + ch * 8, true);
         }
@@ -71,7 +86,7 @@ __global__ void __launch_bounds__(128, 1) gather_kernel(const __grid_constant__ 
       cp_async_wait<0>();
       fence_proxy_async_smem();
       mbar_arrive(&bars[st]);
-    } else if (warp == 0) {
+    } else if (warp == 0 && MODE == 1) {
       if (lane == 0) mbar_expect_tx(&bars[st], 2 * kTile);
       __syncwarp();
       // 2 (K,V) x 2 halves x 32 row groups = 128 gather4 ops; 4 per lane
@@ -121,17 +136,23 @@ int main(int argc, char** argv) {
                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (rc != CUDA_SUCCESS) { printf("encode failed %d\n", (int)rc); return 1; }
-  const int smem = 2 * 2 * kTile + 64 + 1024 + 65536;
-  cudaFuncSetAttribute(gather_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(gather_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int smem = 2 * 2 * kTile + 64 + 1024 + 65536 + 1024;
+  cudaFuncSetAttribute(gather_kernel_t<0, 96>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(gather_kernel_t<1, 96>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(gather_kernel_t<0, 192>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(gather_kernel_t<0, 288>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(gather_kernel_t<4, 96>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  for (int mode = 0; mode < (argc > 4 ? atoi(argv[4]) : 2); ++mode) {
+  for (int mode = (argc > 5 ? atoi(argv[5]) : 0); mode < (argc > 4 ? atoi(argv[4]) : 2); ++mode) {
     for (int it = 0; it < 3; ++it) {
       cudaEventRecord(a);
-      if (mode == 0) gather_kernel<0><<<grid, 128, smem>>>(tm, k, pos, nblocks, npos, sink);
-      else gather_kernel<1><<<grid, 128, smem>>>(tm, k, pos, nblocks, npos, sink);
+      if (mode == 0) gather_kernel_t<0, 96><<<grid, 128, smem>>>(tm, k, pos, nblocks, npos, sink);
+      else if (mode == 1) gather_kernel_t<1, 96><<<grid, 128, smem>>>(tm, k, pos, nblocks, npos, sink);
+      else if (mode == 2) gather_kernel_t<0, 192><<<grid, 224, smem>>>(tm, k, pos, nblocks, npos, sink);
+      else if (mode == 3) gather_kernel_t<0, 288><<<grid, 320, smem>>>(tm, k, pos, nblocks, npos, sink);
+      else gather_kernel_t<4, 96><<<grid, 128, smem>>>(tm, k, pos, nblocks, npos, sink);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
