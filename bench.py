@@ -496,24 +496,105 @@ def bench_configs(args, dev, world, dist):
                 "note": "KV of 32 sequences x 36 layers is 618 GB: layers cycle over the distinct buffers that "
                         "fit (each layer's KV >> L2)"})
 
-    # configs[4]: Llama-3.1-70B, one kv head of 8-way kv-head sharding, 128K
-    from paper_2512_16391_b200.host_types import read_plan
+    # configs[4]: Llama-3.1-70B at 128K, kv-head sharded
+    from paper_2512_16391_b200.host_types import KBudgetPolicy, read_plan
     p70 = read_plan(os.path.join(PLANS, "llama70b.json"))
+    p70.k_policy = KBudgetPolicy(args.fraction, args.k_min)
+    try:
+        if world > 1 and 8 % world == 0:
+            entry = sharded_70b(dev, world, dist, p70, 131072, 8, steps, warm, 16000 + rank_seed)
+        else:
+            entry = shard_proxy_70b(dev, world, dist, p70, args, steps, warm, rank_seed)
+    except Exception as e:  # an extra config must never cost the headline line
+        entry = {"config": 4, "error": f"{type(e).__name__}: {e}"}
+    out.append(entry)
+    return out
+
+
+def shard_proxy_70b(dev, world, dist, p70, args, steps, warm, rank_seed):
+    """One GPU: the work ONE rank of the 8-way kv-head-sharded 70B job does
+    (1 KV + 8 Q heads, 80 layers), minus the index-list all-gathers."""
     shard = shard_plan(p70, args.fraction, args.k_min)
     L7, Hq7 = 80, 8
     m_pa, m_pd, nd_p = _prefill_config(dev, world, dist, shard, L7, Hq7, 1, 131072, 1, 1, 14000 + rank_seed)
     m_da, m_dd, nd_d = _decode_config(dev, world, dist, shard, L7, 8, Hq7, 1, 131072, steps, warm, 15000 + rank_seed)
-    out.append({"config": 4, "workload": "llama70b-128k-kv-head-shard (1 KV + 8 Q heads per GPU, 80 layers, k0.1)",
-                "plan": "plans/llama70b.json (reference build_plan, budget 12)", "anchors": p70.anchors,
-                "prefill_kascade_ms_per_layer": round(m_pa / L7, 3), "prefill_dense_ms_per_layer": round(m_pd / L7, 3),
-                "prefill_speedup_vs_dense": round(m_pd / m_pa, 3),
-                "decode_kascade_us_per_token": round(m_da * 1e3 / 8, 2),
-                "decode_dense_us_per_token": round(m_dd * 1e3 / 8, 2),
-                "decode_speedup_vs_dense": round(m_dd / m_da, 3), "decode_batch": 8,
-                "layers_distinct": {"prefill": nd_p, "decode": nd_d},
-                "note": "per-GPU work of the 8-way job; the index-list all-gather after each of the 12 anchor "
-                        "layers (<= 54 MB per GPU at 128K prefill) is not in this single-GPU timing"})
-    return out
+    return {"config": 4, "workload": "llama70b-128k-kv-head-shard (1 KV + 8 Q heads per GPU, 80 layers, k0.1)",
+            "plan": "plans/llama70b.json (reference build_plan, budget 12)", "anchors": p70.anchors,
+            "prefill_kascade_ms_per_layer": round(m_pa / L7, 3), "prefill_dense_ms_per_layer": round(m_pd / L7, 3),
+            "prefill_speedup_vs_dense": round(m_pd / m_pa, 3),
+            "decode_kascade_us_per_token": round(m_da * 1e3 / 8, 2),
+            "decode_dense_us_per_token": round(m_dd * 1e3 / 8, 2),
+            "decode_speedup_vs_dense": round(m_dd / m_da, 3), "decode_batch": 8,
+            "layers_distinct": {"prefill": nd_p, "decode": nd_d},
+            "note": "per-GPU work of the 8-way job; the index-list all-gather after each of the 12 anchor "
+                    "layers (<= 54 MB per GPU at 128K prefill) is not in this single-GPU timing"}
+
+
+def sharded_70b(dev, world, dist, plan, N, B, steps, warm, seed, L=80, Hq=64, Hkv=8, n_distinct_max=None):
+    """Several GPUs: the 70B layer stack kv-head sharded over the ranks
+    (sharding.ShardedKascadePrefill / ShardedKascadeDecoder) with the REAL
+    global head maps, so every anchor layer all-gathers its index lists over
+    the process group (NCCL on the box) and reuse heads read lists owned by
+    other ranks.  Strong scaling: the whole model's work is split; time is the
+    max over ranks.  The dense baseline runs the same local heads."""
+    import torch
+    from paper_2512_16391_b200 import sharding
+    g0, g1 = sharding.kv_head_shard(Hkv)
+    G = Hq // Hkv
+    Hl, Hql = g1 - g0, (g1 - g0) * G
+    gen = torch.Generator(device=dev)
+    # prefill
+    per_layer = (Hql + 2 * Hl) * N * 128 * 2
+    free, _ = torch.cuda.mem_get_info(dev)
+    nd = int(max(2, min(L, (free - 24 * 2**30) // per_layer)))
+    if n_distinct_max:
+        nd = min(nd, n_distinct_max)
+    pf = sharding.ShardedKascadePrefill(plan, L, Hq, Hkv, N)
+    qs, ks, vs = [], [], []
+    for i in range(nd):
+        gen.manual_seed(seed + i)
+        qs.append(torch.randn(Hql, N, 128, device=dev, generator=gen, dtype=torch.bfloat16))
+        ks.append(torch.randn(Hl, N, 128, device=dev, generator=gen, dtype=torch.bfloat16))
+        vs.append(torch.randn(Hl, N, 128, device=dev, generator=gen, dtype=torch.bfloat16))
+    Q = [qs[l % nd] for l in range(L)]
+    K = [ks[l % nd] for l in range(L)]
+    V = [vs[l % nd] for l in range(L)]
+    m_pa = _timed(lambda: pf.forward(Q, K, V), 1, 1, world, dist, dev)
+    m_pd = _timed(lambda: pf.local.dense_forward(Q, K, V), 1, 1, world, dist, dev)
+    del pf, qs, ks, vs, Q, K, V
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    # decode: all B sequences, the rank's kv heads
+    per_layer = 2 * B * Hl * N * 128 * 2
+    free, _ = torch.cuda.mem_get_info(dev)
+    ndd = int(max(2, min(L, (free - 24 * 2**30) // per_layer)))
+    if n_distinct_max:
+        ndd = min(ndd, n_distinct_max)
+    dec = sharding.ShardedKascadeDecoder(plan, L, B, Hq, Hkv, N)
+    Kc, Vc = [], []
+    for i in range(ndd):
+        gen.manual_seed(seed + 500 + i)
+        Kc.append(torch.randn(B, Hl, N, 128, device=dev, dtype=torch.bfloat16, generator=gen))
+        Vc.append(torch.randn(B, Hl, N, 128, device=dev, dtype=torch.bfloat16, generator=gen))
+    Ks = [Kc[l % ndd] for l in range(L)]
+    Vs = [Vc[l % ndd] for l in range(L)]
+    q = (torch.randn(L, B, Hql, 128, device=dev, generator=gen) * 2.0).to(torch.bfloat16)
+    m_da = _timed(lambda: dec.step(q, Ks, Vs, N), steps, warm, world, dist, dev)
+    m_dd = _timed(lambda: dec.local.dense_step(q, Ks, Vs, N), steps, warm, world, dist, dev)
+    del dec, Kc, Vc, Ks, Vs, q
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return {"config": 4, "workload": f"llama70b-128k kv-head sharded x{world} ({Hl} KV + {Hql} Q heads per GPU, "
+                                     f"{L} layers, k{plan.k_policy.fraction:g})",
+            "plan": "plans/llama70b.json (reference build_plan, budget 12)", "anchors": plan.anchors,
+            "sharding": f"kv-head x{world}, index-list all-gather after every anchor layer",
+            "scaling": "strong",
+            "prefill_kascade_ms_per_layer": round(m_pa / L, 3), "prefill_dense_ms_per_layer": round(m_pd / L, 3),
+            "prefill_speedup_vs_dense": round(m_pd / m_pa, 3),
+            "decode_kascade_us_per_token": round(m_da * 1e3 / B, 2),
+            "decode_dense_us_per_token": round(m_dd * 1e3 / B, 2),
+            "decode_speedup_vs_dense": round(m_dd / m_da, 3), "decode_batch": B,
+            "layers_distinct": {"prefill": nd, "decode": ndd}}
 
 
 # ------------------------------------------------------------------ GPU arm

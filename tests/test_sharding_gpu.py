@@ -87,3 +87,47 @@ def test_kv_head_sharded_executors_match_unsharded(cuda_ok):
         msgs.append(errq.get())
     assert not msgs, msgs
     assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+
+
+def _bench_worker(rank, world, port, errq):
+    """bench.py's multi-GPU configs[4] path (sharded_70b) at toy sizes, two
+    gloo ranks sharing cuda:0: it must run end to end and time on every rank."""
+    import sys
+    import torch.distributed as dist
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        sys.path.insert(0, repo)
+        import bench
+        from paper_2512_16391_b200.host_types import KBudgetPolicy, read_plan
+        plan = read_plan(os.path.join(repo, "plans", "llama70b.json"))
+        plan.k_policy = KBudgetPolicy(0.1, 64)
+        out = bench.sharded_70b(torch.device("cuda", 0), world, dist, plan, 1024, 2, 2, 1, 7 + 97 * rank,
+                                n_distinct_max=2)
+        assert out["config"] == 4 and out["prefill_speedup_vs_dense"] > 0 and out["decode_speedup_vs_dense"] > 0, out
+        assert "x2" in out["sharding"]
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # reported to the parent
+        errq.put(f"rank {rank}: {type(e).__name__}: {e}")
+        raise
+
+
+def test_bench_sharded_70b_path_runs(cuda_ok):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    errq = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, 2, port, errq)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(600)
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert not errs, errs
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
