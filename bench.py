@@ -468,33 +468,44 @@ def bench_configs(args, dev, world, dist):
     out = []
     steps, warm = max(3, args.steps // 2), max(3, args.warmup)
 
-    # configs[1]: Llama-3.1-8B decode, 32K, batch 8, Top-k 2.5 %
-    L, Hq, Hkv = CFG["layers"], CFG["Hq"], CFG["Hkv"]
-    plan = make_plan(L, Hkv, LLAMA_ANCHORS, 0.025, args.k_min)
-    m_a, m_d, nd = _decode_config(dev, world, dist, plan, L, 8, Hq, Hkv, 32768, steps, warm, 11000 + rank_seed)
-    out.append({"config": 1, "workload": "llama8b-decode-32k-b8-k2.5%", "plan": "plans/llama8b.json",
+    def config1():
+        # configs[1]: Llama-3.1-8B decode, 32K, batch 8, Top-k 2.5 %
+        plan = make_plan(L, Hkv, LLAMA_ANCHORS, 0.025, args.k_min)
+        m_a, m_d, nd = _decode_config(dev, world, dist, plan, L, 8, Hq, Hkv, 32768, steps, warm, 11000 + rank_seed)
+        return {"config": 1, "workload": "llama8b-decode-32k-b8-k2.5%", "plan": "plans/llama8b.json",
                 "kascade_us_per_token": round(m_a * 1e3 / 8, 2), "dense_us_per_token": round(m_d * 1e3 / 8, 2),
-                "speedup_vs_dense": round(m_d / m_a, 3), "batch_per_gpu": 8, "kv_layers_distinct": nd})
+                "speedup_vs_dense": round(m_d / m_a, 3), "batch_per_gpu": 8, "kv_layers_distinct": nd}
 
-    # configs[2]: Llama-3.1-8B prefill, 64K, tile-level Top-k 10 % + head remap
-    plan = make_plan(L, Hkv, LLAMA_ANCHORS, args.fraction, args.k_min)
-    m_a, m_d, nd = _prefill_config(dev, world, dist, plan, L, Hq, Hkv, 65536, 1, 1, 12000 + rank_seed)
-    out.append({"config": 2, "workload": "llama8b-prefill-64k-b1-k0.1", "plan": "plans/llama8b.json",
+    def config2():
+        # configs[2]: Llama-3.1-8B prefill, 64K, tile-level Top-k 10 % + head remap
+        plan = make_plan(L, Hkv, LLAMA_ANCHORS, args.fraction, args.k_min)
+        m_a, m_d, nd = _prefill_config(dev, world, dist, plan, L, Hq, Hkv, 65536, 1, 1, 12000 + rank_seed)
+        return {"config": 2, "workload": "llama8b-prefill-64k-b1-k0.1", "plan": "plans/llama8b.json",
                 "kascade_ms_per_layer": round(m_a / L, 3), "dense_ms_per_layer": round(m_d / L, 3),
                 "kascade_ms": round(m_a, 2), "dense_ms": round(m_d, 2), "speedup_vs_dense": round(m_d / m_a, 3),
-                "layers_distinct": nd})
+                "layers_distinct": nd}
 
-    # configs[3]: Qwen3-8B-shaped decode, 128K, batch 32 split over the ranks
-    Lq = 36
-    B3 = max(1, 32 // world)
-    plan = make_plan(Lq, Hkv, [0, 2, 7, 14, 23], args.fraction, args.k_min, name="qwen3_8b")
-    m_a, m_d, nd = _decode_config(dev, world, dist, plan, Lq, B3, Hq, Hkv, 131072, steps, warm, 13000 + rank_seed)
-    out.append({"config": 3, "workload": f"qwen3-8b-decode-128k-b32-k0.1 (batch {B3} per GPU x {world})",
+    def config3():
+        # configs[3]: Qwen3-8B-shaped decode, 128K, batch 32 split over the ranks
+        Lq = 36
+        B3 = max(1, 32 // world)
+        plan = make_plan(Lq, Hkv, [0, 2, 7, 14, 23], args.fraction, args.k_min, name="qwen3_8b")
+        m_a, m_d, nd = _decode_config(dev, world, dist, plan, Lq, B3, Hq, Hkv, 131072, steps, warm,
+                                      13000 + rank_seed)
+        return {"config": 3, "workload": f"qwen3-8b-decode-128k-b32-k0.1 (batch {B3} per GPU x {world})",
                 "plan": "plans/qwen3_8b.json", "kascade_us_per_token": round(m_a * 1e3 / (B3 * world), 2),
                 "dense_us_per_token": round(m_d * 1e3 / (B3 * world), 2), "speedup_vs_dense": round(m_d / m_a, 3),
                 "batch_per_gpu": B3, "kv_layers_distinct": nd,
                 "note": "KV of 32 sequences x 36 layers is 618 GB: layers cycle over the distinct buffers that "
-                        "fit (each layer's KV >> L2)"})
+                        "fit (each layer's KV >> L2)"}
+
+    L, Hq, Hkv = CFG["layers"], CFG["Hq"], CFG["Hkv"]
+    for i, fn in ((1, config1), (2, config2), (3, config3)):
+        try:
+            out.append(fn())
+        except Exception as e:  # an extra config must never cost the headline line
+            out.append({"config": i, "error": f"{type(e).__name__}: {e}"})
+            torch_empty_cache()
 
     # configs[4]: Llama-3.1-70B at 128K, kv-head sharded
     from paper_2512_16391_b200.host_types import KBudgetPolicy, read_plan
@@ -507,8 +518,15 @@ def bench_configs(args, dev, world, dist):
             entry = shard_proxy_70b(dev, world, dist, p70, args, steps, warm, rank_seed)
     except Exception as e:  # an extra config must never cost the headline line
         entry = {"config": 4, "error": f"{type(e).__name__}: {e}"}
+        torch_empty_cache()
     out.append(entry)
     return out
+
+
+def torch_empty_cache():
+    import torch
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
 
 
 def shard_proxy_70b(dev, world, dist, p70, args, steps, warm, rank_seed):
