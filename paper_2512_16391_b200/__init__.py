@@ -22,7 +22,22 @@ def __getattr__(name):
         import importlib
         return importlib.import_module(f".{name}", __name__)
     if name in ("dense_attention", "topk_attention", "oracle_topk_indices", "run_kascade", "run_dense",
-                "compare", "softmax_row"):
+                "compare", "softmax_row", "AttentionDistribution", "pool_presoftmax", "pool_postsoftmax",
+                "layer_distribution", "mass_coverage", "sim_score", "pooled_all_heads_topk"):
         from . import compat
         return getattr(compat, name)
+    if name in ("compute_head_map", "compute_head_maps", "head_similarity", "similarity_matrix", "SimilarityMatrix",
+                "LayerImportance", "layer_importance", "apply_importance", "select_anchors", "build_plan"):
+        from . import calibration
+        return getattr(calibration, name)
+    if name in ("BenchRow", "CostParams", "CostReport", "get_preset", "predict_ratios", "predict_report",
+                "preset_names", "weighted_pipeline_time", "report_from_preset", "fit_ratios"):
+        from . import costmodel
+        return getattr(costmodel, name)
+    if name in ("SynthConfig", "generate_synthetic"):
+        from . import synth
+        return getattr(synth, name)
+    if name in ("read_trace", "write_trace"):
+        from . import kscd_io
+        return getattr(kscd_io, name)
     raise AttributeError(name)

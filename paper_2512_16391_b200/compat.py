@@ -369,3 +369,105 @@ def compare(outputs_a, outputs_b) -> RunReport:
     errs = np.array(rel)
     return RunReport(per_layer=reports,
                      overall={"mean_output_rel_err_l2": float(errs.mean()), "max_output_rel_err_l2": float(errs.max())})
+
+
+# ------------------------------------------------ small reference utilities
+# The reference's pooling / coverage helpers (tiles.py:92-114, metrics.py:
+# 80-131, heads.py:155-171, attention.py:21-37) with the same signatures,
+# evaluated on the device (fp64 accumulation, fp32 results as in numpy).
+
+class AttentionDistribution:
+    """attention.py:21-37: post-softmax weights over the attendable keys of one row."""
+
+    def __init__(self, weights, key_positions):
+        self.weights = np.asarray(weights)
+        self.key_positions = np.asarray(key_positions)
+
+    def validate(self):
+        w = np.asarray(self.weights, dtype=np.float64)
+        pos = np.asarray(self.key_positions)
+        if w.shape != pos.shape or w.ndim != 1:
+            raise InvalidArgumentError("weights/key_positions must be matching vectors")
+        if abs(float(w.sum()) - 1.0) > 1e-6:
+            raise InvalidArgumentError("weights must sum to 1 within 1e-6")
+        if (w < 0).any():
+            raise InvalidArgumentError("weights must be non-negative")
+        if pos.size > 1 and not (np.diff(pos) > 0).all():
+            raise InvalidArgumentError("key_positions must be strictly increasing")
+
+
+def _dev64(a) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(_dev())
+
+
+def pool_presoftmax(q_tile) -> np.ndarray:
+    """tiles.py:92-97: mean of the tile's query vectors, fp64 -> fp32."""
+    q = np.asarray(q_tile)
+    if q.ndim != 2 or q.shape[0] < 1:
+        raise InvalidArgumentError("q_tile must be a non-empty [T][d] array")
+    return _dev64(q).mean(dim=0).to(torch.float32).cpu().numpy()
+
+
+def pool_postsoftmax(rows) -> np.ndarray:
+    """tiles.py:100-114: mean of per-query distributions, shorter rows
+    zero-extended to the longest support."""
+    rows = [np.asarray(r) for r in rows]
+    if not rows:
+        raise InvalidArgumentError("cannot pool an empty tile")
+    width = max(r.shape[0] for r in rows)
+    acc = torch.zeros(width, dtype=torch.float64, device=_dev())
+    for r in rows:
+        acc[: r.shape[0]] += _dev64(r)
+    return (acc / len(rows)).to(torch.float32).cpu().numpy()
+
+
+def layer_distribution(P) -> np.ndarray:
+    """metrics.py:97-102: mean of the per-head distributions [Hq][N][N] -> [N][N]."""
+    P = np.asarray(P)
+    if P.ndim != 3:
+        raise InvalidArgumentError("P must be [Hq][N][N]")
+    return _dev64(P).mean(dim=0).to(torch.float32).cpu().numpy()
+
+
+def mass_coverage(P, k: int, per_row: bool = False) -> np.ndarray:
+    """metrics.py:80-94: attention mass captured by each row's top-k keys."""
+    if k < 1:
+        raise InvalidArgumentError(f"k must be >= 1, got {k}")
+    P = np.asarray(P)
+    if P.ndim == 2:
+        P = P[None]
+    take = min(k, P.shape[-1])
+    t = torch.from_numpy(np.ascontiguousarray(P)).to(_dev())
+    top = torch.topk(t, take, dim=-1, sorted=False).values.to(torch.float64)
+    cov = top.sum(dim=-1)
+    out = cov.to(torch.float32) if per_row else cov.mean(dim=-1).to(torch.float32)
+    return out.cpu().numpy()
+
+
+def sim_score(p_b, I_a, I_b) -> float:
+    """metrics.py:111-131: mass of p_b on I_a relative to its own Top-k set I_b."""
+    from .exceptions import UndefinedScoreError
+    idx_a = np.asarray(I_a.indices if hasattr(I_a, "indices") else I_a, dtype=np.int64)
+    idx_b = np.asarray(I_b.indices if hasattr(I_b, "indices") else I_b, dtype=np.int64)
+    if idx_a.size != idx_b.size or idx_a.size == 0:
+        raise InvalidArgumentError(
+            f"index sets must be non-empty and equal-sized, got {idx_a.size} and {idx_b.size}")
+    p = np.asarray(p_b, dtype=np.float64)
+    if idx_a.max() >= p.size or idx_b.max() >= p.size:
+        raise InvalidArgumentError("index set outside the distribution's support")
+    pd = _dev64(p)
+    num = float(pd[torch.from_numpy(idx_a).to(pd.device)].sum())
+    den = float(pd[torch.from_numpy(idx_b).to(pd.device)].sum())
+    if den == 0.0:
+        raise UndefinedScoreError("distribution carries no mass on its own Top-k set")
+    return float(np.float32(num / den))
+
+
+def pooled_all_heads_topk(group_dists, k: int, tile_id: int = 0) -> TopKIndexSet:
+    """heads.py:155-171: shared Top-k set of the mean of per-kv-head pooled
+    distributions (kv_head recorded as -1), via the exact Top-k kernel."""
+    g = np.asarray(group_dists)
+    if g.ndim == 1:
+        g = g[None]
+    pooled = _dev64(g).mean(dim=0).cpu().numpy()
+    return oracle_topk_indices(pooled, k, kv_head=-1, tile_id=tile_id)
