@@ -1,8 +1,8 @@
-"""``python -m paper_2512_16391_b200 run|plan|cost``: the reference CLI's
-``run`` subcommand (cli.py:80-89,216-233) on the B200 engine, its ``plan``
-subcommand (cli.py:66-78,195-213) on the GPU calibration (calibration.py),
-and its ``cost`` subcommand (cli.py:90-105,236-300) over the B200 presets
-(costmodel.py).
+"""``python -m paper_2512_16391_b200 gen|analyze|plan|run|cost|report``: the
+reference CLI (cli.py:33-112) on this package -- ``run`` on the B200 engine,
+``analyze`` / ``plan`` on the GPU calibration (calibration.py), ``cost`` over
+the B200 presets (costmodel.py), ``gen`` / ``report`` with the same trace,
+plan and report formats.  Exit codes as in the reference (cli.py:20-23).
 
     python -m paper_2512_16391_b200 run --trace t.kscd --plan p.json \\
         [--phase prefill|decode] [--mode remapped|all-heads-pooled] [--out report.json] [--fail-above X]
@@ -33,6 +33,32 @@ class _Parser(argparse.ArgumentParser):
 def build_parser():
     p = _Parser(prog="kascade-b200", description=__doc__)
     sub = p.add_subparsers(dest="command", required=True)
+    gen = sub.add_parser("gen", help="generate a synthetic trace file")
+    gen.add_argument("--layers", type=int, required=True)
+    gen.add_argument("--q-heads", type=int, required=True)
+    gen.add_argument("--kv-heads", type=int, required=True)
+    gen.add_argument("--dim", type=int, required=True)
+    gen.add_argument("--tokens", type=int, required=True)
+    gen.add_argument("--rho", type=float, default=1.0, help="cross-layer key correlation in [0, 1]")
+    gen.add_argument("--seed", type=int, default=0)
+    gen.add_argument("--temperature", type=float, default=4.0, help="query sharpness")
+    gen.add_argument("--query-correlation", type=float, default=0.85)
+    gen.add_argument("--layer0-temperature-scale", type=float, default=1.0)
+    gen.add_argument("--permute-heads", action="store_true",
+                     help="random kv-head permutation per layer (layer 0 stays identity)")
+    gen.add_argument("--xy", action="store_true", help="include attention-block input/output hidden states")
+    gen.add_argument("--prompt-id", default="")
+    gen.add_argument("--out", required=True)
+    analyze = sub.add_parser("analyze", help="coverage, similarity and importance reports (GPU)")
+    analyze.add_argument("--trace", nargs="+", required=True)
+    analyze.add_argument("--k", type=int, default=64)
+    analyze.add_argument("--token-agg", choices=["mean", "min"], default="mean")
+    analyze.add_argument("--mode", choices=["diagnostic", "planning"], default="diagnostic")
+    analyze.add_argument("--tile-size", type=int, default=128)
+    analyze.add_argument("--importance", action="store_true")
+    analyze.add_argument("--out-dir", default=".")
+    report = sub.add_parser("report", help="render a saved report file as text")
+    report.add_argument("file")
     run = sub.add_parser("run", help="execute the anchor/reuse pipeline on the GPU and report fidelity vs dense")
     run.add_argument("--trace", required=True)
     run.add_argument("--plan", required=True)
@@ -134,6 +160,81 @@ def cmd_cost(args) -> int:
     return EXIT_OK
 
 
+def cmd_gen(args) -> int:
+    """cli.py:117-148."""
+    import os
+    import numpy as np
+    from . import kscd_io
+    from .synth import SynthConfig, generate_synthetic
+    perms = None
+    if args.permute_heads:
+        rng = np.random.default_rng(args.seed ^ 0x9E3779B9)
+        perms = [list(range(args.kv_heads))] + [list(rng.permutation(args.kv_heads)) for _ in range(args.layers - 1)]
+    trace = generate_synthetic(SynthConfig(
+        num_layers=args.layers, num_query_heads=args.q_heads, num_kv_heads=args.kv_heads, head_dim=args.dim,
+        seq_len=args.tokens, seed=args.seed, layer_correlation=args.rho, head_permutations=perms,
+        heavy_tail_temperature=args.temperature, query_correlation=args.query_correlation,
+        layer0_temperature_scale=args.layer0_temperature_scale, include_xy=args.xy, prompt_id=args.prompt_id))
+    kscd_io.write_trace(args.out, trace)
+    size = os.path.getsize(args.out)
+    print(f"wrote {args.out}: layers={trace.num_layers} q_heads={trace.num_query_heads} "
+          f"kv_heads={trace.num_kv_heads} dim={trace.head_dim} tokens={trace.seq_len} "
+          f"xy={int(trace.has_xy())} bytes={size}")
+    return EXIT_OK
+
+
+def _csv_similarity(S) -> str:
+    lines = ["row,col,value"]
+    for a in range(S.num_layers):
+        for b in range(a, S.num_layers):
+            lines.append(f"{a},{b},{S.S[a, b]:.8g}")
+    return "\n".join(lines) + "\n"
+
+
+def cmd_analyze(args) -> int:
+    """cli.py:151-192 with P, coverage and the similarity matrix on the GPU."""
+    from pathlib import Path
+    import numpy as np
+    from . import calibration, compat, kscd_io
+    traces = [kscd_io.TraceFile(p) for p in args.trace]
+    out_dir = Path(args.out_dir)
+    out_dir.mkdir(parents=True, exist_ok=True)
+    lines = ["layer,head,coverage"]
+    for layer in range(traces[0].num_layers):
+        per = [compat.mass_coverage(calibration.layer_probs(t, layer).cpu().numpy(), args.k) for t in traces]
+        for head, cov in enumerate(np.atleast_1d(np.mean(per, axis=0))):
+            lines.append(f"{layer},{head},{cov:.8g}")
+    (out_dir / "coverage.csv").write_text("\n".join(lines) + "\n")
+    S = calibration.similarity_matrix(traces, k=args.k, token_agg=args.token_agg, mode=args.mode,
+                                      tile_size=args.tile_size)
+    (out_dir / "similarity.csv").write_text(_csv_similarity(S))
+    if args.importance:
+        if all(t.X is not None and t.Y is not None for t in traces):
+            imp = calibration.layer_importance(traces)
+        else:
+            print("warning: trace(s) lack attention input/output hidden states; using uniform importance weights",
+                  file=sys.stderr)
+            imp = calibration.LayerImportance(w=np.ones(traces[0].num_layers), source_prompt_count=len(traces))
+        (out_dir / "importance.csv").write_text(
+            "\n".join(["layer,weight"] + [f"{l},{w:.8g}" for l, w in enumerate(imp.w)]) + "\n")
+    print(f"analyzed {len(traces)} trace(s): k={args.k} mode={args.mode} token_agg={args.token_agg} "
+          f"undefined_scores={S.undefined_scores} -> {out_dir}")
+    return EXIT_OK
+
+
+def cmd_report(args) -> int:
+    """cli.py:323-330."""
+    import json
+    from . import kscd_io
+    with open(args.file, "r", encoding="utf-8") as f:
+        data = json.load(f)
+    if isinstance(data, dict) and data.get("kind") == "kascade-run-report":
+        print(kscd_io.format_report(kscd_io.read_report(args.file)), end="")
+    else:
+        print(json.dumps(data, indent=2, sort_keys=True))
+    return EXIT_OK
+
+
 def cmd_plan(args) -> int:
     """cli.py:195-213 with the similarity matrix and head maps on the GPU."""
     from . import calibration, kscd_io
@@ -179,7 +280,8 @@ def main(argv=None) -> int:
     except SystemExit as e:
         return int(e.code or 0)
     try:
-        return {"cost": cmd_cost, "plan": cmd_plan, "run": cmd_run}[args.command](args)
+        return {"gen": cmd_gen, "analyze": cmd_analyze, "cost": cmd_cost, "plan": cmd_plan, "run": cmd_run,
+                "report": cmd_report}[args.command](args)
     except (KascadeError, OSError) as e:
         sys.stderr.write(f"{build_parser().prog}: {e}\n")
         return EXIT_DATA

@@ -79,3 +79,44 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def analyze_golden():
+    """`kascade analyze` (cli.py:151-192) on the CLI golden trace, both
+    similarity modes, plus `gen` output bytes' hash with --permute-heads."""
+    import contextlib
+    import hashlib
+    import io
+    import json
+    import tempfile
+    from kascade import cli as ref_cli
+    from kascade import traceio as ref_io
+    c = json.load(open(os.path.join(HERE, "cli_cases.json")))
+    a = c["trace_args"]
+    Q, K, V = orc.synth_qkv(a["L"], a["Hq"], a["Hkv"], a["d"], a["N"], seed=a["seed"], rho=a["rho"], perms=a["perms"])
+    Q, K, V = (orc.bf16_round(x) for x in (Q, K, V))
+    tc = AttentionTrace(num_layers=a["L"], num_query_heads=a["Hq"], num_kv_heads=a["Hkv"], head_dim=a["d"],
+                        seq_len=a["N"], Q=Q, K=K, V=V, prompt_id=c["trace_prompt_id"])
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        tpath = os.path.join(td, "t.kscd")
+        ref_io.write_trace(tpath, tc)
+        for mode, extra in (("diagnostic", []), ("planning", ["--tile-size", "64", "--token-agg", "min"])):
+            od = os.path.join(td, mode)
+            argv = ["analyze", "--trace", tpath, "--k", "16", "--mode", mode, "--importance", "--out-dir", od] + extra
+            buf = io.StringIO()
+            with contextlib.redirect_stdout(buf), contextlib.redirect_stderr(io.StringIO()):
+                assert ref_cli.main(argv) == 0
+            out[mode] = {"argv": ["--k", "16", "--mode", mode, "--importance"] + extra,
+                         "stdout": buf.getvalue().split(" -> ")[0],
+                         "files": {f: open(os.path.join(od, f)).read() for f in sorted(os.listdir(od))}}
+        gp = os.path.join(td, "g.kscd")
+        with contextlib.redirect_stdout(io.StringIO()):
+            ref_cli.main(["gen", "--layers", "3", "--q-heads", "4", "--kv-heads", "2", "--dim", "8", "--tokens", "10",
+                          "--permute-heads", "--seed", "5", "--xy", "--out", gp])
+        out["gen_sha256"] = hashlib.sha256(open(gp, "rb").read()).hexdigest()
+    json.dump(out, open(os.path.join(HERE, "cli_analyze.json"), "w"), indent=1)
+
+
+if __name__ == "__main__" and os.environ.get("KSCD_ANALYZE_ONLY"):
+    analyze_golden()

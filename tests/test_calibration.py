@@ -73,3 +73,35 @@ def test_score_aggregation_rules():
     assert cal._aggregate_scores(num, den, "min")[0, 0] == 0.5
     with pytest.raises(InvalidArgumentError):
         cal.head_similarity_from_dists(None, None, None, token_agg="median")
+
+
+def test_gen_cli_matches_reference_bytes(tmp_path, capsys):
+    """`gen` (cli.py:117-148) writes the reference's exact bytes (X/Y and
+    per-layer kv-head permutations included)."""
+    import hashlib
+    import json
+    import os
+    from conftest import GOLDEN
+    from paper_2512_16391_b200 import cli
+    want = json.load(open(os.path.join(GOLDEN, "cli_analyze.json")))["gen_sha256"]
+    out = tmp_path / "g.kscd"
+    assert cli.main(["gen", "--layers", "3", "--q-heads", "4", "--kv-heads", "2", "--dim", "8", "--tokens", "10",
+                     "--permute-heads", "--seed", "5", "--xy", "--out", str(out)]) == 0
+    assert hashlib.sha256(out.read_bytes()).hexdigest() == want
+    assert capsys.readouterr().out.startswith(f"wrote {out}: layers=3 q_heads=4 kv_heads=2 dim=8 tokens=10 xy=1")
+
+
+def test_report_cli(tmp_path, capsys):
+    import json
+    import os
+    from conftest import GOLDEN
+    from paper_2512_16391_b200 import cli
+    case = json.load(open(os.path.join(GOLDEN, "cli_cases.json")))["cases"]["t128_prefill_remapped"]
+    p = tmp_path / "r.json"
+    p.write_text(json.dumps(case["report"]))
+    assert cli.main(["report", str(p)]) == 0
+    assert capsys.readouterr().out == case["stdout"]
+    q = tmp_path / "other.json"
+    q.write_text('{"b": 1, "a": [2]}')
+    assert cli.main(["report", str(q)]) == 0
+    assert json.loads(capsys.readouterr().out) == {"a": [2], "b": 1}

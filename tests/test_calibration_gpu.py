@@ -145,3 +145,27 @@ def test_plan_cli_matches_reference_cli(cuda_ok, tmp_path, capsys):
     assert abs(got.pop("objective_value") - want.pop("objective_value")) < 1e-4
     got.pop("source_digest", None), want.pop("source_digest", None)
     assert got == want
+
+
+@pytest.mark.parametrize("mode", ["diagnostic", "planning"])
+def test_analyze_cli_matches_reference_cli(cuda_ok, tmp_path, capsys, mode):
+    """`python -m paper_2512_16391_b200 analyze` vs the reference's `kascade
+    analyze` (cli.py:151-192) on the CLI golden trace: the same files, rows
+    and keys; coverage and similarity values within the P tolerance."""
+    from paper_2512_16391_b200 import cli
+    from test_kscd_io import cli_trace
+    path, _ = cli_trace(tmp_path)
+    ref = json.load(open(os.path.join(GOLDEN, "cli_analyze.json")))[mode]
+    od = tmp_path / "out"
+    assert cli.main(["analyze", "--trace", str(path), *ref["argv"], "--out-dir", str(od)]) == 0
+    assert capsys.readouterr().out.split(" -> ")[0] == ref["stdout"]
+    assert sorted(os.listdir(od)) == sorted(ref["files"])
+    for name, text in ref["files"].items():
+        got = (od / name).read_text().splitlines()
+        want = text.splitlines()
+        assert got[0] == want[0] and len(got) == len(want), name
+        for g, w in zip(got[1:], want[1:]):
+            gk, gv = g.rsplit(",", 1)
+            wk, wv = w.rsplit(",", 1)
+            assert gk == wk
+            assert abs(float(gv) - float(wv)) <= ATOL, (name, g, w)
