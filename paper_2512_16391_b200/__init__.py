@@ -27,7 +27,8 @@ def __getattr__(name):
         from . import compat
         return getattr(compat, name)
     if name in ("compute_head_map", "compute_head_maps", "head_similarity", "similarity_matrix", "SimilarityMatrix",
-                "LayerImportance", "layer_importance", "apply_importance", "select_anchors", "build_plan"):
+                "LayerImportance", "layer_importance", "apply_importance", "select_anchors", "build_plan",
+                "exhaustive_select", "objective"):
         from . import calibration
         return getattr(calibration, name)
     if name in ("BenchRow", "CostParams", "CostReport", "get_preset", "predict_ratios", "predict_report",

@@ -433,6 +433,30 @@ def select_anchors(S, M: int) -> AnchorPlanCore:
     return AnchorPlanCore(anchors, M, objective(mat, anchors), digest)
 
 
+EXHAUSTIVE_LIMIT = 10**6     # planner.py:128
+
+
+def exhaustive_select(S, M: int) -> AnchorPlanCore:
+    """planner.py:131-160: brute force over every anchor set in lexicographic
+    order, keeping the first maximum (select_anchors' tie-break)."""
+    import math
+    from itertools import combinations
+    mat = _matrix_of(S)
+    L = mat.shape[0]
+    if not (1 <= M <= L):
+        raise InvalidArgumentError(f"anchor budget {M} outside [1, {L}]")
+    n_sets = math.comb(L - 1, M - 1)
+    if n_sets > EXHAUSTIVE_LIMIT:
+        raise UnsupportedOperationError(f"{n_sets} candidate sets exceed the exhaustive bound {EXHAUSTIVE_LIMIT}")
+    best, best_value = None, -np.inf
+    for rest in combinations(range(1, L), M - 1):
+        anchors = [0, *rest]
+        value = objective(mat, anchors)
+        if value > best_value:
+            best, best_value = anchors, value
+    return AnchorPlanCore(best, M, best_value, S.digest() if isinstance(S, SimilarityMatrix) else "")
+
+
 def build_plan(traces, budget: int = DEFAULT_ANCHOR_BUDGET, k: int = PLANNING_K, token_agg: str = TOKEN_AGG_MIN,
                tile_size: int = DEFAULT_TILE_SIZE, pooling: str = POOL_POST, mode: str = MODE_REMAPPED,
                k_policy: Optional[KBudgetPolicy] = None, use_importance: bool = True,

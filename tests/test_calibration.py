@@ -105,3 +105,13 @@ def test_report_cli(tmp_path, capsys):
     q.write_text('{"b": 1, "a": [2]}')
     assert cli.main(["report", str(q)]) == 0
     assert json.loads(capsys.readouterr().out) == {"a": [2], "b": 1}
+
+
+@pytest.mark.parametrize("seed,L,M", [(5, 7, 3), (6, 9, 4), (7, 6, 6)])
+def test_exhaustive_select_agrees_with_dp(seed, L, M):
+    rng = np.random.default_rng(seed)
+    mat = np.triu(rng.random((L, L)).astype(np.float32))
+    ex, dp = cal.exhaustive_select(mat, M), cal.select_anchors(mat, M)
+    assert ex.anchors == dp.anchors and abs(ex.objective_value - dp.objective_value) < 1e-12
+    with pytest.raises(UnsupportedOperationError):
+        cal.exhaustive_select(np.zeros((40, 40)), 12)
