@@ -14,8 +14,12 @@
  *     synchronisation happen inside a call: all work is enqueued on `stream`
  *     (a cudaStream_t passed as void*, NULL = legacy default stream), so the
  *     calls are CUDA-graph capturable.
- *   - Dtypes: Q/K/V bf16, head_dim 128 (K/V rows are 256 bytes); outputs,
- *     scores and LSE fp32; index lists int32.
+ *   - Dtypes: Q/K/V bf16 rows of 128 elements (256 bytes); outputs, scores
+ *     and LSE fp32; index lists int32.  head_dim is the logical head size,
+ *     1..128: for head_dim < 128 the caller zero-pads Q and K past head_dim
+ *     (Q.K^T is then exact), the default softmax scale is 1/sqrt(head_dim),
+ *     and output columns >= head_dim are padding.  The performance path is
+ *     head_dim 128 (the reference's small-d test traces use the padding).
  *   - Index-list wire format (anchor -> reuse): int32 idx[rows][k_cap] sorted
  *     ascending and padded with INT32_MAX, plus int32 counts[rows] -- the
  *     reference's TopKIndexSet.indices (attention.py:40-67) per (kv head,
@@ -51,7 +55,7 @@ typedef struct kscd_decode_params {
   int32_t batch;          /* B */
   int32_t num_q_heads;    /* Hq; query head h reads kv head h / (Hq/Hkv), trace.py:38-43 */
   int32_t num_kv_heads;   /* Hkv */
-  int32_t head_dim;       /* must be 128 */
+  int32_t head_dim;       /* 1..128, see Conventions */
   int32_t seq_len;        /* n: keys 0..n-1 are visible (the step's own token included) */
   const void* q;          /* bf16 [B][Hq][128], contiguous */
   const void* k_cache;    /* bf16; row j of (b, g) at k_cache + b*kv_stride_batch + g*kv_stride_head + j*128 */
@@ -111,7 +115,7 @@ typedef struct kscd_topk_params {
 /* Prefill of one layer (batch 1, the paper's prefill setting).  Query tiles
  * are the reference's prefill tiles of 128 rows (tiles.py:137-144). */
 typedef struct kscd_prefill_params {
-  int32_t num_q_heads, num_kv_heads, head_dim, seq_len;   /* head_dim must be 128 */
+  int32_t num_q_heads, num_kv_heads, head_dim, seq_len;   /* head_dim 1..128 */
   int32_t causal;          /* 1: row r sees keys <= r (attention.py:123-127) */
   const void* q;           /* bf16 [Hq][N][128], rows contiguous, head stride q_stride_head */
   const void* k;           /* bf16 [Hkv][N][128], head stride kv_stride_head */

@@ -33,7 +33,7 @@ import numpy as np
 import torch
 
 from . import _lib, ops
-from .compat import _dev, _layer, _probs
+from .compat import _check_head_dim, _dev, _layer, _probs, _scale
 from .exceptions import InvalidArgumentError, UnsupportedOperationError
 from .host_types import (DECODE, MODE_ALL_HEADS_POOLED, MODE_IDENTITY, MODE_REMAPPED, POOL_POST, PREFILL,
                          AnchorPlan, AnchorPlanCore, HeadMap, KBudgetPolicy)
@@ -103,8 +103,8 @@ def _check_agg(token_agg: str) -> None:
 def layer_probs(trace, layer: int) -> torch.Tensor:
     """dense_attention's P (attention.py:106-144) on the device: [Hq][N][N]."""
     q, k, v = _layer(trace, layer)
-    _, lse = ops.dense_prefill(q, k, v)
-    return _probs(q, k, lse, True)
+    _, lse = ops.dense_prefill(q, k, v, scale=_scale(trace))
+    return _probs(q, k, lse, True, trace.head_dim)
 
 
 def pooled_tiles(P: torch.Tensor, num_kv_heads: int, starts: Sequence[int], ends: Sequence[int],
@@ -336,8 +336,7 @@ def similarity_matrix(traces, k: int = PLANNING_K, token_agg: str = TOKEN_AGG_ME
     _check_agg(token_agg)
     mats, undefined = [], 0
     for t in traces:
-        if t.head_dim != 128:
-            raise UnsupportedOperationError(f"head_dim {t.head_dim} unsupported (engine is d=128)")
+        _check_head_dim(t.head_dim)
         if mode == MODE_DIAGNOSTIC:
             S, und = _diagnostic_matrix(t, k, token_agg)
         elif mode == MODE_PLANNING:

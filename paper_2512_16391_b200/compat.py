@@ -47,16 +47,34 @@ def _dev():
     return torch.device("cuda")
 
 
+def _check_head_dim(d: int) -> None:
+    if not 1 <= d <= ops.HEAD_DIM:
+        raise UnsupportedOperationError(f"head_dim {d} unsupported (the engine's rows are {ops.HEAD_DIM} wide)")
+
+
+def _scale(trace) -> float:
+    """attention.py:120: 1/sqrt(d) of the trace's logical head dim."""
+    return 1.0 / math.sqrt(trace.head_dim)
+
+
 def _layer(trace, layer: int):
+    """One layer as bf16 device tensors [H][N][128].  A trace with d < 128
+    (the reference's own small-d tests) is zero-padded to the engine's row
+    width: Q.K^T is unchanged, every call passes the trace's 1/sqrt(d) and
+    the outputs are cut back to d (the C ABI's head_dim convention)."""
     if not 0 <= layer < trace.num_layers:
         raise InvalidArgumentError(f"layer {layer} out of range [0, {trace.num_layers})")
-    if trace.head_dim != 128:
-        raise UnsupportedOperationError(f"head_dim {trace.head_dim} unsupported (engine is d=128)")
+    _check_head_dim(trace.head_dim)
     dev = _dev()
     if hasattr(trace, "layer_device"):          # kscd_io.TraceFile: stream from the mmap
-        return trace.layer_device(layer, dev)
-    to = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev).to(torch.bfloat16)  # noqa
-    return to(trace.Q[layer]), to(trace.K[layer]), to(trace.V[layer])
+        q, k, v = trace.layer_device(layer, dev)
+    else:
+        to = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev).to(torch.bfloat16)  # noqa
+        q, k, v = to(trace.Q[layer]), to(trace.K[layer]), to(trace.V[layer])
+    pad = ops.HEAD_DIM - trace.head_dim
+    if pad:
+        q, k, v = (torch.nn.functional.pad(x, (0, pad)) for x in (q, k, v))
+    return q, k, v
 
 
 def _check_finite(Y: torch.Tensor, layer: int):
@@ -66,12 +84,12 @@ def _check_finite(Y: torch.Tensor, layer: int):
         raise NumericError("non-finite attention intermediate", layer=layer, head=h, row=r)
 
 
-def _probs(q, k, lse, causal: bool) -> torch.Tensor:
+def _probs(q, k, lse, causal: bool, d: int = 128) -> torch.Tensor:
     Hq, N = q.shape[0], q.shape[1]
     if N > MAX_P_SEQ:
         raise UnsupportedOperationError(f"materialised P needs N <= {MAX_P_SEQ} (got {N})")
     P = torch.empty(Hq, N, N, dtype=torch.float32, device=q.device)
-    p = _lib.ProbsParams(num_q_heads=Hq, num_kv_heads=k.shape[0], head_dim=128, seq_len=N,
+    p = _lib.ProbsParams(num_q_heads=Hq, num_kv_heads=k.shape[0], head_dim=d, seq_len=N,
                          causal=1 if causal else 0, q=q.data_ptr(), k=k.data_ptr(), q_stride_head=q.stride(0),
                          kv_stride_head=k.stride(0), lse=lse.data_ptr(), probs=P.data_ptr())
     _lib.call("kscd_dense_probs", p, ops._stream())
@@ -82,10 +100,11 @@ def dense_attention(trace, layer: int, causal: bool = True) -> Tuple[np.ndarray,
     """(P [Hq][N][N], Y [Hq][N][d]) of one layer; P is materialised only
     because the reference returns it (N <= MAX_P_SEQ)."""
     q, k, v = _layer(trace, layer)
-    out, lse = ops.dense_prefill(q, k, v, causal=causal)
-    Y = out.float()
+    d = trace.head_dim
+    out, lse = ops.dense_prefill(q, k, v, causal=causal, scale=_scale(trace))
+    Y = out[..., :d].float()
     _check_finite(Y, layer)
-    P = _probs(q, k, lse, causal)
+    P = _probs(q, k, lse, causal, d)
     return P.cpu().numpy(), Y.cpu().numpy()
 
 
@@ -137,7 +156,7 @@ def _standard_prefill(tiles, N: int, Hkv: int) -> bool:
         sorted((t.kv_head, t.tile_id, t.start, t.end) for t in want)
 
 
-def _sparse_any_tiles(q, k, v, tiles, sels, causal: bool):
+def _sparse_any_tiles(q, k, v, tiles, sels, causal: bool, scale: float):
     """Sparse attention for an arbitrary TileSpec: every query row is one
     'sequence' of the decode sparse kernel whose list is its tile's selection
     truncated to the keys <= row (the staircase), K/V shared (batch stride 0).
@@ -158,7 +177,7 @@ def _sparse_any_tiles(q, k, v, tiles, sels, causal: bool):
     vx = v.unsqueeze(0).expand(N, Hkv, N, 128)
     lse = torch.empty(N, Hq, dtype=torch.float32, device=dev)
     out = ops.sparse_decode(q_rows, kx, vx, N, torch.from_numpy(idx).to(dev), torch.from_numpy(vis).to(dev),
-                            None, lse=lse)
+                            None, lse=lse, scale=scale)
     return out.permute(1, 0, 2).contiguous(), lse.t().contiguous(), vis.T
 
 
@@ -179,7 +198,8 @@ def topk_attention(trace, layer: int, selections, tiles, causal: bool = True, de
                                        f"causal bound {t.causal_bound}")
     q, k, v = _layer(trace, layer)
     dev = q.device
-    _, lse_d = ops.dense_prefill(q, k, v, causal=causal)
+    sc = _scale(trace)
+    _, lse_d = ops.dense_prefill(q, k, v, causal=causal, scale=sc)
     if causal and _standard_prefill(tiles, N, Hkv):
         T = (N + ops.TILE - 1) // ops.TILE
         kc = max(1, max(s.size for s in sels.values()))
@@ -191,7 +211,7 @@ def topk_attention(trace, layer: int, selections, tiles, causal: bool = True, de
                 cnt[g, tid] = sel.size
         lse_s = torch.empty(Hq, N, dtype=torch.float32, device=dev)
         out, _ = ops.sparse_prefill(q, k, v, torch.from_numpy(idx).to(dev), torch.from_numpy(cnt).to(dev),
-                                    lse=lse_s)
+                                    lse=lse_s, scale=sc)
         Y = out.float()
         rows = torch.arange(N, device=dev)
         vis_np = np.zeros((Hkv, N), np.int64)
@@ -200,7 +220,7 @@ def topk_attention(trace, layer: int, selections, tiles, causal: bool = True, de
             vis_np[t.kv_head, t.start:t.end] = np.searchsorted(sel, np.arange(t.start, t.end), side="right")
         del rows
     else:
-        Y, lse_s, vis_np = _sparse_any_tiles(q, k, v, tiles, sels, causal)
+        Y, lse_s, vis_np = _sparse_any_tiles(q, k, v, tiles, sels, causal, sc)
         # rows with no visible selected key: the diagonal fallback V[g][r]
         dead = torch.from_numpy(vis_np == 0).to(dev)                     # [Hkv][N]
         if bool(dead.any()):
@@ -215,6 +235,7 @@ def topk_attention(trace, layer: int, selections, tiles, causal: bool = True, de
         dead_rows = rows[vis_np[t.kv_head, t.start:t.end] == 0]
         for h in range(t.kv_head * G, (t.kv_head + 1) * G):
             fallback.extend((h, int(r)) for r in dead_rows)
+    Y = Y[..., :trace.head_dim]
     return TopkAttentionResult(Y=Y.cpu().numpy(), mass_recovered=mass.float().cpu().numpy(), fallback_rows=fallback)
 
 
@@ -223,8 +244,8 @@ def run_dense(trace) -> np.ndarray:
     outs = []
     for layer in range(trace.num_layers):
         q, k, v = _layer(trace, layer)
-        out, _ = ops.dense_prefill(q, k, v)
-        outs.append(out.float())
+        out, _ = ops.dense_prefill(q, k, v, scale=_scale(trace))
+        outs.append(out[..., :trace.head_dim].float())
     return torch.stack(outs).cpu().numpy()
 
 
@@ -236,7 +257,7 @@ def _rel_l2(a: torch.Tensor, b: torch.Tensor) -> float:
     return float(num / den)
 
 
-def _select_any_tiles(q, k, lse, tiles, plan, Hkv: int) -> Dict[Tuple[int, int], np.ndarray]:
+def _select_any_tiles(q, k, lse, tiles, plan, Hkv: int, d: int = 128) -> Dict[Tuple[int, int], np.ndarray]:
     """_anchor_selections (runner.py:164-207) for an arbitrary TileSpec via
     materialised P (post) or the pre-softmax pooled rows."""
     dev = q.device
@@ -253,7 +274,7 @@ def _select_any_tiles(q, k, lse, tiles, plan, Hkv: int) -> Dict[Tuple[int, int],
     pre = plan.pooling == POOL_PRE
     rows = Hkv
     pooled = torch.zeros(rows, T, stride, dtype=torch.float32, device=dev)
-    pp = _lib.PoolTilesParams(num_q_heads=Hq, num_kv_heads=Hkv, head_dim=128, seq_len=N, num_tiles=T,
+    pp = _lib.PoolTilesParams(num_q_heads=Hq, num_kv_heads=Hkv, head_dim=d, seq_len=N, num_tiles=T,
                               tile_starts=starts.data_ptr(), tile_ends=ends.data_ptr(), pooling=1 if pre else 0,
                               all_heads=0, q=q.data_ptr(), k=k.data_ptr(), q_stride_head=q.stride(0),
                               kv_stride_head=k.stride(0), pooled=pooled.data_ptr(), pooled_stride=stride)
@@ -261,7 +282,7 @@ def _select_any_tiles(q, k, lse, tiles, plan, Hkv: int) -> Dict[Tuple[int, int],
         scratch = torch.empty(Hkv, T, stride, dtype=torch.float64, device=dev)
         pp.scratch = scratch.data_ptr()
     else:
-        P = _probs(q, k, lse, True)
+        P = _probs(q, k, lse, True, d)
         pp.probs = P.data_ptr()
     _lib.call("kscd_pool_tiles", pp, ops._stream())
     if all_heads:
@@ -298,17 +319,19 @@ def run_kascade(trace, plan, phase: str = PREFILL) -> Tuple[np.ndarray, RunRepor
     outputs = np.empty((L, Hq, N, trace.head_dim), np.float32)
     reports: List[LayerReport] = []
     cur = None               # fast path: (idx, cnt) device tensors; else dict of sets
+    d, sc = trace.head_dim, _scale(trace)
     for layer in range(L):
         q, k, v = _layer(trace, layer)
-        out_d, lse_d = ops.dense_prefill(q, k, v)
-        Yd = out_d.float()
+        out_d, lse_d = ops.dense_prefill(q, k, v, scale=sc)
+        Yd = out_d[..., :d].float()
         _check_finite(Yd, layer)
         is_anchor = layer == 0 or layer in anchors
         if is_anchor:
             if fast:
-                cur = ops.select_prefill(q, k, lse_d, plan.k_policy, all_heads=plan.mode == MODE_ALL_HEADS_POOLED)
+                cur = ops.select_prefill(q, k, lse_d, plan.k_policy, all_heads=plan.mode == MODE_ALL_HEADS_POOLED,
+                                         scale=sc)
             else:
-                cur = _select_any_tiles(q, k, lse_d, tiles, plan, Hkv)
+                cur = _select_any_tiles(q, k, lse_d, tiles, plan, Hkv, d)
         if layer == 0:
             outputs[0] = Yd.cpu().numpy()
             reports.append(LayerReport(0, KIND_ANCHOR0, 0.0, 1.0))
@@ -323,8 +346,8 @@ def run_kascade(trace, plan, phase: str = PREFILL) -> Tuple[np.ndarray, RunRepor
             else:
                 hmap = None
             lse_s = torch.empty(Hq, N, dtype=torch.float32, device=q.device)
-            out, _ = ops.sparse_prefill(q, k, v, idx, cnt, hmap, lse=lse_s)
-            Y = out.float()
+            out, _ = ops.sparse_prefill(q, k, v, idx, cnt, hmap, lse=lse_s, scale=sc)
+            Y = out[..., :d].float()
             fb = int((~torch.isfinite(lse_s)).sum().item())
         else:
             if kind == KIND_REUSE and plan.mode == MODE_REMAPPED:
@@ -332,10 +355,11 @@ def run_kascade(trace, plan, phase: str = PREFILL) -> Tuple[np.ndarray, RunRepor
                 sels = {(g, tid): cur[(hm[g], tid)] for (g, tid) in cur}
             else:
                 sels = cur
-            Y, lse_s, vis = _sparse_any_tiles(q, k, v, tiles, sels, True)
+            Y, lse_s, vis = _sparse_any_tiles(q, k, v, tiles, sels, True, sc)
             dead = torch.from_numpy(vis == 0).to(q.device)
             if bool(dead.any()):
                 Y = torch.where(dead.repeat_interleave(G, dim=0)[..., None], v.float().repeat_interleave(G, dim=0), Y)
+            Y = Y[..., :d]
             fb = int(dead.sum().item()) * G
         mass = torch.where(torch.isfinite(lse_s), torch.exp(lse_s - lse_d), torch.zeros_like(lse_s))
         outputs[layer] = Y.cpu().numpy()

@@ -33,6 +33,12 @@ int cuda_status(cudaError_t e, const char* what) {
 }
 
 constexpr int kMaxSplits = 64;
+
+// Every row is stored 128 elements wide.  A logical head_dim d < 128 means
+// the caller zero-padded Q and K past d (Q.K^T is then exact) and the
+// default softmax scale is 1/sqrt(d); output columns >= d are padding.
+bool bad_head_dim(int d) { return d < 1 || d > 128; }
+#define KSCD_HEAD_DIM_MSG "head_dim %d unsupported (1..128; rows are 128 wide, zero-padded past head_dim)"
 constexpr int kSmCount = 148;
 constexpr int kCtasPerSm = 2;
 
@@ -75,7 +81,7 @@ size_t decode_ws_bytes(const kscd_decode_params* p) {
 
 int check_decode(const kscd_decode_params* p, bool need_v, bool sparse) {
   if (!p) return fail(KSCD_INVALID_ARGUMENT, "params is NULL");
-  if (p->head_dim != 128) return fail(KSCD_UNSUPPORTED, "head_dim %d unsupported (engine is d=128)", p->head_dim);
+  if (bad_head_dim(p->head_dim)) return fail(KSCD_UNSUPPORTED, KSCD_HEAD_DIM_MSG, p->head_dim);
   if (p->batch < 1 || p->num_q_heads < 1 || p->num_kv_heads < 1)
     return fail(KSCD_INVALID_ARGUMENT, "batch/num_q_heads/num_kv_heads must be >= 1");
   if (p->num_q_heads % p->num_kv_heads)
@@ -251,7 +257,7 @@ int kscd_topk(const kscd_topk_params* p, void* stream) {
 // ------------------------------------------------------------------ prefill
 static int check_prefill(const kscd_prefill_params* p, bool sparse) {
   if (!p) return fail(KSCD_INVALID_ARGUMENT, "params is NULL");
-  if (p->head_dim != 128) return fail(KSCD_UNSUPPORTED, "head_dim %d unsupported (engine is d=128)", p->head_dim);
+  if (bad_head_dim(p->head_dim)) return fail(KSCD_UNSUPPORTED, KSCD_HEAD_DIM_MSG, p->head_dim);
   if (p->tile_size != 128) return fail(KSCD_UNSUPPORTED, "tile_size %d unsupported (engine tiles are 128)", p->tile_size);
   if (p->num_q_heads < 1 || p->num_kv_heads < 1 || p->num_q_heads % p->num_kv_heads)
     return fail(KSCD_INVALID_ARGUMENT, "num_query_heads (%d) must be divisible by num_kv_heads (%d)",
@@ -323,7 +329,7 @@ extern "C" int kscd_sparse_prefill(const kscd_prefill_params* p, void* stream) {
 
 extern "C" int kscd_dense_probs(const kscd_probs_params* p, void* stream) {
   if (!p) return fail(KSCD_INVALID_ARGUMENT, "params is NULL");
-  if (p->head_dim != 128) return fail(KSCD_UNSUPPORTED, "head_dim %d unsupported", p->head_dim);
+  if (bad_head_dim(p->head_dim)) return fail(KSCD_UNSUPPORTED, KSCD_HEAD_DIM_MSG, p->head_dim);
   if (p->num_q_heads < 1 || p->num_kv_heads < 1 || p->num_q_heads % p->num_kv_heads || p->seq_len < 1)
     return fail(KSCD_INVALID_ARGUMENT, "bad shape");
   if (!p->q || !p->k || !p->lse || !p->probs) return fail(KSCD_INVALID_ARGUMENT, "NULL buffer");
@@ -345,7 +351,7 @@ extern "C" int kscd_dense_probs(const kscd_probs_params* p, void* stream) {
 
 extern "C" int kscd_pool_tiles(const kscd_pool_tiles_params* p, void* stream) {
   if (!p) return fail(KSCD_INVALID_ARGUMENT, "params is NULL");
-  if (p->head_dim != 128) return fail(KSCD_UNSUPPORTED, "head_dim %d unsupported", p->head_dim);
+  if (bad_head_dim(p->head_dim)) return fail(KSCD_UNSUPPORTED, KSCD_HEAD_DIM_MSG, p->head_dim);
   if (p->num_q_heads < 1 || p->num_kv_heads < 1 || p->num_q_heads % p->num_kv_heads || p->seq_len < 1 ||
       p->num_tiles < 1)
     return fail(KSCD_INVALID_ARGUMENT, "bad shape");
@@ -372,12 +378,13 @@ extern "C" int kscd_pool_tiles(const kscd_pool_tiles_params* p, void* stream) {
   a.pooled = p->pooled;
   a.pool_stride = p->pooled_stride;
   a.scratch = p->scratch;
+  a.d = p->head_dim;
   return cuda_status(kscd::launch_pool_rows(a, (cudaStream_t)stream), "kscd_pool_tiles");
 }
 
 extern "C" int kscd_select_prefill(const kscd_select_prefill_params* p, void* stream) {
   if (!p) return fail(KSCD_INVALID_ARGUMENT, "params is NULL");
-  if (p->head_dim != 128) return fail(KSCD_UNSUPPORTED, "head_dim %d unsupported", p->head_dim);
+  if (bad_head_dim(p->head_dim)) return fail(KSCD_UNSUPPORTED, KSCD_HEAD_DIM_MSG, p->head_dim);
   if (p->tile_size != 128) return fail(KSCD_UNSUPPORTED, "tile_size %d unsupported", p->tile_size);
   if (p->num_q_heads < 1 || p->num_kv_heads < 1 || p->num_q_heads % p->num_kv_heads)
     return fail(KSCD_INVALID_ARGUMENT, "bad head shape");
@@ -441,7 +448,7 @@ extern "C" int kscd_select_prefill(const kscd_select_prefill_params* p, void* st
 
 extern "C" int kscd_append_kv(const kscd_append_kv_params* p, void* stream) {
   if (!p) return fail(KSCD_INVALID_ARGUMENT, "params is NULL");
-  if (p->head_dim != 128) return fail(KSCD_UNSUPPORTED, "head_dim %d unsupported", p->head_dim);
+  if (bad_head_dim(p->head_dim)) return fail(KSCD_UNSUPPORTED, KSCD_HEAD_DIM_MSG, p->head_dim);
   if (p->num_layers < 1 || p->batch < 1 || p->num_kv_heads < 1 || p->position < 0)
     return fail(KSCD_INVALID_ARGUMENT, "bad shape");
   if (!p->kv_new || !p->k_caches || !p->v_caches) return fail(KSCD_INVALID_ARGUMENT, "NULL buffer");

@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(256) pre_pool_kernel(const PoolRowsArgs a) {
   }
   __syncthreads();
   float* out = a.pooled + ((int64_t)g * a.T + t) * a.pool_stride;
-  const double inv_sqrt_d = 1.0 / sqrt(128.0);
+  const double inv_sqrt_d = 1.0 / sqrt((double)a.d);
   double mx = -1e300;
   for (int j = tid; j < e; j += 256) {
     double acc = 0.0;

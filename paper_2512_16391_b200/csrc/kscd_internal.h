@@ -146,6 +146,7 @@ struct PoolRowsArgs {
   float* pooled;                          // [Hkv or 1][T][pool_stride]
   int64_t pool_stride;
   double* scratch;                        // pre: [Hkv][T][pool_stride]
+  int d;                                  // logical head dim (pre-softmax scale 1/sqrt(d))
 };
 cudaError_t launch_pool_rows(const PoolRowsArgs& a, cudaStream_t st);
 

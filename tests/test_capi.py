@@ -44,10 +44,13 @@ def test_abi_version_and_k_budget(lib):
 def test_invalid_arguments_map_to_reference_errors(lib):
     from paper_2512_16391_b200 import _lib
     from paper_2512_16391_b200.exceptions import InvalidArgumentError, UnsupportedOperationError
-    p = _lib.DecodeParams(batch=1, num_q_heads=8, num_kv_heads=2, head_dim=64, seq_len=4)
+    p = _lib.DecodeParams(batch=1, num_q_heads=8, num_kv_heads=2, head_dim=129, seq_len=4)
     with pytest.raises(UnsupportedOperationError):
         _lib.call("kscd_dense_decode", p, 0)
-    p.head_dim = 128
+    p.head_dim = 0
+    with pytest.raises(UnsupportedOperationError):
+        _lib.call("kscd_dense_decode", p, 0)
+    p.head_dim = 64                 # logical d < 128: rows zero-padded to 128 (header Conventions)
     p.num_kv_heads = 3
     with pytest.raises(InvalidArgumentError, match="divisible"):
         _lib.call("kscd_dense_decode", p, 0)

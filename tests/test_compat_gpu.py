@@ -240,3 +240,49 @@ def test_invalid_plans(cuda_ok):
     maps = {1: identity_head_map(2, reuse_layer=1, anchor_layer=2)}
     with pytest.raises(InvalidPlanError):
         compat.run_kascade(t, AnchorPlan(AnchorPlanCore([0, 2], 2, 0.0), head_maps=maps))
+
+
+# ---------------------------------------------------------- head_dim < 128
+@pytest.mark.parametrize("d", [16, 64])
+def test_small_head_dim_matches_reference_golden(cuda_ok, d):
+    """The reference's tests use d in {4..64}: the engine zero-pads rows to
+    128 and passes 1/sqrt(d) (make_smalld_golden.py)."""
+    from paper_2512_16391_b200 import AnchorPlan, AnchorPlanCore, HeadMap, KBudgetPolicy, compat
+    z = golden("smalld")
+    t = trace(bf16(z[f"Q{d}"]), bf16(z[f"K{d}"]), bf16(z[f"V{d}"]))
+    P, Y = compat.dense_attention(t, 0)
+    assert Y.shape == (4, 48, d)
+    assert_outputs_close(Y, z[f"Y{d}"])
+    np.testing.assert_allclose(P, z[f"P{d}"], atol=2e-5)
+    core = AnchorPlanCore([0, 1], 2, 0.0)
+    maps = {2: HeadMap(2, 1, [1, 0])}
+    pol = KBudgetPolicy(0.25, 4)
+    outs, rep = compat.run_kascade(t, AnchorPlan(core, head_maps=maps, k_policy=pol, tile_size=16))
+    assert_outputs_close(outs, z[f"outs{d}"])
+    np.testing.assert_allclose([r.mass_recovered_mean for r in rep.per_layer], z[f"mass{d}"], atol=2e-3)
+    outs, _ = compat.run_kascade(t, AnchorPlan(core, head_maps=maps, pooling="pre", k_policy=pol, tile_size=16))
+    assert_outputs_close(outs, z[f"outs_pre{d}"])
+    outs, rep = compat.run_kascade(t, AnchorPlan(core, head_maps=maps, k_policy=pol, tile_size=16), phase="decode")
+    assert_outputs_close(outs, z[f"outs_dec{d}"])
+    np.testing.assert_allclose([r.mass_recovered_mean for r in rep.per_layer], z[f"mass_dec{d}"], atol=2e-3)
+
+
+def test_small_head_dim_fast_prefill_path_matches_oracle(cuda_ok):
+    """d = 64 through the tcgen05 prefill kernels (tile 128, post pooling)
+    against the oracle on the same bf16 inputs."""
+    from paper_2512_16391_b200 import AnchorPlan, AnchorPlanCore, HeadMap, KBudgetPolicy, compat
+    Q, K, V = orc.random_qkv(77, 3, 4, 2, 64, 300)
+    Q, K, V = (orc.bf16_round(x) for x in (Q, K, V))
+    t = trace(Q, K, V)
+    plan = AnchorPlan(AnchorPlanCore([0, 1], 2, 0.0), head_maps={2: HeadMap(2, 1, [1, 0])},
+                      k_policy=KBudgetPolicy(0.25, 16), tile_size=128)
+    outs, _ = compat.run_kascade(t, plan)
+    ref, _ = orc.run_kascade(Q, K, V, [0, 1], {2: [1, 0]}, 0.25, 16, tile_size=128)
+    assert_outputs_close(outs, ref)
+
+
+def test_head_dim_above_128_rejected(cuda_ok):
+    from paper_2512_16391_b200 import UnsupportedOperationError, compat
+    Q, K, V = orc.random_qkv(5, 1, 2, 1, 160, 8)
+    with pytest.raises(UnsupportedOperationError):
+        compat.dense_attention(trace(Q, K, V), 0)

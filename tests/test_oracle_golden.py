@@ -108,6 +108,23 @@ def test_mode_variants_match_reference():
     np.testing.assert_allclose(outs, z["outs_pre"], rtol=0, atol=1e-6)
 
 
+@pytest.mark.parametrize("d", [16, 64])
+def test_small_head_dim_matches_reference(d):
+    """The reference's own small-d traces (make_smalld_golden.py)."""
+    z = golden("smalld")
+    Q, K, V = bf16(z[f"Q{d}"]), bf16(z[f"K{d}"]), bf16(z[f"V{d}"])
+    P, Y = orc.dense_layer(Q[0], K[0], V[0])
+    np.testing.assert_allclose(P, z[f"P{d}"], rtol=0, atol=1e-6)
+    np.testing.assert_allclose(Y, z[f"Y{d}"], rtol=0, atol=1e-6)
+    for key, kw in ((f"outs{d}", {}), (f"outs_pre{d}", {"pooling": orc.PRE}), (f"outs_dec{d}", {"phase": "decode"})):
+        outs, rep = orc.run_kascade(Q, K, V, [0, 1], {2: [1, 0]}, 0.25, 4, tile_size=16, **kw)
+        np.testing.assert_allclose(outs, z[key], rtol=0, atol=1e-6)
+        if key.startswith("outs_dec"):
+            np.testing.assert_allclose([r["mass"] for r in rep], z[f"mass_dec{d}"], rtol=1e-6)
+        elif not key.startswith("outs_pre"):
+            np.testing.assert_allclose([r["mass"] for r in rep], z[f"mass{d}"], rtol=1e-6)
+
+
 @pytest.fixture(scope="module")
 def config1():
     meta = json.load(open(os.path.join(GOLDEN, "golden.json")))
