@@ -1,7 +1,7 @@
 """``python -m paper_2512_16391_b200 gen|analyze|plan|run|cost|report``: the
 reference CLI (cli.py:33-112) on this package -- ``run`` on the B200 engine,
 ``analyze`` / ``plan`` on the GPU calibration (calibration.py), ``cost`` over
-the B200 presets (costmodel.py), ``gen`` / ``report`` with the same trace,
+the paper's Table 3 or the measured B200 presets (costmodel.py), ``gen`` / ``report`` with the same trace,
 plan and report formats.  Exit codes as in the reference (cli.py:20-23).
 
     python -m paper_2512_16391_b200 run --trace t.kscd --plan p.json \\
@@ -9,7 +9,7 @@ plan and report formats.  Exit codes as in the reference (cli.py:20-23).
     python -m paper_2512_16391_b200 plan --trace a.kscd [b.kscd ...] --out plan.json [--budget 5] [--k 64]
         [--token-agg min|mean] [--tile-size 128] [--pooling post|pre] [--mode remapped|all-heads-pooled]
         [--fraction 0.1] [--k-min 128] [--no-importance]
-    python -m paper_2512_16391_b200 cost [--preset b200-decode-131072-k10 ...] [--list-presets]
+    python -m paper_2512_16391_b200 cost [--preset table3-decode-131072-k10 ...] [--list-presets] [--table b200]
         [--ratios a0,a,r | --predict] [--phase] [--fraction] [--seq-len] [--layers] [--anchors]
         [--baseline-time] [--csv] [--out results.json]
 
@@ -83,10 +83,13 @@ def build_parser():
     plan.add_argument("--out", required=True)
     cost = sub.add_parser("cost", help="weighted-average pipeline time and speedup (B200 presets)")
     cost.add_argument("--preset", action="append", default=None,
-                      help="B200 preset name (repeatable); see --list-presets")
+                      help="preset name, e.g. table3-decode-131072-k10 or b200-decode-131072-k10 (repeatable)")
     cost.add_argument("--list-presets", action="store_true")
+    cost.add_argument("--table", choices=["table3", "b200"], default="table3",
+                      help="preset table for --list-presets, --predict and the default listing: the paper's "
+                           "H100 Table 3 (reference default) or the rows measured on B200")
     cost.add_argument("--ratios", default=None, help="anchor0,anchor,reuse per-layer times")
-    cost.add_argument("--predict", action="store_true", help="use the ratio model fitted on the B200 rows")
+    cost.add_argument("--predict", action="store_true", help="use the ratio model fitted on --table's rows")
     cost.add_argument("--phase", choices=["decode", "prefill"], default="decode")
     cost.add_argument("--fraction", type=float, default=0.1)
     cost.add_argument("--seq-len", type=int, default=131072)
@@ -99,7 +102,8 @@ def build_parser():
 
 
 def _cost_rows(args):
-    """cli.py:236-273 over the B200 presets."""
+    """cli.py:236-273; ``--table b200`` selects the measured B200 rows for
+    the listing and the fitted prediction."""
     from . import costmodel
     from .exceptions import KascadeError
     rows = []
@@ -117,43 +121,54 @@ def _cost_rows(args):
             params, {"anchor0": parts[0], "anchor": parts[1], "reuse": parts[2]}), None))
     elif args.predict:
         rep = costmodel.predict_report(args.phase, args.fraction, args.seq_len, num_layers=args.layers,
-                                       num_anchors=args.anchors, baseline_layer_time=args.baseline_time)
-        rows.append((f"predict-b200-{args.phase}-{args.seq_len}-k{args.fraction}", rep, None))
+                                       num_anchors=args.anchors, baseline_layer_time=args.baseline_time,
+                                       table=args.table)
+        tag = "" if args.table == costmodel.TABLE_PUBLISHED else f"{args.table}-"
+        rows.append((f"predict-{tag}{args.phase}-{args.seq_len}-k{args.fraction}", rep, None))
     else:
-        for name in costmodel.preset_names():
+        for name in costmodel.preset_names(args.table):
             rows.append((name, costmodel.report_from_preset(name), costmodel.get_preset(name)))
     return rows
 
 
+def _tabulated(row):
+    """The row's own pipeline time / speedup columns: printed as published
+    for Table 3 rows (cli.py:284-297), 6 significant digits for B200 rows."""
+    from . import costmodel
+    if row.table == costmodel.TABLE_PUBLISHED:
+        return f"{row.kascade_ms}", f"{row.speedup_tl}"
+    return f"{row.kascade_ms:.6g}", f"{row.speedup_tl:.6g}"
+
+
 def cmd_cost(args) -> int:
-    """cli.py:276-320; the reference's "published" columns are the
-    measured B200 pipeline time / speedup of the preset row."""
+    """cli.py:276-320 (same text, CSV and JSON forms)."""
     import json
     from . import costmodel
     if args.list_presets:
-        for name in costmodel.preset_names():
+        for name in costmodel.preset_names(args.table):
             print(name)
         return EXIT_OK
     rows = _cost_rows(args)
     if args.csv:
-        print("name,kascade_time,baseline_time,speedup,measured_time,measured_speedup")
+        print("name,kascade_time,baseline_time,speedup,published_time,published_speedup")
         for name, rep, row in rows:
-            mt = f"{row.kascade_ms:.6g}" if row else ""
-            ms = f"{row.speedup:.6g}" if row else ""
-            print(f"{name},{rep.kascade_time:.6g},{rep.baseline_time:.6g},{rep.speedup:.6g},{mt},{ms}")
+            pub_t, pub_s = _tabulated(row) if row else ("", "")
+            print(f"{name},{rep.kascade_time:.6g},{rep.baseline_time:.6g},{rep.speedup:.6g},{pub_t},{pub_s}")
     else:
         for name, rep, row in rows:
             line = f"{name}: time={rep.kascade_time:.4g} baseline={rep.baseline_time:.4g} speedup={rep.speedup:.3f}"
             if row:
-                line += f" (measured B200 time={row.kascade_ms:.4g} speedup={row.speedup:.3f})"
+                pub_t, pub_s = _tabulated(row)
+                label = "published" if row.table == costmodel.TABLE_PUBLISHED else "measured B200"
+                line += f" ({label} time={pub_t} speedup={pub_s})"
             if not rep.valid:
                 line += f" [!] {rep.note}"
             print(line)
     if args.out:
         payload = [{"name": name, "kascade_time": rep.kascade_time, "baseline_time": rep.baseline_time,
                     "speedup": rep.speedup, "per_kind": rep.per_kind, "valid": rep.valid,
-                    "measured_time": row.kascade_ms if row else None,
-                    "measured_speedup": row.speedup if row else None} for name, rep, row in rows]
+                    "published_time": row.kascade_ms if row else None,
+                    "published_speedup": row.speedup_tl if row else None} for name, rep, row in rows]
         with open(args.out, "w", encoding="utf-8") as f:
             json.dump(payload, f, indent=2)
             f.write("\n")
@@ -183,14 +198,6 @@ def cmd_gen(args) -> int:
     return EXIT_OK
 
 
-def _csv_similarity(S) -> str:
-    lines = ["row,col,value"]
-    for a in range(S.num_layers):
-        for b in range(a, S.num_layers):
-            lines.append(f"{a},{b},{S.S[a, b]:.8g}")
-    return "\n".join(lines) + "\n"
-
-
 def cmd_analyze(args) -> int:
     """cli.py:151-192 with P, coverage and the similarity matrix on the GPU."""
     from pathlib import Path
@@ -199,15 +206,12 @@ def cmd_analyze(args) -> int:
     traces = [kscd_io.TraceFile(p) for p in args.trace]
     out_dir = Path(args.out_dir)
     out_dir.mkdir(parents=True, exist_ok=True)
-    lines = ["layer,head,coverage"]
-    for layer in range(traces[0].num_layers):
-        per = [compat.mass_coverage(calibration.layer_probs(t, layer).cpu().numpy(), args.k) for t in traces]
-        for head, cov in enumerate(np.atleast_1d(np.mean(per, axis=0))):
-            lines.append(f"{layer},{head},{cov:.8g}")
-    (out_dir / "coverage.csv").write_text("\n".join(lines) + "\n")
+    coverage = [np.mean([compat.mass_coverage(calibration.layer_probs(t, layer).cpu().numpy(), args.k)
+                         for t in traces], axis=0) for layer in range(traces[0].num_layers)]
+    (out_dir / "coverage.csv").write_text(kscd_io.coverage_csv(coverage))
     S = calibration.similarity_matrix(traces, k=args.k, token_agg=args.token_agg, mode=args.mode,
                                       tile_size=args.tile_size)
-    (out_dir / "similarity.csv").write_text(_csv_similarity(S))
+    (out_dir / "similarity.csv").write_text(kscd_io.similarity_csv(S))
     if args.importance:
         if all(t.X is not None and t.Y is not None for t in traces):
             imp = calibration.layer_importance(traces)
@@ -215,8 +219,7 @@ def cmd_analyze(args) -> int:
             print("warning: trace(s) lack attention input/output hidden states; using uniform importance weights",
                   file=sys.stderr)
             imp = calibration.LayerImportance(w=np.ones(traces[0].num_layers), source_prompt_count=len(traces))
-        (out_dir / "importance.csv").write_text(
-            "\n".join(["layer,weight"] + [f"{l},{w:.8g}" for l, w in enumerate(imp.w)]) + "\n")
+        (out_dir / "importance.csv").write_text(kscd_io.importance_csv(imp))
     print(f"analyzed {len(traces)} trace(s): k={args.k} mode={args.mode} token_agg={args.token_agg} "
           f"undefined_scores={S.undefined_scores} -> {out_dir}")
     return EXIT_OK
@@ -275,10 +278,16 @@ def main(argv=None) -> int:
     failure) and every OSError maps to exit 2, as in the reference main
     (cli.py:341-361); argparse errors return 1."""
     from .exceptions import KascadeError
+    parser = build_parser()
     try:
-        args = build_parser().parse_args(argv)
+        args = parser.parse_args(argv)
     except SystemExit as e:
         return int(e.code or 0)
+    if args.command == "gen" and args.q_heads % args.kv_heads != 0:     # usage error (cli.py:346-352)
+        parser.print_usage(sys.stderr)
+        sys.stderr.write(f"{parser.prog}: error: --q-heads ({args.q_heads}) must be divisible "
+                         f"by --kv-heads ({args.kv_heads})\n")
+        return EXIT_USAGE
     try:
         return {"gen": cmd_gen, "analyze": cmd_analyze, "cost": cmd_cost, "plan": cmd_plan, "run": cmd_run,
                 "report": cmd_report}[args.command](args)

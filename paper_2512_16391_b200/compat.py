@@ -495,3 +495,74 @@ def pooled_all_heads_topk(group_dists, k: int, tile_id: int = 0) -> TopKIndexSet
         g = g[None]
     pooled = _dev64(g).mean(dim=0).cpu().numpy()
     return oracle_topk_indices(pooled, k, kv_head=-1, tile_id=tile_id)
+
+
+def topk_table(arr, take: int) -> np.ndarray:
+    """ranking.py:14-25: indices of the ``take`` largest entries along the
+    last axis, ordered by (value descending, index ascending) -- a stable
+    device sort of the negated values."""
+    a = np.asarray(arr)
+    take = min(int(take), a.shape[-1])
+    t = torch.from_numpy(np.ascontiguousarray(a)).to(_dev())
+    order = torch.sort(-t, dim=-1, stable=True).indices[..., :take]
+    return order.cpu().numpy()
+
+
+def topk_tables(P, k: int) -> np.ndarray:
+    """heads.py:62-64: per-kv-head, per-token Top-k index tables [Hkv][N][min(k, N)]."""
+    P = np.asarray(P)
+    return topk_table(P, min(k, P.shape[-1]))
+
+
+def group_distributions(trace, layer: int, P=None) -> np.ndarray:
+    """heads.py:50-59: per-kv-head, per-token distributions (the mean of the
+    group's query-head rows of P, fp64 -> fp32) [Hkv][N][N]; P from the
+    device dense pass when not given."""
+    from .calibration import layer_probs
+    Pd = layer_probs(trace, layer) if P is None else torch.from_numpy(np.ascontiguousarray(P)).to(_dev())
+    Hq, N = Pd.shape[0], Pd.shape[1]
+    Hkv = trace.num_kv_heads
+    return Pd.double().view(Hkv, Hq // Hkv, N, Pd.shape[2]).mean(dim=1).float().cpu().numpy()
+
+
+def _token_topk(pooled, k: int):
+    """metrics.py:133-149: per-token Top-k over the causal rows of a pooled
+    [N][N] distribution: (idx [N][take] padded with -1, valid [N][take],
+    den [N] = each row's fp64 mass on its own set)."""
+    pooled = np.asarray(pooled)
+    N = pooled.shape[0]
+    take = min(k, N)
+    order = torch.from_numpy(topk_table(pooled, take)).to(_dev())
+    ar = torch.arange(take, device=order.device)
+    valid = ar[None, :] < torch.clamp(torch.arange(N, device=order.device) + 1, max=take)[:, None]
+    pd = torch.from_numpy(np.ascontiguousarray(pooled)).to(_dev()).double()
+    gathered = torch.gather(pd, 1, torch.where(valid, order, torch.zeros_like(order)))
+    den = torch.where(valid, gathered, torch.zeros_like(gathered)).sum(dim=1)
+    idx = torch.where(valid, order, torch.full_like(order, -1))
+    return idx.cpu().numpy(), valid.cpu().numpy(), den.cpu().numpy()
+
+
+def head_similarity_from_dists(Pa, Pb, k: int = 64, token_agg: str = "mean", idx_a=None) -> np.ndarray:
+    """heads.py:67-108 with the reference's signature: [Hkv][Hkv] reuse
+    scores from two layers' per-kv-head distributions (numpy, as from
+    group_distributions) or the anchor's Top-k tables ``idx_a``.  The
+    masked sums run in the kscd_masked_mass kernel (fp64)."""
+    from . import calibration as cal
+    cal._check_agg(token_agg)
+    Db = torch.from_numpy(np.ascontiguousarray(Pb, dtype=np.float32)).to(_dev())
+    Hkv, N = Db.shape[0], Db.shape[1]
+    take = min(k, N)
+    if idx_a is None:
+        idx, cnt = cal._token_sets(torch.from_numpy(np.ascontiguousarray(Pa, dtype=np.float32)).to(_dev()), k)
+    else:
+        # only the first min(r + 1, take) entries of each table row count
+        # (heads.py:86); the masked sum does not depend on their order
+        idx = torch.from_numpy(np.ascontiguousarray(idx_a, dtype=np.int32)[..., :take]).to(_dev())
+        cnt = torch.clamp(torch.arange(N, device=idx.device, dtype=torch.int32) + 1, max=take).repeat(Hkv, 1)
+        idx = torch.where(torch.arange(take, device=idx.device)[None, None, :] < cnt[..., None], idx,
+                          torch.zeros_like(idx))
+    idx_b, cnt_b = cal._token_sets(Db, k)
+    num = cal.masked_mass(Db, idx, cnt, N).cpu().numpy()
+    own = cal.masked_mass(Db, idx_b, cnt_b, N).cpu().numpy()
+    den = np.stack([own[j, j] for j in range(Hkv)])
+    return cal._aggregate_scores(num, den, token_agg)

@@ -1,19 +1,20 @@
-"""B200 presets for the reference's analytic cost model (SURVEY.md 8(f)
-rank 4).
+"""The reference's analytic cost model (costmodel.py), with B200 presets
+(SURVEY.md 8(f) rank 4).
 
-The reference bundles the paper's H100 kernel microbenchmarks as presets
-(costmodel.py:43-112, PUBLISHED_BENCH) and fits a ratio model on them
-(costmodel.py:204-258).  This module restates the same arithmetic -- the
+Two tables of per-layer kernel times feed the same arithmetic -- the
 weighted pipeline time (costmodel.py:156-184), the per-preset report
-(187-201) and the least-squares ratio fit and prediction (204-280) -- over
-rows MEASURED on B200 with this engine (scripts/table3_b200.py ->
-b200_presets.json): dense baseline layer, anchor0, anchor and reuse layer
-times per phase / context / Top-k %.  The dense baseline is this engine's
-own Top-k = 100 % mode (both of the paper's baseline columns map to it).
+(187-201) and the least-squares ratio fit and prediction (204-280):
 
-Names, dataclass fields and error types follow the reference so
-`kascade cost` users find the same API; presets are named
-``b200-{phase}-{seq_len}-k{pct}``.
+* ``PUBLISHED_BENCH`` -- the paper's H100 Table 3 rows the reference
+  bundles (costmodel.py:64-112), presets ``table3-{phase}-{seq}-k{pct}``.
+  Every reference name defaults to this table, so a reference caller gets
+  the reference's numbers (pinned by tests/golden/costmodel_ref.json).
+* ``B200_BENCH`` -- rows MEASURED on B200 with this engine
+  (scripts/table3_b200.py -> b200_presets.json): the dense baseline layer
+  (this engine's Top-k = 100 % mode, standing in for both of the paper's
+  baseline columns), anchor0, anchor and reuse layer times, presets
+  ``b200-{phase}-{seq}-k{pct}``; pass ``table="b200"`` to the fit and the
+  predictions.
 """
 
 import json
@@ -29,76 +30,100 @@ from .exceptions import InvalidArgumentError
 PHASE_DECODE = "decode"
 PHASE_PREFILL = "prefill"
 
-PIPELINE_LAYERS = 32       # Llama-3.1-8B, the shapes behind the presets
-PIPELINE_ANCHORS = 5       # anchors [0, 2, 8, 13, 14]
+PIPELINE_LAYERS = 32       # layer count behind the published weights (costmodel.py:35)
+PIPELINE_ANCHORS = 5       # anchor count behind the published weights (costmodel.py:36)
 
 FIT_MIN_SEQ = 65536        # rows used for the ratio fit (costmodel.py:38)
 VALID_MIN_SEQ = 16384      # below this the fitted model is flagged (costmodel.py:39)
 
-_PRESETS = os.path.join(os.path.dirname(os.path.abspath(__file__)), "b200_presets.json")
+TABLE_PUBLISHED, TABLE_B200 = "table3", "b200"
+_HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 @dataclass(frozen=True)
 class BenchRow:
-    """One measured B200 row (times in ms per layer), the reference's
-    BenchRow (costmodel.py:42-62) with the baseline columns = dense_ms."""
+    """One kernel microbenchmark row, times in ms per layer
+    (costmodel.py:42-62; same fields and order).  ``table`` names the
+    preset family; B200 rows carry their dense layer in both baseline
+    columns and derive the ratio / pipeline columns from their times."""
 
     phase: str
     seq_len: int
     topk_pct: int
-    dense_ms: float
+    fa3_ms: float
+    tl_ms: float
     anchor0_ms: float
+    anchor0_ratio: float
     anchor_ms: float
+    anchor_ratio: float
     reuse_ms: float
+    reuse_ratio: float
+    kascade_ms: float
+    speedup_fa3: float
+    speedup_tl: float
+    table: str = TABLE_PUBLISHED
     batch: int = 1
 
     @property
-    def anchor0_ratio(self) -> float:
-        return self.anchor0_ms / self.dense_ms
+    def preset_name(self) -> str:
+        return f"{self.table}-{self.phase}-{self.seq_len}-k{self.topk_pct}"
 
     @property
-    def anchor_ratio(self) -> float:
-        return self.anchor_ms / self.dense_ms
-
-    @property
-    def reuse_ratio(self) -> float:
-        return self.reuse_ms / self.dense_ms
-
-    @property
-    def kascade_ms(self) -> float:
-        return (self.anchor0_ms + (PIPELINE_ANCHORS - 1) * self.anchor_ms
-                + (PIPELINE_LAYERS - PIPELINE_ANCHORS) * self.reuse_ms) / PIPELINE_LAYERS
+    def dense_ms(self) -> float:
+        """The baseline column report_from_preset divides by."""
+        return self.tl_ms
 
     @property
     def speedup(self) -> float:
-        return self.dense_ms / self.kascade_ms
-
-    @property
-    def preset_name(self) -> str:
-        return f"b200-{self.phase}-{self.seq_len}-k{self.topk_pct}"
+        return self.speedup_tl
 
 
-def _load() -> List[BenchRow]:
-    with open(_PRESETS, "r", encoding="utf-8") as f:
+def _published() -> List[BenchRow]:
+    with open(os.path.join(_HERE, "published_table3.json"), "r", encoding="utf-8") as f:
         data = json.load(f)
-    return [BenchRow(phase=r["phase"], seq_len=int(r["seq_len"]), topk_pct=int(r["topk_pct"]),
-                     dense_ms=float(r["dense_ms"]), anchor0_ms=float(r["anchor0_ms"]),
-                     anchor_ms=float(r["anchor_ms"]), reuse_ms=float(r["reuse_ms"]),
-                     batch=int(r.get("batch", 1))) for r in data["rows"]]
+    return [BenchRow(**dict(zip(data["fields"], row))) for row in data["rows"]]
 
 
-B200_BENCH: List[BenchRow] = _load()
+def _b200_row(phase, seq_len, topk_pct, dense_ms, anchor0_ms, anchor_ms, reuse_ms, batch=1) -> BenchRow:
+    kascade = (anchor0_ms + (PIPELINE_ANCHORS - 1) * anchor_ms
+               + (PIPELINE_LAYERS - PIPELINE_ANCHORS) * reuse_ms) / PIPELINE_LAYERS
+    return BenchRow(phase, seq_len, topk_pct, dense_ms, dense_ms, anchor0_ms, anchor0_ms / dense_ms, anchor_ms,
+                    anchor_ms / dense_ms, reuse_ms, reuse_ms / dense_ms, kascade, dense_ms / kascade,
+                    dense_ms / kascade, table=TABLE_B200, batch=batch)
 
 
-def preset_names() -> List[str]:
-    return [row.preset_name for row in B200_BENCH]
+def _b200() -> List[BenchRow]:
+    with open(os.path.join(_HERE, "b200_presets.json"), "r", encoding="utf-8") as f:
+        data = json.load(f)
+    return [_b200_row(r["phase"], int(r["seq_len"]), int(r["topk_pct"]), float(r["dense_ms"]),
+                      float(r["anchor0_ms"]), float(r["anchor_ms"]), float(r["reuse_ms"]), int(r.get("batch", 1)))
+            for r in data["rows"]]
+
+
+PUBLISHED_BENCH: List[BenchRow] = _published()
+B200_BENCH: List[BenchRow] = _b200()
+_TABLES = {TABLE_PUBLISHED: PUBLISHED_BENCH, TABLE_B200: B200_BENCH}
+
+
+def _table(table: str) -> List[BenchRow]:
+    if table not in _TABLES:
+        raise InvalidArgumentError(f"unknown preset table {table!r}; known: {', '.join(_TABLES)}")
+    return _TABLES[table]
+
+
+def preset_names(table: str = TABLE_PUBLISHED) -> List[str]:
+    """costmodel.py:115-116 (``table="b200"`` for the measured B200 rows)."""
+    return [row.preset_name for row in _table(table)]
 
 
 def get_preset(name: str) -> BenchRow:
-    for row in B200_BENCH:
-        if row.preset_name == name:
-            return row
-    raise InvalidArgumentError(f"unknown preset {name!r}; known presets: {', '.join(preset_names())}")
+    """costmodel.py:119-125; resolves ``table3-...`` and ``b200-...`` names."""
+    for rows in _TABLES.values():
+        for row in rows:
+            if row.preset_name == name:
+                return row
+    raise InvalidArgumentError(f"unknown preset {name!r}; known presets: "
+                               f"{', '.join(preset_names(TABLE_PUBLISHED) + preset_names(TABLE_B200))}")
 
 
 @dataclass
@@ -148,7 +173,8 @@ def weighted_pipeline_time(params: CostParams, per_kind_times: Dict[str, float])
 
 
 def report_from_preset(name: str) -> CostReport:
-    """costmodel.py:187-201 on a B200 row against its own dense column."""
+    """costmodel.py:187-201: one row's per-kind times against its own
+    dense-baseline column (tl_ms)."""
     row = get_preset(name)
     params = CostParams(phase=row.phase, topk_fraction=row.topk_pct / 100.0, seq_len=row.seq_len,
                         baseline_layer_time=row.dense_ms)
@@ -187,25 +213,26 @@ def fit_ratios_from(rows, phase: str) -> RatioFit:
 
 
 @lru_cache(maxsize=None)
-def fit_ratios(phase: str) -> RatioFit:
-    """fit_ratios_from over the measured B200 rows."""
-    return fit_ratios_from(B200_BENCH, phase)
+def fit_ratios(phase: str, table: str = TABLE_PUBLISHED) -> RatioFit:
+    """costmodel.py:212-238: fit_ratios_from over one preset table."""
+    return fit_ratios_from(_table(table), phase)
 
 
-def predict_ratios(phase: str, topk_fraction: float, seq_len: int) -> Dict[str, float]:
+def predict_ratios(phase: str, topk_fraction: float, seq_len: int, table: str = TABLE_PUBLISHED) -> Dict[str, float]:
     """costmodel.py:244-258."""
     if not (0.0 < topk_fraction <= 1.0):
         raise InvalidArgumentError(f"topk_fraction must be in (0, 1], got {topk_fraction}")
-    fit = fit_ratios(phase)
+    fit = fit_ratios(phase, table)
     reuse = topk_fraction + fit.c_gather
     return {"anchor0": 1.0 + fit.c_select, "anchor": fit.c_pass1 + fit.c_select + reuse, "reuse": reuse,
             "valid": float(seq_len >= VALID_MIN_SEQ)}
 
 
 def predict_report(phase: str, topk_fraction: float, seq_len: int, num_layers: int = PIPELINE_LAYERS,
-                   num_anchors: int = PIPELINE_ANCHORS, baseline_layer_time: float = 1.0) -> CostReport:
+                   num_anchors: int = PIPELINE_ANCHORS, baseline_layer_time: float = 1.0,
+                   table: str = TABLE_PUBLISHED) -> CostReport:
     """costmodel.py:261-280."""
-    ratios = predict_ratios(phase, topk_fraction, seq_len)
+    ratios = predict_ratios(phase, topk_fraction, seq_len, table)
     params = CostParams(phase=phase, num_layers=num_layers, num_anchors=num_anchors, topk_fraction=topk_fraction,
                         seq_len=seq_len, baseline_layer_time=baseline_layer_time)
     times = {kind: ratios[kind] * baseline_layer_time for kind in ("anchor0", "anchor", "reuse")}

@@ -281,21 +281,47 @@ class AttentionTrace:
     prompt_id: str = ""
 
     def __post_init__(self):
+        self.validate()
+
+    def validate(self) -> None:
+        """trace.py:52-98: positive dims, GQA divisibility, tensor shapes,
+        finite payloads, X/Y together with matching [L][N][model_dim]."""
         dims = dict(num_layers=self.num_layers, num_query_heads=self.num_query_heads,
                     num_kv_heads=self.num_kv_heads, head_dim=self.head_dim, seq_len=self.seq_len)
         for name, v in dims.items():
             if v < 1:
                 raise InvalidArgumentError(f"{name} must be >= 1, got {v}")
         if self.num_query_heads % self.num_kv_heads:
-            raise InvalidArgumentError("num_query_heads must be divisible by num_kv_heads")
+            raise InvalidArgumentError(f"num_query_heads ({self.num_query_heads}) must be divisible by "
+                                       f"num_kv_heads ({self.num_kv_heads})")
         L, Hq, Hkv, d, N = (self.num_layers, self.num_query_heads, self.num_kv_heads, self.head_dim,
                             self.seq_len)
         for name, shape in (("Q", (L, Hq, N, d)), ("K", (L, Hkv, N, d)), ("V", (L, Hkv, N, d))):
             arr = getattr(self, name)
             if tuple(arr.shape) != shape:
                 raise InvalidArgumentError(f"{name} has shape {tuple(arr.shape)}, header implies {shape}")
+            if not np.isfinite(arr).all():
+                raise InvalidArgumentError(f"{name} contains non-finite values")
         if (self.X is None) != (self.Y is None):
             raise InvalidArgumentError("X and Y must be supplied together")
+        if self.X is not None:
+            for name in ("X", "Y"):
+                arr = getattr(self, name)
+                if arr.ndim != 3 or arr.shape[0] != L or arr.shape[1] != N:
+                    raise InvalidArgumentError(f"{name} has shape {tuple(arr.shape)}, expected "
+                                               f"[L={L}][N={N}][model_dim]")
+                if not np.isfinite(arr).all():
+                    raise InvalidArgumentError(f"{name} contains non-finite values")
+            if self.X.shape != self.Y.shape:
+                raise InvalidArgumentError(f"X shape {tuple(self.X.shape)} != Y shape {tuple(self.Y.shape)}")
+
+    def equals(self, other) -> bool:
+        """trace.py:100-120: bit-exact equality of header and tensors."""
+        head = ("num_layers", "num_query_heads", "num_kv_heads", "head_dim", "seq_len", "prompt_id")
+        if any(getattr(self, f) != getattr(other, f) for f in head) or self.has_xy() != other.has_xy():
+            return False
+        names = ("Q", "K", "V", "X", "Y") if self.has_xy() else ("Q", "K", "V")
+        return all(np.array_equal(getattr(self, n), getattr(other, n)) for n in names)
 
     @property
     def group_size(self) -> int:

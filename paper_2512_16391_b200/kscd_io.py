@@ -189,15 +189,26 @@ def write_report(path, report: RunReport) -> None:
         f.write("\n")
 
 
+def report_from_dict(data: dict) -> RunReport:
+    """traceio.py:438-453."""
+    rows = [LayerReport(e["layer"], e["kind"], e["output_rel_err_l2"], e["mass_recovered_mean"],
+                        e.get("fallback_rows", 0)) for e in data.get("per_layer", [])]
+    return RunReport(per_layer=rows, overall=data.get("overall", {}), config=data.get("config", {}))
+
+
 def read_report(path) -> RunReport:
     with open(path, "r", encoding="utf-8") as f:
         try:
             data = json.load(f)
         except json.JSONDecodeError as e:
             raise FormatError(f"report file is not valid JSON: {e}") from None
-    rows = [LayerReport(e["layer"], e["kind"], e["output_rel_err_l2"], e["mass_recovered_mean"],
-                        e.get("fallback_rows", 0)) for e in data.get("per_layer", [])]
-    return RunReport(per_layer=rows, overall=data.get("overall", {}), config=data.get("config", {}))
+    return report_from_dict(data)
+
+
+def plans_equal(a, b) -> bool:
+    """traceio.py:410-411: equal serialised forms."""
+    from .host_types import plan_to_dict
+    return plan_to_dict(a) == plan_to_dict(b)
 
 
 def format_report(report: RunReport) -> str:
@@ -213,3 +224,28 @@ def format_report(report: RunReport) -> str:
     for key, val in sorted(report.config.items()):
         buf.write(f"  # {key}: {val}\n")
     return buf.getvalue()
+
+
+# ----------------------------------------------------- CSV text forms (analyze)
+def similarity_csv(S) -> str:
+    """traceio.py:488-494: upper triangle of a SimilarityMatrix."""
+    lines = ["row,col,value"]
+    for a in range(S.num_layers):
+        for b in range(a, S.num_layers):
+            lines.append(f"{a},{b},{S.S[a, b]:.8g}")
+    return "\n".join(lines) + "\n"
+
+
+def importance_csv(importance) -> str:
+    """traceio.py:497-501."""
+    lines = ["layer,weight"] + [f"{layer},{w:.8g}" for layer, w in enumerate(importance.w)]
+    return "\n".join(lines) + "\n"
+
+
+def coverage_csv(coverage_by_layer) -> str:
+    """traceio.py:504-510: coverage_by_layer[l][h] = mean Top-k mass of (layer l, head h)."""
+    lines = ["layer,head,coverage"]
+    for layer, per_head in enumerate(coverage_by_layer):
+        for head, cov in enumerate(np.atleast_1d(per_head)):
+            lines.append(f"{layer},{head},{cov:.8g}")
+    return "\n".join(lines) + "\n"

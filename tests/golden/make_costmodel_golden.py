@@ -41,7 +41,34 @@ def main():
                                                                             "reuse": r}))})
     for args in [("decode", 0.1, 131072, 32, 5, 1.0), ("prefill", 0.25, 8192, 36, 5, 3.0)]:
         out["predict"].append({"args": list(args), "report": rep(cm.predict_report(*args))})
+    # the reference CLI's `cost` output (cli.py:236-320), stdout verbatim
+    import contextlib
+    import io
+    from kascade.cli import main as ref_main
+    out["cli"] = []
+    for argv in (["cost", "--preset", "table3-decode-131072-k10", "--preset", "table3-prefill-8192-k30"],
+                 ["cost", "--preset", "table3-prefill-131072-k20", "--csv"],
+                 ["cost", "--predict", "--phase", "prefill", "--csv"],
+                 ["cost", "--predict", "--fraction", "0.25", "--seq-len", "8192"],
+                 ["cost", "--ratios", "1.2,0.9,0.1", "--baseline-time", "2", "--layers", "40", "--anchors", "6"],
+                 ["cost", "--list-presets"],
+                 ["cost"]):
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            rc = ref_main(list(argv))
+        out["cli"].append({"argv": argv, "rc": rc, "stdout": buf.getvalue()})
     json.dump(out, open(os.path.join(HERE, "costmodel_ref.json"), "w"), indent=1)
+    # the paper's Table 3 rows (costmodel.py:64-112) as package data, so the
+    # reference-named presets resolve to the same numbers
+    fields = ["phase", "seq_len", "topk_pct", "fa3_ms", "tl_ms", "anchor0_ms", "anchor0_ratio", "anchor_ms",
+              "anchor_ratio", "reuse_ms", "reuse_ratio", "kascade_ms", "speedup_fa3", "speedup_tl"]
+    table = {"source": "Kascade paper Table 3 (H100 kernel microbenchmarks), as bundled by the reference "
+                       "(costmodel.py:64-112); frozen by tests/golden/make_costmodel_golden.py",
+             "fields": fields, "rows": [[getattr(r, f) for f in fields] for r in cm.PUBLISHED_BENCH]}
+    with open(os.path.join(HERE, "..", "..", "paper_2512_16391_b200", "published_table3.json"), "w") as f:
+        head = json.dumps({k: v for k, v in table.items() if k != "rows"}, indent=1)[:-2]
+        rows = ",\n  ".join(json.dumps(r) for r in table["rows"])
+        f.write(f'{head},\n "rows": [\n  {rows}\n ]\n}}\n')
 
 
 if __name__ == "__main__":

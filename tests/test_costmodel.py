@@ -58,20 +58,45 @@ def test_preset_report_formula_matches_reference():
         _same_report(got, GOLD["presets"][name])
 
 
+def test_published_table_is_the_reference_default():
+    """Reference names give the reference's numbers (costmodel_ref.json)."""
+    assert len(cm.PUBLISHED_BENCH) == len(GOLD["rows"])
+    for row, ref in zip(cm.PUBLISHED_BENCH, GOLD["rows"]):
+        for k, v in ref.items():
+            assert getattr(row, k) == v, (row.preset_name, k)
+    assert cm.preset_names() == [f"table3-{r['phase']}-{r['seq_len']}-k{r['topk_pct']}" for r in GOLD["rows"]]
+    for name, ref in GOLD["presets"].items():
+        _same_report(cm.report_from_preset(name), ref)
+    for phase in ("decode", "prefill"):
+        fit, ref = cm.fit_ratios(phase), GOLD["fits"][phase]
+        _close(fit.c_gather, ref["c_gather"])
+        _close(fit.c_select, ref["c_select"])
+        _close(fit.c_pass1, ref["c_pass1"])
+    for case in GOLD["predict"]:
+        _same_report(cm.predict_report(*case["args"]), case["report"])
+    assert cm.get_preset("table3-decode-131072-k10").kascade_ms == 2.83
+
+
 def test_b200_presets_load_and_report():
-    names = cm.preset_names()
+    names = cm.preset_names("b200")
     assert len(names) == len(set(names)) >= 30
     assert "b200-decode-131072-k10" in names and "b200-prefill-131072-k10" in names
     for name in names:
         row = cm.get_preset(name)
         rep = cm.report_from_preset(name)
-        assert row.dense_ms > 0 and row.reuse_ms > 0
+        assert row.table == "b200" and row.dense_ms > 0 and row.reuse_ms > 0
         assert abs(rep.kascade_time - row.kascade_ms) < 1e-9
         assert abs(rep.speedup - row.speedup) < 1e-9
+        assert abs(row.reuse_ratio - row.reuse_ms / row.dense_ms) < 1e-12
     # the sparse reuse layer is cheaper than dense at every measured point
     assert all(r.reuse_ms < r.dense_ms for r in cm.B200_BENCH)
+    fit = cm.fit_ratios("decode", "b200")
+    assert fit.c_gather != cm.fit_ratios("decode").c_gather
+    assert cm.predict_report("decode", 0.1, 131072, table="b200").speedup > 1.0
     with pytest.raises(InvalidArgumentError):
-        cm.get_preset("table3-decode-131072-k10")
+        cm.get_preset("b200-decode-1-k99")
+    with pytest.raises(InvalidArgumentError):
+        cm.preset_names("h100")
 
 
 def test_predict_and_validation():
@@ -88,6 +113,9 @@ def test_predict_and_validation():
 
 def test_cost_cli(tmp_path, capsys):
     out = tmp_path / "c.json"
+    for case in GOLD["cli"]:                       # the reference CLI's stdout, verbatim
+        assert cli.main(list(case["argv"])) == case["rc"]
+        assert capsys.readouterr().out == case["stdout"], case["argv"]
     assert cli.main(["cost", "--preset", "b200-decode-131072-k10", "--out", str(out)]) == 0
     text = capsys.readouterr().out
     assert text.startswith("b200-decode-131072-k10: time=") and "measured B200" in text
@@ -96,5 +124,11 @@ def test_cost_cli(tmp_path, capsys):
     assert cli.main(["cost", "--ratios", "1.2,0.9,0.1", "--baseline-time", "1"]) == 0
     assert cli.main(["cost", "--ratios", "1,2"]) == 2
     assert cli.main(["cost", "--preset", "nope"]) == 2
+    capsys.readouterr()
     assert cli.main(["cost", "--list-presets"]) == 0
+    assert capsys.readouterr().out.splitlines()[0] == "table3-decode-8192-k10"
+    assert cli.main(["cost", "--list-presets", "--table", "b200"]) == 0
+    assert capsys.readouterr().out.splitlines()[0].startswith("b200-")
     assert cli.main(["cost", "--predict", "--phase", "prefill", "--csv"]) == 0
+    assert cli.main(["cost", "--predict", "--table", "b200"]) == 0
+    assert "predict-b200-decode-131072-k0.1" in capsys.readouterr().out

@@ -42,3 +42,42 @@ def test_utility_errors(cuda_ok):
     with pytest.raises(k.InvalidArgumentError):
         d.validate()
     k.AttentionDistribution(np.array([0.25, 0.75]), np.array([1, 3])).validate()
+
+
+def test_namespace_device_utilities_match_reference(cuda_ok):
+    """ranking.topk_table, heads.topk_tables / head_similarity_from_dists /
+    group_distributions and metrics._token_topk with the reference's
+    signatures (tests/golden/namespace_ref.npz)."""
+    from paper_2512_16391_b200.kascade import heads, metrics, ranking
+    z = golden("namespace_ref")
+    np.testing.assert_array_equal(ranking.topk_table(z["arr"], 9), z["table"])
+    np.testing.assert_array_equal(ranking.topk_table(z["arr"], 40), z["table_all"])
+    np.testing.assert_array_equal(ranking.topk_table(z["ties"], 33), z["ties_all"])   # stable: index ascending
+    # partial tables with ties at the k-th value keep the smallest indices
+    # (the reference's argpartition picks an implementation-defined subset;
+    # every masked sum over the set is the same either way)
+    part = ranking.topk_table(z["ties"], 9)
+    np.testing.assert_array_equal(part, z["ties_all"][..., :9])
+    np.testing.assert_array_equal(heads.topk_tables(z["Pa"], 5), z["tables"])
+    for key, kw in (("hs_mean", {"token_agg": "mean"}), ("hs_min", {"token_agg": "min"})):
+        np.testing.assert_allclose(heads.head_similarity_from_dists(z["Pa"], z["Pb"], 5, **kw), z[key],
+                                   rtol=0, atol=1e-7)
+    np.testing.assert_allclose(heads.head_similarity_from_dists(None, z["Pb"], 5, "mean", idx_a=z["tables"]),
+                               z["hs_idx"], rtol=0, atol=1e-7)
+    idx, valid, den = metrics._token_topk(z["Pa"][1], 7)
+    np.testing.assert_array_equal(idx, z["tok_idx"])
+    np.testing.assert_array_equal(valid, z["tok_valid"])
+    np.testing.assert_allclose(den, z["tok_den"], rtol=1e-12)
+
+
+def test_namespace_group_distributions_match_oracle(cuda_ok):
+    """heads.group_distributions: the group mean of dense P, fp64 -> fp32."""
+    from oracle import kascade_oracle as orc
+    from paper_2512_16391_b200 import AttentionTrace
+    from paper_2512_16391_b200.kascade import heads
+    Q, K, V = (orc.bf16_round(x) for x in orc.random_qkv(9, 1, 4, 2, 64, 40))
+    t = AttentionTrace(1, 4, 2, 64, 40, Q, K, V)
+    P, _ = orc.dense_layer(Q[0], K[0], V[0])
+    want = np.stack([P[2 * g:2 * g + 2].mean(axis=0, dtype=np.float64) for g in range(2)]).astype(np.float32)
+    np.testing.assert_allclose(heads.group_distributions(t, 0), want, rtol=0, atol=2e-6)
+    np.testing.assert_allclose(heads.group_distributions(t, 0, P=P), want, rtol=0, atol=1e-7)
