@@ -67,7 +67,18 @@ cudaError_t launch_pool_decode(const PoolDecodeArgs& a, cudaStream_t st) {
 // ------------------------------------------------------------------ Top-k
 constexpr int kTopkThreads = 512;
 constexpr int kTopkWarps = kTopkThreads / 32;
-constexpr int kTopkItems = 8;  // consecutive elements per thread per compaction chunk
+#ifndef KSCD_TOPK_BATCH
+#define KSCD_TOPK_BATCH 2
+#endif
+// float4 loads in flight per thread in the counting passes.  Measured on
+// B200 (scripts/perf_topk.py, same box): 1 -> 2 cuts the decode select
+// 65.5 -> 62.2 us (64 rows x 128K) and the 128K prefill select 2658 -> 2426
+// us; 4 is equal on decode and slower on prefill; 8 drops occupancy.
+constexpr int kTopkBatch = KSCD_TOPK_BATCH;
+#ifndef KSCD_TOPK_ITEMS
+#define KSCD_TOPK_ITEMS 8
+#endif
+constexpr int kTopkItems = KSCD_TOPK_ITEMS;  // consecutive elements per thread per compaction chunk
 
 KSCD_DEV uint32_t order_key(float f) {
   const uint32_t u = __float_as_uint(f + 0.0f);  // -0 -> +0: equal values tie
@@ -103,20 +114,35 @@ KSCD_DEV uint32_t block_excl_scan(uint32_t v, uint32_t* warp_tot, uint32_t& tota
   return res;
 }
 
-// Four consecutive values of a row (plus the second partial plane when the
-// row is stored as two sums, see pool_prefill.cu); out-of-range -> 0.
-KSCD_DEV void load4(const float* vals, const float* vals2, int j, int end, bool vec, float (&v)[4]) {
+// Four consecutive values of a row; out-of-range -> 0.
+KSCD_DEV void load4_plane(const float* vals, int j, int end, bool vec, float (&v)[4]) {
   if (vec && j + 3 < end) {
     const float4 f = __ldcg(reinterpret_cast<const float4*>(vals + j));
     v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-    if (vals2) {
-      const float4 f2 = __ldcg(reinterpret_cast<const float4*>(vals2 + j));
-      v[0] += f2.x; v[1] += f2.y; v[2] += f2.z; v[3] += f2.w;
-    }
   } else {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      v[i] = j + i < end ? __ldcg(vals + j + i) + (vals2 ? __ldcg(vals2 + j + i) : 0.f) : 0.f;
+    for (int i = 0; i < 4; ++i) v[i] = j + i < end ? __ldcg(vals + j + i) : 0.f;
+  }
+}
+
+// NB groups of four values at j0 + b*step (plus the second partial plane
+// when the row is stored as two sums, see pool_prefill.cu).  Every load is
+// issued before the first add: an add right behind its own load (even a
+// predicated-off one) waits on the load's scoreboard and serialises the
+// loads -- the dominant stall of the counting passes (ncu, decode shapes).
+template <int NB>
+KSCD_DEV void load_groups(const float* vals, const float* vals2, int j0, int step, int end, bool vec,
+                          float (&v)[NB][4]) {
+#pragma unroll
+  for (int b = 0; b < NB; ++b) load4_plane(vals, j0 + b * step, end, vec, v[b]);
+  if (vals2) {
+    float w[NB][4];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) load4_plane(vals2, j0 + b * step, end, vec, w[b]);
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[b][i] += w[b][i];
   }
 }
 
@@ -172,23 +198,30 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
     const int nb = pass == 2 ? 256 : 4096;
     for (int i = tid; i < nb; i += kTopkThreads) sh.hist[i] = 0;
     __syncthreads();
-    for (int it = 0; it < iters; ++it) {
-      const int j = seg0 + (it * kTopkThreads + tid) * 4;
-      float v[4];
-      load4(vals, vals2, j, seg1, vec, v);
+    // kTopkBatch float4 loads in flight per thread before any atomic: the
+    // row streams from L2 and one outstanding load per thread leaves the
+    // pass latency-bound (few CTAs per SM at decode shapes)
+#pragma unroll 1
+    for (int it0 = 0; it0 < iters; it0 += kTopkBatch) {
+      float v[kTopkBatch][4];
+      load_groups<kTopkBatch>(vals, vals2, seg0 + (it0 * kTopkThreads + tid) * 4, kTopkThreads * 4, seg1, vec, v);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t key = order_key(v[i]);
-        const bool m = (j + i < seg1) && ((key & pmask) == prefix);
-        const uint32_t bin = (key >> shift) & (nb - 1);
-        if (AGG) {
-          const uint32_t act = __ballot_sync(0xffffffffu, m);
-          if (m) {
-            const uint32_t peers = __match_any_sync(act, bin);
-            if (lane == __ffs(peers) - 1) atomicAdd(&sh.hist[bin], (uint32_t)__popc(peers));
+      for (int b = 0; b < kTopkBatch; ++b) {
+        const int j = seg0 + ((it0 + b) * kTopkThreads + tid) * 4;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t key = order_key(v[b][i]);
+          const bool m = (j + i < seg1) && ((key & pmask) == prefix);
+          const uint32_t bin = (key >> shift) & (nb - 1);
+          if (AGG) {
+            const uint32_t act = __ballot_sync(0xffffffffu, m);
+            if (m) {
+              const uint32_t peers = __match_any_sync(act, bin);
+              if (lane == __ffs(peers) - 1) atomicAdd(&sh.hist[bin], (uint32_t)__popc(peers));
+            }
+          } else if (m) {
+            atomicAdd(&sh.hist[bin], 1u);
           }
-        } else if (m) {
-          atomicAdd(&sh.hist[bin], 1u);
         }
       }
     }
@@ -272,15 +305,19 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
   // ---- ordered compaction ------------------------------------------------
   const int chunk = kTopkThreads * kTopkItems;
   uint32_t gt_seg = 0, eq_seg = 0;
-  for (int base = seg0; base < seg1; base += kTopkThreads * 4) {
-    const int j = base + tid * 4;
-    float v[4];
-    load4(vals, vals2, j, seg1, vec, v);
+#pragma unroll 1
+  for (int base = seg0; base < seg1; base += kTopkThreads * 4 * kTopkBatch) {
+    float v[kTopkBatch][4];
+    load_groups<kTopkBatch>(vals, vals2, base + tid * 4, kTopkThreads * 4, seg1, vec, v);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t key = order_key(v[i]);
-      gt_seg += (j + i < seg1 && key > T);
-      eq_seg += (j + i < seg1 && key == T);
+    for (int b = 0; b < kTopkBatch; ++b) {
+      const int j = base + (b * kTopkThreads + tid) * 4;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t key = order_key(v[b][i]);
+        gt_seg += (j + i < seg1 && key > T);
+        eq_seg += (j + i < seg1 && key == T);
+      }
     }
   }
   uint32_t tg, te;
@@ -306,13 +343,11 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
     uint32_t keys[kTopkItems];
     uint32_t gt = 0, eq = 0;
     const int j0 = base + tid * kTopkItems;
+    {
+      float v[kTopkItems / 4][4];
+      load_groups<kTopkItems / 4>(vals, vals2, j0, 4, seg1, vec, v);
 #pragma unroll
-    for (int h = 0; h < kTopkItems; h += 4) {
-      float v[4];
-      const int j = j0 + h;
-      load4(vals, vals2, j, seg1, vec, v);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) keys[h + i] = order_key(v[i]);
+      for (int h = 0; h < kTopkItems; ++h) keys[h] = order_key(v[h / 4][h % 4]);
     }
 #pragma unroll
     for (int i = 0; i < kTopkItems; ++i) {
@@ -503,8 +538,9 @@ __global__ void __launch_bounds__(kFastThreads) topk_sample_kernel(const TopkArg
   const int iters = (n + 4 * kFastThreads - 1) / (4 * kFastThreads);
   for (int it = 0; it < iters; ++it) {
     const int j = (it * kFastThreads + tid) * 4;
-    float v[4];
-    load4(vals, vals2, j, n, vec, v);
+    float v4[1][4];
+    load_groups<1>(vals, vals2, j, 0, n, vec, v4);
+    const float (&v)[4] = v4[0];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const uint32_t key = order_key(v[i]);
@@ -540,12 +576,11 @@ __global__ void __launch_bounds__(kFastThreads) topk_sample_kernel(const TopkArg
     uint32_t keys[kTopkItems];
     uint32_t gt = 0, eq = 0;
     const int j0 = base + tid * kTopkItems;
+    {
+      float v[kTopkItems / 4][4];
+      load_groups<kTopkItems / 4>(vals, vals2, j0, 4, n, vec, v);
 #pragma unroll
-    for (int h = 0; h < kTopkItems; h += 4) {
-      float v[4];
-      load4(vals, vals2, j0 + h, n, vec, v);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) keys[h + i] = order_key(v[i]);
+      for (int h = 0; h < kTopkItems; ++h) keys[h] = order_key(v[h / 4][h % 4]);
     }
 #pragma unroll
     for (int i = 0; i < kTopkItems; ++i) {
