@@ -85,6 +85,18 @@ def shard_plan(plan, fraction, k_min):
                       k_policy=KBudgetPolicy(fraction, k_min))
 
 
+def _decode_gather_ceiling(achieved: float):
+    """The reuse kernel against the measured random-row HBM gather ceiling
+    (profiles/hbm_gather_ceiling.json, scripts/micro/hbm_gather.cu): the
+    same lists and bytes with plain loads and no math."""
+    try:
+        peak = float(json.load(open(os.path.join(REPO, "profiles", "hbm_gather_ceiling.json")))["random_rows_best_GBs"])
+    except (OSError, KeyError, ValueError):
+        return None
+    return {"bound": "hbm_random_rows", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "peak_kind": "measured (scripts/micro/hbm_gather.cu)", "frac": round(achieved / peak, 4)}
+
+
 def load_traffic(key):
     """Per-launch DRAM bytes of a roofline kernel from the committed ncu capture
     (profiles/traffic.json), or None when the bench shape has none."""
@@ -802,7 +814,8 @@ def main():
                      "frac": round(achieved / hbm, 4), "traffic": load_traffic(f"sparse_decode_{n // 1024}k_b{B}"),
                      "peak_kind": peaks_kind,
                      "bytes_per_launch": reuse_bytes, "launch_ms": round(reuse_ms, 4),
-                     "dense_decode_frac": round(dense_bytes / (dense_ms_launch * 1e-3) / 1e9 / hbm, 4)},
+                     "dense_decode_frac": round(dense_bytes / (dense_ms_launch * 1e-3) / 1e9 / hbm, 4),
+                     "gather": _decode_gather_ceiling(achieved)},
         "clocks": clk,
         "gpu_launches": launches_per_step * args.steps,
         "cpu_baseline": cpu,
