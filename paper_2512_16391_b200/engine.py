@@ -16,6 +16,8 @@ dominate the small reuse layers.
 
 from __future__ import annotations
 
+import os
+
 from typing import Dict, List, Optional, Sequence
 
 import torch
@@ -33,6 +35,10 @@ def layer_kinds(plan, num_layers: int) -> List[str]:
 
 
 class KascadeDecoder:
+    # output-copy chunk boundaries of capture_host_step (layers); overridable
+    # for experiments as KSCD_D2H_SPLITS="16,28"
+    D2H_SPLITS = tuple(int(x) for x in os.environ.get("KSCD_D2H_SPLITS", "8,16,24").split(",") if x)
+
     def __init__(self, plan, num_layers: int, batch: int, num_q_heads: int, num_kv_heads: int,
                  max_seq_len: int, device=None, validate: bool = True):
         if validate:   # sharded executors validate against the GLOBAL head count themselves
@@ -129,42 +135,49 @@ class KascadeDecoder:
             if t.is_cuda or not t.is_pinned():
                 raise InvalidArgumentError(f"{name} must be pinned host memory")
         kv_dev = torch.empty(kv_host.shape, dtype=torch.bfloat16, device=self.device)
-        tables = ops.cache_pointer_tables(k_caches, v_caches, self.device)
+        kp, vp, sb, sh = ops.cache_pointer_tables(k_caches, v_caches, self.device)
+        tables0, tables_rest = (kp[:1], vp[:1], sb, sh), (kp[1:], vp[1:], sb, sh)
         layer = self._dense_layer if dense else self._layer
         # The copies are pipelined against the layer loop on two side streams
-        # (graph branches): the new K/V rows and layer 0's queries arrive
-        # first, the other layers' queries stream in (one copy) behind layer
-        # 0, and the outputs leave in chunks of 8 layers as they complete.
+        # (graph branches): layer 0's new K/V rows and queries arrive first
+        # and layer 0 starts behind their append; the other layers' rows and
+        # queries stream in behind layer 0 and get one append launch.  The
+        # outputs leave in chunks that shrink toward the end (boundaries
+        # D2H_SPLITS), so the copy exposed after the last layer is small.
         # Few cross-stream edges keep consecutive reuse-layer kernels chained
         # by programmatic dependent launch (decode.cu).
         h2d, d2h = torch.cuda.Stream(device=self.device), torch.cuda.Stream(device=self.device)
         ev_first, ev_rest = torch.cuda.Event(), torch.cuda.Event()
-        chunk = 8
-        ev_done = [torch.cuda.Event() for _ in range(0, self.L, chunk)]
+        ends = sorted({e for e in self.D2H_SPLITS if 0 < e < self.L} | {self.L})
+        ev_done = [torch.cuda.Event() for _ in ends]
 
         def body():
             main = torch.cuda.current_stream()
             h2d.wait_stream(main)
             d2h.wait_stream(main)
             with torch.cuda.stream(h2d):
-                kv_dev.copy_(kv_host, non_blocking=True)
+                kv_dev[:1].copy_(kv_host[:1], non_blocking=True)
                 q[0].copy_(q_host[0], non_blocking=True)
                 ev_first.record(h2d)
                 if self.L > 1:
+                    kv_dev[1:].copy_(kv_host[1:], non_blocking=True)
                     q[1:].copy_(q_host[1:], non_blocking=True)
                 ev_rest.record(h2d)
             main.wait_event(ev_first)
-            ops.append_kv(kv_dev, seq_len - 1, tables)
+            ops.append_kv(kv_dev[:1], seq_len - 1, tables0)
+            start = 0
             for l in range(self.L):
                 if l == 1:
                     main.wait_event(ev_rest)
+                    ops.append_kv(kv_dev[1:], seq_len - 1, tables_rest)
                 layer(l, q, k_caches, v_caches, seq_len)
-                if (l + 1) % chunk == 0 or l == self.L - 1:
-                    c = l // chunk
+                if l + 1 in ends:
+                    c = ends.index(l + 1)
                     ev_done[c].record(main)
                     with torch.cuda.stream(d2h):
                         d2h.wait_event(ev_done[c])
-                        out_host[c * chunk:l + 1].copy_(self.out[c * chunk:l + 1], non_blocking=True)
+                        out_host[start:l + 1].copy_(self.out[start:l + 1], non_blocking=True)
+                    start = l + 1
             main.wait_stream(h2d)
             main.wait_stream(d2h)
 
@@ -173,7 +186,7 @@ class KascadeDecoder:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             body()
-        self._graphs[("host", seq_len, dense)] = (g, kv_dev, tables, h2d, d2h)   # keep the staging alive
+        self._graphs[("host", seq_len, dense)] = (g, kv_dev, kp, vp, h2d, d2h)   # keep the staging alive
         return g
 
 
