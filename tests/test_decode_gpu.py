@@ -262,7 +262,8 @@ def test_decode_engine_llama_shapes_vs_oracle(cuda_ok):
         assert_outputs_close(out[:, b], Y)
 
 
-def test_host_step_graph_appends_and_matches_step(cuda_ok):
+@pytest.mark.parametrize("splits", [(), (1, 2)])
+def test_host_step_graph_appends_and_matches_step(cuda_ok, splits):
     """capture_host_step (pinned H2D + one-launch KV append + layer loop +
     D2H as one CUDA graph) equals appending by hand and running step(); the
     appended rows land bit-exactly at position n-1 of every layer."""
@@ -280,6 +281,7 @@ def test_host_step_graph_appends_and_matches_step(cuda_ok):
     Kr = [x.clone() for x in Ks]
     Vr = [x.clone() for x in Vs]
     dec = engine.KascadeDecoder(plan, L, B, Hq, Hkv, n_cap)
+    dec.D2H_SPLITS = splits                        # one output copy, or one per layer
     q = torch.empty(L, B, Hq, 128, dtype=torch.bfloat16, device="cuda")
     graph = dec.capture_host_step(q_host, kv_host, out_host, q, Ks, Vs, n)
     out_host.zero_()

@@ -1,0 +1,59 @@
+"""Head-group shapes beyond the bench's GQA-4: MHA (G = 1), odd groups
+(G = 3), G = 8 and G = 16 through the decode and prefill executors, against
+the oracle (decode_step / run_kascade) on the same bf16 inputs, with
+non-identity head maps and ragged lengths.  Needs a B200."""
+import numpy as np
+import pytest
+
+from oracle import kascade_oracle as orc
+from parity import assert_outputs_close
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+SHAPES = [(2, 2), (6, 2), (8, 1), (16, 1), (12, 4)]
+
+
+def _maps(Hkv):
+    """A non-identity map for layer 1 (a reuse layer) when Hkv > 1."""
+    return list(reversed(range(Hkv)))
+
+
+@pytest.mark.parametrize("Hq,Hkv", SHAPES)
+def test_decode_engine_head_groups(cuda_ok, Hq, Hkv):
+    from paper_2512_16391_b200 import engine
+    from paper_2512_16391_b200.host_types import AnchorPlan, AnchorPlanCore, HeadMap, KBudgetPolicy
+    L, B, n = 3, 2, 1531
+    rng = np.random.default_rng(Hq * 31 + Hkv)
+    hm = _maps(Hkv)
+    plan = AnchorPlan(AnchorPlanCore([0, 2], 2, 0.0), head_maps={1: HeadMap(1, 0, hm)},
+                      k_policy=KBudgetPolicy(0.1, 16))
+    q = orc.bf16_round((rng.standard_normal((L, B, Hq, 128)) * 2.5).astype(np.float32))
+    K = orc.bf16_round(rng.standard_normal((L, B, Hkv, n, 128)).astype(np.float32))
+    V = orc.bf16_round(rng.standard_normal((L, B, Hkv, n, 128)).astype(np.float32))
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda().to(torch.bfloat16)  # noqa: E731
+    dec = engine.KascadeDecoder(plan, L, B, Hq, Hkv, n)
+    out = dec.step(dev(q), [dev(K[l]) for l in range(L)], [dev(V[l]) for l in range(L)], n).cpu().numpy()
+    for b in range(B):
+        Y, _, _ = orc.decode_step(q[:, b], K[:, b], V[:, b], [0, 2], {1: hm}, 0.1, 16, want_mass=False)
+        assert_outputs_close(out[:, b], Y)
+
+
+@pytest.mark.parametrize("Hq,Hkv", SHAPES)
+def test_prefill_engine_head_groups(cuda_ok, Hq, Hkv):
+    from paper_2512_16391_b200 import engine
+    from paper_2512_16391_b200.host_types import AnchorPlan, AnchorPlanCore, HeadMap, KBudgetPolicy
+    L, N = 3, 601
+    rng = np.random.default_rng(Hq * 17 + Hkv)
+    hm = _maps(Hkv)
+    plan = AnchorPlan(AnchorPlanCore([0, 2], 2, 0.0), head_maps={1: HeadMap(1, 0, hm)},
+                      k_policy=KBudgetPolicy(0.2, 32), tile_size=128)
+    Q = orc.bf16_round((rng.standard_normal((L, Hq, N, 128)) * 2.0).astype(np.float32))
+    K = orc.bf16_round(rng.standard_normal((L, Hkv, N, 128)).astype(np.float32))
+    V = orc.bf16_round(rng.standard_normal((L, Hkv, N, 128)).astype(np.float32))
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda().to(torch.bfloat16)  # noqa: E731
+    eng = engine.KascadePrefill(plan, L, Hq, Hkv, N)
+    out = eng.forward([dev(Q[l]) for l in range(L)], [dev(K[l]) for l in range(L)],
+                      [dev(V[l]) for l in range(L)]).float().cpu().numpy()
+    want, _ = orc.run_kascade(Q, K, V, [0, 2], {1: hm}, 0.2, 32, tile_size=128)
+    assert_outputs_close(out, want)
