@@ -146,12 +146,23 @@ KSCD_DEV void load_groups(const float* vals, const float* vals2, int j0, int ste
   }
 }
 
+// Keys of the threshold bin of the first digit that a CTA keeps on chip
+// (candidate mode, see the kernel); more than this in any CTA of a cluster
+// and the row takes the full-segment passes instead.
+#ifndef KSCD_TOPK_CAND
+#define KSCD_TOPK_CAND 6144
+#endif
+constexpr int kRadixCandCap = KSCD_TOPK_CAND;
+
 struct TopkShared {
   uint32_t hist[4096];
   uint32_t range_tot[16];     // per-CTA bin-range totals (valid in CTA 0)
   uint32_t seg_cnt[16][2];    // per-CTA (gt, eq) counts (valid in CTA 0)
   uint32_t scan_buf[33];
   uint32_t sel_bin, sel_above;
+  uint32_t ncand;             // candidates appended by this CTA
+  uint32_t ovf[16];           // per-CTA candidate overflow flags (every CTA holds all)
+  uint32_t cand[kRadixCandCap];    // candidate keys (threshold bin of digit 0)
 };
 
 template <int CL, int AGG>
@@ -192,12 +203,26 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
   // ---- radix select of the take-th largest key -------------------------
   uint32_t prefix = 0, pmask = 0, remaining = (uint32_t)take;
   const int iters = (seg1 - seg0 + 4 * kTopkThreads - 1) / (4 * kTopkThreads);
+  // Candidate mode: after the first digit, the keys of its threshold bin
+  // are copied to shared memory in one more pass over the segment, and the
+  // two remaining digits and the (gt, eq) counts of the compaction run on
+  // that copy -- three passes over the row from L2 instead of five.
+  bool cand_mode = false;
+  uint32_t above_bin = 0;     // this CTA's keys above digit 0's threshold bin
+  if (tid == 0) sh.ncand = 0;
 #pragma unroll 1
   for (int pass = 0; pass < 3; ++pass) {
     const int shift = pass == 0 ? 20 : (pass == 1 ? 8 : 0);
     const int nb = pass == 2 ? 256 : 4096;
     for (int i = tid; i < nb; i += kTopkThreads) sh.hist[i] = 0;
     __syncthreads();
+    if (cand_mode) {
+      const int nc = (int)sh.ncand;
+      for (int i = tid; i < nc; i += kTopkThreads) {
+        const uint32_t key = sh.cand[i];
+        if ((key & pmask) == prefix) atomicAdd(&sh.hist[(key >> shift) & (nb - 1)], 1u);
+      }
+    } else
     // kTopkBatch float4 loads in flight per thread before any atomic: the
     // row streams from L2 and one outstanding load per thread leaves the
     // pass latency-bound (few CTAs per SM at decode shapes)
@@ -298,6 +323,49 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
     pmask |= (uint32_t)(nb - 1) << shift;
     remaining -= sh.sel_above;
     if (CL > 1) cluster.sync(); else __syncthreads();   // hist / sel reuse in the next pass
+    if (pass == 0) {
+      // copy the threshold bin's keys on chip and count the keys above it
+      const uint32_t hi_key = prefix | 0x000fffffu;
+      uint32_t ab = 0;
+#pragma unroll 1
+      for (int it0 = 0; it0 < iters; it0 += kTopkBatch) {
+        float v[kTopkBatch][4];
+        load_groups<kTopkBatch>(vals, vals2, seg0 + (it0 * kTopkThreads + tid) * 4, kTopkThreads * 4, seg1, vec, v);
+#pragma unroll
+        for (int b = 0; b < kTopkBatch; ++b) {
+          const int j = seg0 + ((it0 + b) * kTopkThreads + tid) * 4;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t key = order_key(v[b][i]);
+            const bool ok = j + i < seg1;
+            ab += ok && key > hi_key;
+            const bool isc = ok && (key & pmask) == prefix;
+            const uint32_t m = __ballot_sync(0xffffffffu, isc);
+            if (m) {
+              const int leader = __ffs(m) - 1;
+              uint32_t base = 0;
+              if (lane == leader) base = atomicAdd(&sh.ncand, (uint32_t)__popc(m));
+              base = __shfl_sync(0xffffffffu, base, leader);
+              const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
+              if (isc && pos < (uint32_t)kRadixCandCap) sh.cand[pos] = key;
+            }
+          }
+        }
+      }
+      uint32_t ab_tot;
+      block_excl_scan(ab, sh.scan_buf, ab_tot);    // (its barriers also publish ncand)
+      above_bin = ab_tot;
+      const uint32_t my_ovf = sh.ncand > (uint32_t)kRadixCandCap;
+      if (tid < CL) {
+        uint32_t* dst = CL > 1 ? cluster.map_shared_rank(sh.ovf, tid) : sh.ovf;
+        dst[c] = my_ovf;
+      }
+      if (CL > 1) cluster.sync(); else __syncthreads();
+      uint32_t any = 0;
+#pragma unroll
+      for (int q = 0; q < CL; ++q) any |= sh.ovf[q];
+      cand_mode = any == 0;
+    }
   }
   const uint32_t T = prefix;       // exact key of the take-th largest
   const uint32_t r_eq = remaining; // how many keys == T to keep (lowest indices)
@@ -305,6 +373,15 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
   // ---- ordered compaction ------------------------------------------------
   const int chunk = kTopkThreads * kTopkItems;
   uint32_t gt_seg = 0, eq_seg = 0;
+  if (cand_mode) {
+    const int nc = (int)sh.ncand;
+    for (int i = tid; i < nc; i += kTopkThreads) {
+      const uint32_t key = sh.cand[i];
+      gt_seg += key > T;
+      eq_seg += key == T;
+    }
+    if (tid == 0) gt_seg += above_bin;
+  } else
 #pragma unroll 1
   for (int base = seg0; base < seg1; base += kTopkThreads * 4 * kTopkBatch) {
     float v[kTopkBatch][4];
