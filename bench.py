@@ -746,6 +746,25 @@ def main():
     dense_ms_launch = float(np.mean([s.elapsed_time(e) for s, e in evs]))
     dense_bytes = B * Hkv * n * 512
 
+    # ---- per-layer-kind times (Table-3 layout) and the reference cost
+    # model's weighted pipeline time from them (SURVEY 8(d) cross-check)
+    per_kind = {}
+    for kind, l in (("anchor0", 0), ("reuse", reuse_layers[0]), ("anchor", LLAMA_ANCHORS[1])):
+        evs = []
+        for rep in range(3):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            dec._layer(l, q, Ks, Vs, n)
+            e.record()
+            evs.append((s, e))
+        torch.cuda.synchronize()
+        per_kind[kind] = float(np.median([s.elapsed_time(e) for s, e in evs]))
+    dec.step(q, Ks, Vs, n)   # restore the step's final state
+    from paper_2512_16391_b200 import costmodel
+    cm = costmodel.weighted_pipeline_time(
+        costmodel.CostParams(phase="decode", num_layers=L, num_anchors=len(LLAMA_ANCHORS), topk_fraction=args.fraction,
+                             seq_len=n, baseline_layer_time=dense_ms_launch), per_kind)
+
     # ---- end to end through the public API with host buffers ------------
     e2e = None
     if not args.no_e2e:
@@ -820,6 +839,11 @@ def main():
                    "l2": "inputs > L2 (each layer's KV is %.1f GB)" % (per_layer / 1e9),
                    "cuda_graph": True},
         "dense_us_per_token": round(ms_den * 1e3 / (B * world), 2),
+        "per_layer_ms": {"dense": round(dense_ms_launch, 4), **{k_: round(v, 4) for k_, v in per_kind.items()},
+                         "costmodel_weighted_us_per_token": round(cm.kascade_time * 1e3 * L / B, 2),
+                         "costmodel_speedup": round(cm.speedup, 3),
+                         "note": "one isolated launch sequence per layer kind; the cost model "
+                                 "(costmodel.weighted_pipeline_time) composes them to the 32-layer step"},
         "speedup_vs_dense": round(ms_den / ms_kas, 3),
         "paper_h100_us_per_token": 1415,
         "roofline": {"kernel": "kscd sparse_decode (reuse layer)", "bound": "hbm",
