@@ -88,6 +88,33 @@ def gather_index_lists(local_idx: torch.Tensor, local_cnt: torch.Tensor, group=N
     return cat(local_idx), cat(local_cnt)
 
 
+class PendingIndexGather:
+    """An index-list all-gather in flight (NCCL: on the communicator's
+    stream, ordered after the select that produced the lists).  ``wait()``
+    makes the current stream wait for it and returns (idx, cnt) in global
+    kv-head order, as gather_index_lists does."""
+
+    def __init__(self, local_idx, local_cnt, group=None, head_dim: int = 1):
+        self.head_dim = head_dim
+        self.works, self.outs, self.done = [], [], None
+        world, _ = _world(group)
+        if world == 1 or not local_idx.is_cuda or dist.get_backend(group) == "gloo":
+            self.done = gather_index_lists(local_idx, local_cnt, group, head_dim)   # staged / trivial: in place
+            return
+        for t in (local_idx, local_cnt):
+            src = t.movedim(head_dim, 0).contiguous()
+            out = torch.empty((world * src.shape[0],) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+            self.works.append(dist.all_gather_into_tensor(out, src, group=group, async_op=True))
+            self.outs.append(out)
+
+    def wait(self) -> Tuple[torch.Tensor, torch.Tensor]:
+        if self.done is None:
+            for w in self.works:
+                w.wait()
+            self.done = tuple(o.movedim(0, self.head_dim).contiguous() for o in self.outs)
+        return self.done
+
+
 def gather_head_outputs(local_out: torch.Tensor, group=None, head_dim: int = 1) -> torch.Tensor:
     """Reassemble head-sharded outputs (decode [B][Hq_loc][d], head_dim 1;
     prefill [Hq_loc][N][d], head_dim 0)."""
@@ -129,7 +156,6 @@ class ShardedKascadeDecoder:
         self.kinds = self.local.kinds
         self.maps = {l: local_head_map(plan.head_maps[l].map, self.g0, self.g1, dev)
                      for l, kind in enumerate(self.kinds) if kind == KIND_REUSE}
-        self.own = torch.arange(self.g0, self.g1, dtype=torch.int32, device=dev)
         kc = k_budget(plan.k_policy, max_seq_len)
         self.full_idx = torch.empty(batch, num_kv_heads, kc, dtype=torch.int32, device=dev)
         self.full_cnt = torch.zeros(batch, num_kv_heads, dtype=torch.int32, device=dev)
@@ -150,11 +176,14 @@ class ShardedKascadeDecoder:
                 ops.anchor_scores_decode(ql, kl, seq_len, loc.scores, loc.lse)
             ops.select_decode(loc.scores, loc.lse, seq_len, pol, self.Hloc, indices=loc.indices, counts=loc.counts,
                               pooled=loc.pooled)
-            idx, cnt = gather_index_lists(loc.indices, loc.counts, self.group, head_dim=1)
+            # the exchange overlaps the anchor's own sparse pass, which only
+            # needs this rank's lists
+            pending = PendingIndexGather(loc.indices, loc.counts, self.group, head_dim=1)
+            if kind == KIND_ANCHOR:
+                ops.sparse_decode(ql, kl, vl, seq_len, loc.indices, loc.counts, None, out=loc.out[l])
+            idx, cnt = pending.wait()
             self.full_idx[:, :, :idx.shape[2]].copy_(idx)
             self.full_cnt.copy_(cnt)
-            if kind == KIND_ANCHOR:
-                ops.sparse_decode(ql, kl, vl, seq_len, self.full_idx, self.full_cnt, self.own, out=loc.out[l])
         return loc.out
 
     def gather_outputs(self) -> torch.Tensor:
@@ -186,7 +215,6 @@ class ShardedKascadePrefill:
         self.kinds = self.local.kinds
         self.maps = {l: local_head_map(plan.head_maps[l].map, self.g0, self.g1, dev)
                      for l, kind in enumerate(self.kinds) if kind == KIND_REUSE}
-        self.own = torch.arange(self.g0, self.g1, dtype=torch.int32, device=dev)
         T = self.local.indices.shape[1]
         kc = k_budget(plan.k_policy, seq_len)
         self.full_idx = torch.empty(num_kv_heads, T, kc, dtype=torch.int32, device=dev)
@@ -209,9 +237,10 @@ class ShardedKascadePrefill:
             else:
                 ops.anchor_lse_prefill(q, k, lse=loc.lse)
             ops.select_prefill(q, k, loc.lse, pol, indices=loc.indices, counts=loc.counts, pooled=loc.pooled)
-            idx, cnt = gather_index_lists(loc.indices, loc.counts, self.group, head_dim=0)
+            pending = PendingIndexGather(loc.indices, loc.counts, self.group, head_dim=0)
+            if kind == KIND_ANCHOR:           # overlaps the exchange: own lists only
+                ops.sparse_prefill(q, k, v, loc.indices, loc.counts, None, out=loc.out[l])
+            idx, cnt = pending.wait()
             self.full_idx.copy_(idx)
             self.full_cnt.copy_(cnt)
-            if kind == KIND_ANCHOR:
-                ops.sparse_prefill(q, k, v, self.full_idx, self.full_cnt, self.own, out=loc.out[l])
         return loc.out

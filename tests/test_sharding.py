@@ -52,6 +52,13 @@ def _worker_exchange(rank, world, port, errq):
         idx, cnt = sharding.gather_index_lists(local_idx, local_cnt)
         assert torch.equal(idx, torch.from_numpy(full)), "gathered lists differ from the unsharded selection"
         assert torch.equal(cnt, torch.full((B, Hkv), k, dtype=torch.int32))
+        # the overlapped form the sharded executors use gives the same lists
+        # (prefill layout too: heads on dim 0)
+        pidx, pcnt = sharding.PendingIndexGather(local_idx, local_cnt, head_dim=1).wait()
+        assert torch.equal(pidx, idx) and torch.equal(pcnt, cnt)
+        tidx, tcnt = sharding.PendingIndexGather(local_idx.permute(1, 0, 2).contiguous(), local_cnt.t().contiguous(),
+                                                 head_dim=0).wait()
+        assert torch.equal(tidx, idx.permute(1, 0, 2)) and torch.equal(tcnt, cnt.t())
         # head-remap routing of this rank's reuse heads through the GLOBAL map
         head_map = [3, 0, 2, 1]
         lm = sharding.local_head_map(head_map, g0, g1)
