@@ -68,6 +68,7 @@ struct TopkArgs {
   int tile, T;
   double fraction;
   int k_min;
+  int cand_off;                           // 1: skip the on-chip candidate copy (dev knob KSCD_TOPK_NOCAND)
 };
 cudaError_t launch_topk(const TopkArgs& a, cudaStream_t st);
 

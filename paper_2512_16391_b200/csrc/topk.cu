@@ -159,7 +159,7 @@ struct TopkShared {
   uint32_t range_tot[16];     // per-CTA bin-range totals (valid in CTA 0)
   uint32_t seg_cnt[16][2];    // per-CTA (gt, eq) counts (valid in CTA 0)
   uint32_t scan_buf[33];
-  uint32_t sel_bin, sel_above;
+  uint32_t sel_bin, sel_above, sel_cnt;   // threshold bin, keys above it, keys in it (cluster-wide)
   uint32_t ncand;             // candidates appended by this CTA
   uint32_t ovf[16];           // per-CTA candidate overflow flags (every CTA holds all)
   uint32_t cand[kRadixCandCap];    // candidate keys (threshold bin of digit 0)
@@ -311,6 +311,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
                 TopkShared* dst = CL > 1 ? cluster.map_shared_rank(&sh, q) : &sh;
                 dst->sel_bin = (uint32_t)bin;
                 dst->sel_above = above;
+                dst->sel_cnt = cnts[i];
               }
             }
             above += cnts[i];
@@ -323,7 +324,10 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
     pmask |= (uint32_t)(nb - 1) << shift;
     remaining -= sh.sel_above;
     if (CL > 1) cluster.sync(); else __syncthreads();   // hist / sel reuse in the next pass
-    if (pass == 0) {
+    // only when the bin's cluster-wide count says the copy will (very
+    // likely) fit: long prefill rows of near-uniform attention put most of a
+    // row in one bin, and a wasted copy pass costs more than it saves
+    if (pass == 0 && !a.cand_off && sh.sel_cnt <= (uint32_t)(CL == 1 ? kRadixCandCap : kRadixCandCap * CL / 2)) {
       // copy the threshold bin's keys on chip and count the keys above it
       const uint32_t hi_key = prefix | 0x000fffffu;
       uint32_t ab = 0;
@@ -709,8 +713,11 @@ static cudaError_t launch_topk_cl(const TopkArgs& a, cudaStream_t st) {
   return cudaLaunchKernelEx(&cfg, topk_kernel<CL, AGG>, a);
 }
 
-cudaError_t launch_topk(const TopkArgs& a, cudaStream_t st) {
-  if (a.rows <= 0) return cudaSuccess;
+cudaError_t launch_topk(const TopkArgs& a_in, cudaStream_t st) {
+  if (a_in.rows <= 0) return cudaSuccess;
+  static const bool nocand = getenv("KSCD_TOPK_NOCAND") != nullptr;
+  TopkArgs a = a_in;
+  a.cand_off = nocand ? 1 : 0;
   // KSCD_TOPK_VARIANT (dev knob): <cluster><agg>, e.g. "80", "81", "10", "11"
   static const char* forced = getenv("KSCD_TOPK_VARIANT");
   int cl = 1, agg = 0;
