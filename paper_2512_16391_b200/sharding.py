@@ -96,7 +96,7 @@ class PendingIndexGather:
 
     def __init__(self, local_idx, local_cnt, group=None, head_dim: int = 1):
         self.head_dim = head_dim
-        self.works, self.outs, self.done = [], [], None
+        self.works, self.outs, self.srcs, self.done = [], [], [], None
         world, _ = _world(group)
         if world == 1 or not local_idx.is_cuda or dist.get_backend(group) == "gloo":
             self.done = gather_index_lists(local_idx, local_cnt, group, head_dim)   # staged / trivial: in place
@@ -106,12 +106,14 @@ class PendingIndexGather:
             out = torch.empty((world * src.shape[0],) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
             self.works.append(dist.all_gather_into_tensor(out, src, group=group, async_op=True))
             self.outs.append(out)
+            self.srcs.append(src)          # alive until wait(): the collective reads it asynchronously
 
     def wait(self) -> Tuple[torch.Tensor, torch.Tensor]:
         if self.done is None:
             for w in self.works:
                 w.wait()
             self.done = tuple(o.movedim(0, self.head_dim).contiguous() for o in self.outs)
+            self.srcs = []
         return self.done
 
 
