@@ -37,7 +37,16 @@ def main():
         e.record()
         torch.cuda.synchronize()
         us = s.elapsed_time(e) / reps * 1e3
-        res.append(f"splits={sp}:{us:.1f}us({B * Hkv * k * 516 / us / 1e3:.0f}GB/s,err={err:.1e})")
+        iso = []
+        for i in range(20):   # isolated launches, events around each (as bench.py's roofline)
+            s1, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s1.record()
+            ops.sparse_decode(q, ks[i % L], vs[i % L], n, idx, cnt, None, out=out, num_splits=sp)
+            e1.record()
+            iso.append((s1, e1))
+        torch.cuda.synchronize()
+        iso_us = sum(a.elapsed_time(b) for a, b in iso) / len(iso) * 1e3
+        res.append(f"splits={sp}:chain {us:.1f}us iso {iso_us:.1f}us (err={err:.1e})")
     print(f"stages={os.environ.get('KSCD_SPARSE_STAGES', '3')}", " ".join(res))
 
 
