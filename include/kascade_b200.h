@@ -53,7 +53,7 @@ extern "C" {
  * decode tile [t, t+1) with causal bound n = t + 1, tiles.py:145-150). */
 typedef struct kscd_decode_params {
   int32_t batch;          /* B */
-  int32_t num_q_heads;    /* Hq; query head h reads kv head h / (Hq/Hkv), trace.py:38-43 */
+  int32_t num_q_heads;    /* Hq; query head h reads kv head h / (Hq/Hkv), trace.py:38-43; any group size */
   int32_t num_kv_heads;   /* Hkv */
   int32_t head_dim;       /* 1..128, see Conventions */
   int32_t seq_len;        /* n: keys 0..n-1 are visible (the step's own token included) */

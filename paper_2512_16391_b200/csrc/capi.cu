@@ -71,11 +71,21 @@ int plan_splits(int pairs, int keys, int requested) {
   return std::max(1, std::min(best, std::max(tiles, 1)));
 }
 
+// Virtual kv heads per kv head for a query group of G heads: the smallest
+// divisor r of G with G / r <= 16 (the decode kernel's m16 tile).
+int kv_rep_for(int G) {
+  for (int r = 1; r <= G; ++r)
+    if (G % r == 0 && G / r <= 16) return r;
+  return G;
+}
+
 size_t decode_ws_bytes(const kscd_decode_params* p) {
+  const int G = p->num_kv_heads > 0 ? p->num_q_heads / p->num_kv_heads : 1;
+  const int pairs = p->batch * p->num_kv_heads * kv_rep_for(std::max(G, 1));
   const size_t bh = (size_t)p->batch * p->num_q_heads;
-  size_t bytes = bh * max_splits_for(p->batch * p->num_kv_heads) * (kscd::kHeadDimC + 2) * sizeof(float);
+  size_t bytes = bh * max_splits_for(pairs) * (kscd::kHeadDimC + 2) * sizeof(float);
   bytes = (bytes + 255) & ~(size_t)255;
-  bytes += (size_t)p->batch * p->num_kv_heads * sizeof(int);
+  bytes += (size_t)pairs * sizeof(int);
   return bytes;
 }
 
@@ -87,8 +97,6 @@ int check_decode(const kscd_decode_params* p, bool need_v, bool sparse) {
   if (p->num_q_heads % p->num_kv_heads)
     return fail(KSCD_INVALID_ARGUMENT, "num_query_heads (%d) must be divisible by num_kv_heads (%d)",
                 p->num_q_heads, p->num_kv_heads);
-  const int G = p->num_q_heads / p->num_kv_heads;
-  if (G > 16) return fail(KSCD_UNSUPPORTED, "group size %d > 16 unsupported", G);
   if (p->seq_len < 1) return fail(KSCD_INVALID_ARGUMENT, "seq_len must be >= 1");
   if (!p->q || !p->k_cache || (need_v && !p->v_cache))
     return fail(KSCD_INVALID_ARGUMENT, "q/k_cache/v_cache must be non-NULL");
@@ -116,8 +124,9 @@ kscd::DecodeArgs make_args(const kscd_decode_params* p, int keys) {
   kscd::DecodeArgs a{};
   a.B = p->batch;
   a.Hq = p->num_q_heads;
-  a.Hkv = p->num_kv_heads;
-  a.G = p->num_q_heads / p->num_kv_heads;
+  a.kv_rep = kv_rep_for(p->num_q_heads / p->num_kv_heads);
+  a.Hkv = p->num_kv_heads * a.kv_rep;                // virtual heads (kscd_internal.h)
+  a.G = p->num_q_heads / a.Hkv;
   a.n = p->seq_len;
   a.q = (const __nv_bfloat16*)p->q;
   a.k = (const __nv_bfloat16*)p->k_cache;

@@ -49,13 +49,14 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
     decode_attn_kernel(const DecodeArgs a) {
   using Cfg = DecodeCfg<MODE, STG>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
+  const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;   // g: (virtual) head group
+  const int gk = g / a.kv_rep;                                        // its kv head
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int G = a.G;
 
-  const __nv_bfloat16* kbase = a.k + (int64_t)b * a.kv_sb + (int64_t)g * a.kv_sh;
-  const __nv_bfloat16* vbase = a.v + (int64_t)b * a.kv_sb + (int64_t)g * a.kv_sh;
+  const __nv_bfloat16* kbase = a.k + (int64_t)b * a.kv_sb + (int64_t)gk * a.kv_sh;
+  const __nv_bfloat16* vbase = a.v + (int64_t)b * a.kv_sb + (int64_t)gk * a.kv_sh;
   const int* sel = nullptr;
   // Programmatic dependent launch (consecutive decode layers): let the next
   // layer's kernel start filling SMs as ours retire.  Our inputs are all
@@ -68,7 +69,7 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   int count = a.n;
   if (MODE == MODE_SPARSE) {
-    const int src = a.head_map ? __ldg(a.head_map + g) : g;
+    const int src = a.head_map ? __ldg(a.head_map + gk) : gk;
     sel = a.idx + (int64_t)b * a.idx_sb + (int64_t)src * a.idx_sh;
     count = min(__ldg(a.cnt + (int64_t)b * a.cnt_sb + src), a.k_cap);
   }

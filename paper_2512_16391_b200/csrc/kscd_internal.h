@@ -32,6 +32,10 @@ struct DecodeArgs {
   float* part_ml;                         // [B][Hq][splits][2]
   int* counters;                          // [B][Hkv], zero at allocation, self re-arming
   int splits;
+  // groups of more than 16 query heads run as kv_rep "virtual" kv heads of
+  // G = Hq / (Hkv * kv_rep) query heads each; Hkv and G above are the
+  // virtual ones, and virtual head gv reads kv head gv / kv_rep
+  int kv_rep;
 };
 
 cudaError_t launch_decode_attn(int mode, const DecodeArgs& a, cudaStream_t st);

@@ -1,5 +1,5 @@
 """Head-group shapes beyond the bench's GQA-4: MHA (G = 1), odd groups
-(G = 3), G = 8 and G = 16 through the decode and prefill executors, against
+(G = 3), G = 8, 16, 24 and 32 (MQA-style) through the decode and prefill executors, against
 the oracle (decode_step / run_kascade) on the same bf16 inputs, with
 non-identity head maps and ragged lengths.  Needs a B200."""
 import numpy as np
@@ -11,7 +11,9 @@ from parity import assert_outputs_close
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
-SHAPES = [(2, 2), (6, 2), (8, 1), (16, 1), (12, 4)]
+# G = 24 and 32 exceed the decode kernel's 16-row MMA tile and run as 2
+# virtual kv heads per kv head (kscd_internal.h DecodeArgs.kv_rep)
+SHAPES = [(2, 2), (6, 2), (8, 1), (16, 1), (12, 4), (32, 1), (48, 2)]
 
 
 def _maps(Hkv):
