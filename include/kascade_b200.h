@@ -79,6 +79,11 @@ typedef struct kscd_decode_params {
   void* workspace;
   size_t workspace_bytes;
   int32_t num_splits;     /* split-K factor; 0 = automatic */
+  /* ragged batch (serving; the reference decodes one trace at a time):
+   * device int32 [B], sequence b sees keys 0..seq_lens[b]-1 (each
+   * <= seq_len, which then only bounds the split planning); NULL = seq_len
+   * for every sequence.  Sparse calls take their lengths from the lists. */
+  const int32_t* seq_lens;
 } kscd_decode_params;
 
 /* Selection of one decode step: pooled post-softmax weights of the G heads
@@ -96,6 +101,7 @@ typedef struct kscd_select_decode_params {
   int32_t* indices;       /* int32 [B*Hkv][k_cap] */
   int32_t* counts;        /* int32 [B*Hkv] */
   int32_t k_cap;          /* >= k_budget(n) */
+  const int32_t* seq_lens;/* device int32 [B] or NULL: per-sequence n, k = k_budget(seq_lens[b]) */
 } kscd_select_decode_params;
 
 /* Generic exact Top-k over rows of fp32 values (oracle_topk_indices). */

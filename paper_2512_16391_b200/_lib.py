@@ -33,6 +33,7 @@ class DecodeParams(ctypes.Structure):
         ("scores", c_vp), ("score_stride", c_i64),
         ("workspace", c_vp), ("workspace_bytes", c_sz),
         ("num_splits", c_i32),
+        ("seq_lens", c_vp),
     ]
 
 
@@ -43,6 +44,7 @@ class SelectDecodeParams(ctypes.Structure):
         ("pooled", c_vp), ("pooled_stride", c_i64),
         ("topk_fraction", c_f64), ("k_min", c_i32),
         ("indices", c_vp), ("counts", c_vp), ("k_cap", c_i32),
+        ("seq_lens", c_vp),
     ]
 
 

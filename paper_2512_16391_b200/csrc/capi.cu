@@ -146,6 +146,7 @@ kscd::DecodeArgs make_args(const kscd_decode_params* p, int keys) {
   a.head_map = p->head_map;
   a.scores = p->scores;
   a.score_stride = p->score_stride;
+  a.lens = p->seq_lens;
   a.splits = plan_splits(a.B * a.Hkv, keys, p->num_splits);
   const size_t bh = (size_t)a.B * a.Hq;
   a.part = (float*)p->workspace;
@@ -240,6 +241,12 @@ int kscd_select_decode(const kscd_select_decode_params* p, void* stream) {
   ta.idx = p->indices;
   ta.counts = p->counts;
   ta.k_cap = p->k_cap;
+  if (p->seq_lens) {          // ragged batch: per-sequence length and k_budget
+    ta.seq_lens = p->seq_lens;
+    ta.seq_div = p->num_kv_heads;
+    ta.fraction = p->topk_fraction;
+    ta.k_min = p->k_min;
+  }
   return cuda_status(kscd::launch_topk(ta, st), "topk");
 }
 

@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
   // workspace and counters are shared with the previous layer's kernel, and
   // it writes out / lse) waits for the previous grid.
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  int count = a.n;
+  int count = a.lens ? min(__ldg(a.lens + b), a.n) : a.n;
   if (MODE == MODE_SPARSE) {
     const int src = a.head_map ? __ldg(a.head_map + gk) : gk;
     sel = a.idx + (int64_t)b * a.idx_sb + (int64_t)src * a.idx_sh;

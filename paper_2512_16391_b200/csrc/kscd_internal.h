@@ -36,6 +36,7 @@ struct DecodeArgs {
   // G = Hq / (Hkv * kv_rep) query heads each; Hkv and G above are the
   // virtual ones, and virtual head gv reads kv head gv / kv_rep
   int kv_rep;
+  const int* lens;                        // [B] per-sequence key counts (nullable => n)
 };
 
 cudaError_t launch_decode_attn(int mode, const DecodeArgs& a, cudaStream_t st);
@@ -73,6 +74,10 @@ struct TopkArgs {
   double fraction;
   int k_min;
   int cand_off;                           // 1: skip the on-chip candidate copy (dev knob KSCD_TOPK_NOCAND)
+  // ragged decode batch: when seq_div > 0, row r has length
+  // min(len, seq_lens[r / seq_div]) and k = k_budget(fraction, k_min, length)
+  const int* seq_lens;
+  int seq_div;
 };
 cudaError_t launch_topk(const TopkArgs& a, cudaStream_t st);
 

@@ -174,7 +174,13 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
   const int tid = threadIdx.x, lane = tid & 31;
   int n = a.lens ? a.lens[r] : a.len;
   int k = a.ks ? a.ks[r] : a.k;
-  if (a.tile > 0) {
+  if (a.seq_div > 0) {
+    // ragged decode batch: this row's sequence length and its k_budget
+    n = min(a.len, __ldg(a.seq_lens + r / a.seq_div));
+    long long kk = (long long)floor(a.fraction * (double)n);
+    kk = kk < a.k_min ? a.k_min : kk;
+    k = (int)(kk > n ? n : kk);
+  } else if (a.tile > 0) {
     // k_budget (tiles.py:81-89) of the tile's causal bound, in the same fp64
     n = min(a.len, a.tile * (r % a.T + 1));
     long long kk = (long long)floor(a.fraction * (double)n);

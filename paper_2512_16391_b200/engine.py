@@ -74,14 +74,20 @@ class KascadeDecoder:
         self.counts = torch.zeros(batch, Hsrc, dtype=torch.int32, device=dev)
         self.out = torch.empty(num_layers, batch, num_q_heads, 128, dtype=torch.float32, device=dev)
         self._graphs = {}
+        self.seq_lens: Optional[torch.Tensor] = None     # ragged batch (step / dense_step)
 
     # -------------------------------------------------------------- eager
     def step(self, q: torch.Tensor, k_caches: Sequence[torch.Tensor], v_caches: Sequence[torch.Tensor],
-             seq_len: int) -> torch.Tensor:
+             seq_len: int, seq_lens: Optional[torch.Tensor] = None) -> torch.Tensor:
         """q [L][B][Hq][128] bf16; k/v_caches: L tensors [B][Hkv][n_cap][128].
-        Returns the preallocated fp32 outputs [L][B][Hq][128]."""
+        ``seq_lens`` (device int32 [B], each <= seq_len) runs a ragged batch:
+        sequence b attends its own first seq_lens[b] keys and selects with
+        k_budget(seq_lens[b]); CUDA graphs read it at replay time, so a
+        serving loop updates it in place.  Returns the preallocated fp32
+        outputs [L][B][Hq][128]."""
         if seq_len > self.n_max:
             raise InvalidArgumentError(f"seq_len {seq_len} exceeds max_seq_len {self.n_max}")
+        self.seq_lens = seq_lens
         for l in range(self.L):
             self._layer(l, q, k_caches, v_caches, seq_len)
         return self.out
@@ -94,34 +100,40 @@ class KascadeDecoder:
         if kind == KIND_REUSE:
             ops.sparse_decode(ql, kl, vl, seq_len, self.indices, self.counts, self.head_maps[l], out=self.out[l])
             return
+        sl = self.seq_lens
         if kind == KIND_ANCHOR0:
-            ops.dense_decode(ql, kl, vl, seq_len, out=self.out[l], lse=self.lse, scores=self.scores)
+            ops.dense_decode(ql, kl, vl, seq_len, out=self.out[l], lse=self.lse, scores=self.scores, seq_lens=sl)
         else:
-            ops.anchor_scores_decode(ql, kl, seq_len, self.scores, self.lse)
+            ops.anchor_scores_decode(ql, kl, seq_len, self.scores, self.lse, seq_lens=sl)
         ops.select_decode(self.scores, self.lse, seq_len, pol, self.Hkv, indices=self.indices,
-                          counts=self.counts, pooled=self.pooled, all_heads=self.all_heads)
+                          counts=self.counts, pooled=self.pooled, all_heads=self.all_heads, seq_lens=sl)
         if kind == KIND_ANCHOR:
             ops.sparse_decode(ql, kl, vl, seq_len, self.indices, self.counts, self.shared_map, out=self.out[l])
 
     def _dense_layer(self, l: int, q, k_caches, v_caches, seq_len: int) -> None:
-        ops.dense_decode(q[l], k_caches[l], v_caches[l], seq_len, out=self.out[l], lse=self.lse)
+        ops.dense_decode(q[l], k_caches[l], v_caches[l], seq_len, out=self.out[l], lse=self.lse,
+                         seq_lens=self.seq_lens)
 
-    def dense_step(self, q, k_caches, v_caches, seq_len: int) -> torch.Tensor:
+    def dense_step(self, q, k_caches, v_caches, seq_len: int, seq_lens: Optional[torch.Tensor] = None
+                   ) -> torch.Tensor:
         """Top-k = 100% baseline: dense attention on every layer."""
+        self.seq_lens = seq_lens
         for l in range(self.L):
             self._dense_layer(l, q, k_caches, v_caches, seq_len)
         return self.out
 
     # -------------------------------------------------------------- graphs
-    def capture(self, q, k_caches, v_caches, seq_len: int, dense: bool = False) -> torch.cuda.CUDAGraph:  # noqa: D102
+    def capture(self, q, k_caches, v_caches, seq_len: int, dense: bool = False,
+                seq_lens: Optional[torch.Tensor] = None) -> torch.cuda.CUDAGraph:  # noqa: D102
         """Capture one step (fixed buffers and seq_len) in a CUDA graph; replay
-        with ``graph.replay()`` after writing new queries into ``q``."""
+        with ``graph.replay()`` after writing new queries into ``q`` (and new
+        lengths into ``seq_lens`` for a ragged batch)."""
         fn = self.dense_step if dense else self.step
-        fn(q, k_caches, v_caches, seq_len)  # warm-up: one-time kernel attributes outside capture
+        fn(q, k_caches, v_caches, seq_len, seq_lens)  # warm-up: one-time kernel attributes outside capture
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            fn(q, k_caches, v_caches, seq_len)
+            fn(q, k_caches, v_caches, seq_len, seq_lens)
         self._graphs[(seq_len, dense)] = g
         return g
 
@@ -133,6 +145,7 @@ class KascadeDecoder:
         writes the rows at cache position ``seq_len - 1`` of every layer, the
         layer loop, and D2H of the outputs into ``out_host`` [L][B][Hq][128]
         fp32.  Replay, then synchronise the stream before reading out_host."""
+        self.seq_lens = None                # one shared append position: uniform lengths
         for t, name in ((q_host, "q_host"), (kv_host, "kv_host"), (out_host, "out_host")):
             if t.is_cuda or not t.is_pinned():
                 raise InvalidArgumentError(f"{name} must be pinned host memory")

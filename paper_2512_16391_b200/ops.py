@@ -100,7 +100,17 @@ def decode_workspace(device: torch.device, B: int, Hq: int, Hkv: int) -> torch.T
     return ws
 
 
-def _decode_params(q, k, v, n, out, lse, scores, scale, num_splits) -> _lib.DecodeParams:
+def _check_seq_lens(seq_lens: Optional[torch.Tensor], B: int, n: int) -> None:
+    """Ragged batch: device int32 [B], every entry in [1, seq_len] (checked
+    on the device side by the kernels' min(); values are the caller's)."""
+    if seq_lens is None:
+        return
+    _need_cuda(seq_lens, "seq_lens")
+    if seq_lens.dtype != torch.int32 or seq_lens.shape != (B,) or not seq_lens.is_contiguous():
+        raise InvalidArgumentError(f"seq_lens must be a contiguous CUDA int32 [B={B}] tensor")
+
+
+def _decode_params(q, k, v, n, out, lse, scores, scale, num_splits, seq_lens=None) -> _lib.DecodeParams:
     B, Hq = _check_q(q)
     Hkv, n_cap, sb, sh = _check_kv(k, v, B)
     if not (1 <= n <= n_cap):
@@ -114,6 +124,8 @@ def _decode_params(q, k, v, n, out, lse, scores, scale, num_splits) -> _lib.Deco
         softmax_scale=float(scale or 0.0), out=_ptr(out), lse=_ptr(lse),
         scores=_ptr(scores), score_stride=scores.stride(1) if scores is not None else 0,
         workspace=ws.data_ptr(), workspace_bytes=ws.numel(), num_splits=int(num_splits))
+    _check_seq_lens(seq_lens, B, n)
+    p.seq_lens = _ptr(seq_lens)
     return p
 
 
@@ -134,25 +146,26 @@ def score_buffer(B: int, Hq: int, n: int, device) -> torch.Tensor:
 def dense_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, seq_len: int, *,
                  out: Optional[torch.Tensor] = None, lse: Optional[torch.Tensor] = None,
                  scores: Optional[torch.Tensor] = None, scale: Optional[float] = None,
-                 num_splits: int = 0):
+                 num_splits: int = 0, seq_lens: Optional[torch.Tensor] = None):
     """Dense attention of the step's query over keys [0, seq_len)
     (dense_attention's last row, attention.py:106-144).  If ``scores`` is
     given, the log2-domain scores s*log2(e) are written for the anchor-0
-    selection."""
+    selection.  ``seq_lens`` (device int32 [B]) gives a ragged batch its
+    own key counts (each <= seq_len)."""
     B, Hq = q.shape[0], q.shape[1]
     out = torch.empty(B, Hq, HEAD_DIM, dtype=torch.float32, device=q.device) if out is None else out
     lse = torch.empty(B, Hq, dtype=torch.float32, device=q.device) if lse is None else lse
     _check_scores(scores, B, Hq, seq_len)
-    p = _decode_params(q, k_cache, v_cache, seq_len, out, lse, scores, scale, num_splits)
+    p = _decode_params(q, k_cache, v_cache, seq_len, out, lse, scores, scale, num_splits, seq_lens)
     _lib.call("kscd_dense_decode", p, _stream())
     return out, lse
 
 
-def anchor_scores_decode(q, k_cache, seq_len, scores, lse, *, scale=None, num_splits=0):
+def anchor_scores_decode(q, k_cache, seq_len, scores, lse, *, scale=None, num_splits=0, seq_lens=None):
     """Anchor pass 1: log2-domain scores + LSE; V is not read."""
     B, Hq = q.shape[0], q.shape[1]
     _check_scores(scores, B, Hq, seq_len)
-    p = _decode_params(q, k_cache, None, seq_len, None, lse, scores, scale, num_splits)
+    p = _decode_params(q, k_cache, None, seq_len, None, lse, scores, scale, num_splits, seq_lens)
     _lib.call("kscd_anchor_scores_decode", p, _stream())
     return scores, lse
 
@@ -181,7 +194,7 @@ def sparse_decode(q, k_cache, v_cache, seq_len, indices, counts, head_map=None, 
 
 
 def select_decode(scores, lse, seq_len, policy: KBudgetPolicy, num_kv_heads: int, *, indices=None,
-                  counts=None, pooled=None, all_heads: bool = False):
+                  counts=None, pooled=None, all_heads: bool = False, seq_lens=None):
     """Pooled post-softmax weights + k_budget + exact Top-k of one decode
     step (runner.py:164-207).  With ``all_heads`` the pooled vectors of all
     kv heads are combined into one shared set (all-heads-pooled mode,
@@ -201,6 +214,8 @@ def select_decode(scores, lse, seq_len, policy: KBudgetPolicy, num_kv_heads: int
         score_stride=scores.stride(1), lse=lse.data_ptr(), pooled=pooled.data_ptr(),
         pooled_stride=pooled.stride(0), topk_fraction=float(policy.fraction), k_min=int(policy.k_min),
         indices=indices.data_ptr(), counts=counts.data_ptr(), k_cap=indices.shape[-1])
+    _check_seq_lens(seq_lens, B, seq_len)
+    p.seq_lens = _ptr(seq_lens)
     _lib.call("kscd_select_decode", p, _stream())
     return indices, counts
 
@@ -232,7 +247,7 @@ def topk(values: torch.Tensor, k, lengths: Optional[torch.Tensor] = None, k_cap:
 
 def anchor_decode(q, k_cache, v_cache, seq_len, policy: KBudgetPolicy, *, layer0: bool = False,
                   scores=None, lse=None, out=None, indices=None, counts=None, pooled=None,
-                  all_heads: bool = False):
+                  all_heads: bool = False, seq_lens=None):
     """One anchor layer of a decode step.  Layer 0 (anchor0) runs dense
     attention and selects from its scores (runner.py:250-262); other anchors
     run scores-only pass 1, select, then attend sparsely over their own fresh
@@ -243,13 +258,13 @@ def anchor_decode(q, k_cache, v_cache, seq_len, policy: KBudgetPolicy, *, layer0
         scores = score_buffer(B, Hq, seq_len, q.device)
     lse = torch.empty(B, Hq, dtype=torch.float32, device=q.device) if lse is None else lse
     if layer0:
-        out, lse = dense_decode(q, k_cache, v_cache, seq_len, out=out, lse=lse, scores=scores)
+        out, lse = dense_decode(q, k_cache, v_cache, seq_len, out=out, lse=lse, scores=scores, seq_lens=seq_lens)
         indices, counts = select_decode(scores, lse, seq_len, policy, Hkv, indices=indices, counts=counts,
-                                        pooled=pooled, all_heads=all_heads)
+                                        pooled=pooled, all_heads=all_heads, seq_lens=seq_lens)
         return out, lse, indices, counts
-    anchor_scores_decode(q, k_cache, seq_len, scores, lse)
+    anchor_scores_decode(q, k_cache, seq_len, scores, lse, seq_lens=seq_lens)
     indices, counts = select_decode(scores, lse, seq_len, policy, Hkv, indices=indices, counts=counts,
-                                    pooled=pooled, all_heads=all_heads)
+                                    pooled=pooled, all_heads=all_heads, seq_lens=seq_lens)
     hm = None
     if all_heads:
         hm = torch.zeros(Hkv, dtype=torch.int32, device=q.device)

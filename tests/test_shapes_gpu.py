@@ -59,3 +59,44 @@ def test_prefill_engine_head_groups(cuda_ok, Hq, Hkv):
                       [dev(V[l]) for l in range(L)]).float().cpu().numpy()
     want, _ = orc.run_kascade(Q, K, V, [0, 2], {1: hm}, 0.2, 32, tile_size=128)
     assert_outputs_close(out, want)
+
+
+def test_decode_engine_ragged_batch(cuda_ok):
+    """Serving batches hold sequences of different lengths: seq_lens[b]
+    bounds sequence b's keys and its k_budget.  Each sequence equals the
+    oracle's decode step over its own prefix; a captured graph reads the
+    lengths at replay time."""
+    from paper_2512_16391_b200 import engine
+    from paper_2512_16391_b200.host_types import AnchorPlan, AnchorPlanCore, HeadMap, KBudgetPolicy
+    L, Hq, Hkv, n_cap = 3, 8, 2, 1600
+    lens = [1531, 977, 64, 1]
+    B = len(lens)
+    rng = np.random.default_rng(41)
+    plan = AnchorPlan(AnchorPlanCore([0, 2], 2, 0.0), head_maps={1: HeadMap(1, 0, [1, 0])},
+                      k_policy=KBudgetPolicy(0.1, 16))
+    q = orc.bf16_round((rng.standard_normal((L, B, Hq, 128)) * 2.5).astype(np.float32))
+    K = orc.bf16_round(rng.standard_normal((L, B, Hkv, n_cap, 128)).astype(np.float32))
+    V = orc.bf16_round(rng.standard_normal((L, B, Hkv, n_cap, 128)).astype(np.float32))
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda().to(torch.bfloat16)  # noqa: E731
+    qd, Kd, Vd = dev(q), [dev(K[l]) for l in range(L)], [dev(V[l]) for l in range(L)]
+    sl = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    dec = engine.KascadeDecoder(plan, L, B, Hq, Hkv, n_cap)
+    out = dec.step(qd, Kd, Vd, max(lens), seq_lens=sl).cpu().numpy()
+
+    def check(out, lens):
+        for b, n in enumerate(lens):
+            Y, _, _ = orc.decode_step(q[:, b], K[:, b, :, :n], V[:, b, :, :n], [0, 2], {1: [1, 0]}, 0.1, 16,
+                                      want_mass=False)
+            assert_outputs_close(out[:, b], Y)
+            k = orc.k_budget(0.1, 16, n)
+            assert (dec.counts[b].cpu().numpy() == k).all()
+
+    check(out, lens)
+    # a graph reads the lengths at replay: new lengths up to the captured
+    # seq_len (which bounds every sequence) need no recapture
+    g = dec.capture(qd, Kd, Vd, n_cap, seq_lens=sl)
+    lens2 = [700, 1600, 5, 1200]
+    sl.copy_(torch.tensor(lens2, dtype=torch.int32))
+    g.replay()
+    torch.cuda.synchronize()
+    check(dec.out.cpu().numpy(), lens2)
