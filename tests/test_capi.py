@@ -71,3 +71,61 @@ def test_workspace_size_query(lib):
     nb = ctypes.c_size_t(0)
     assert lib.kscd_decode_workspace_size(ctypes.byref(p), ctypes.byref(nb)) == 0
     assert nb.value >= 8 * 32 * 130 * 4
+
+
+STRUCTS = {"kscd_decode_params": "DecodeParams", "kscd_select_decode_params": "SelectDecodeParams",
+           "kscd_topk_params": "TopkParams", "kscd_prefill_params": "PrefillParams",
+           "kscd_select_prefill_params": "SelectPrefillParams", "kscd_probs_params": "ProbsParams",
+           "kscd_pool_tiles_params": "PoolTilesParams", "kscd_append_kv_params": "AppendKvParams",
+           "kscd_masked_mass_params": "MaskedMassParams"}
+
+
+def _header_fields():
+    """Member names of every params struct, in declaration order."""
+    text = re.sub(r"/\*.*?\*/", "", open(HEADER).read(), flags=re.S)
+    out = {}
+    for name, body in re.findall(r"typedef struct (kscd_\w+)\s*\{(.*?)\}\s*\1\s*;", text, re.S):
+        fields = []
+        for decl in body.split(";"):
+            decl = decl.strip()
+            if not decl:
+                continue
+            head, *rest = decl.split(",")
+            fields.append(re.findall(r"(\w+)\s*$", head)[0])
+            fields.extend(r.strip().lstrip("*").strip() for r in rest)
+        out[name] = fields
+    return out
+
+
+def test_ctypes_structs_match_the_header_layout(tmp_path):
+    """Every params struct of the C ABI: the ctypes binding declares the same
+    members in the same order at the same byte offsets, with the same size,
+    as gcc lays out include/kascade_b200.h."""
+    import shutil
+    import subprocess
+    from paper_2512_16391_b200 import _lib
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    fields = _header_fields()
+    assert set(fields) == set(STRUCTS), sorted(fields)
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "kascade_b200.h"', "int main(void) {"]
+    for cname, members in fields.items():
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for m in members:
+            lines.append(f'  printf("{cname} {m} %zu\\n", offsetof({cname}, {m}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(REPO, "include"), str(src), "-o", str(exe)], check=True)
+    c_layout = {}
+    for line in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines():
+        struct, member, value = line.split()
+        c_layout[(struct, member)] = int(value)
+    for cname, pyname in STRUCTS.items():
+        cls = getattr(_lib, pyname)
+        names = [f[0] for f in cls._fields_]
+        assert names == fields[cname], (cname, names, fields[cname])
+        assert ctypes.sizeof(cls) == c_layout[(cname, "size")], cname
+        for m in names:
+            assert getattr(cls, m).offset == c_layout[(cname, m)], (cname, m)
