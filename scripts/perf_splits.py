@@ -1,5 +1,5 @@
 """Decode kernels (dense, scores, sparse) vs split-K factor, isolated and
-chained launches (dev tool).  python scripts/perf_splits.py B n [splits ...]"""
+chained launches (dev tool).  HQ=32 HKV=8 python scripts/perf_splits.py B n [splits ...]"""
 import os
 import sys
 
@@ -35,7 +35,7 @@ def timed(fn, L):
 def main():
     B, n = int(sys.argv[1]), int(sys.argv[2])
     splits = [int(x) for x in sys.argv[3:]] or [0]
-    Hq, Hkv = 32, 8
+    Hq, Hkv = int(os.environ.get("HQ", 32)), int(os.environ.get("HKV", 8))
     L = max(2, min(6, int(50e9 // (2 * B * Hkv * n * 256))))
     g = torch.Generator(device="cuda").manual_seed(0)
     q = (torch.randn(B, Hq, 128, device="cuda", generator=g) * 2).to(torch.bfloat16)
