@@ -198,6 +198,8 @@ typedef struct kscd_append_kv_params {
   void* const* k_caches;        /* device array of L pointers, bf16 [B][Hkv][n_cap][128] */
   void* const* v_caches;
   int64_t kv_stride_batch, kv_stride_head;   /* elements, shared by every layer's cache */
+  const int32_t* seq_lens;      /* device int32 [B] or NULL: ragged batch, sequence b's row goes to
+                                   seq_lens[b] - 1 (position is then ignored) */
 } kscd_append_kv_params;
 
 int kscd_abi_version(void);

@@ -102,6 +102,7 @@ class AppendKvParams(ctypes.Structure):
         ("num_layers", c_i32), ("batch", c_i32), ("num_kv_heads", c_i32), ("head_dim", c_i32),
         ("position", c_i32), ("kv_new", c_vp), ("k_caches", c_vp), ("v_caches", c_vp),
         ("kv_stride_batch", c_i64), ("kv_stride_head", c_i64),
+        ("seq_lens", c_vp),
     ]
 
 

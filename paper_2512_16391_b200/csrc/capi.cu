@@ -480,6 +480,7 @@ extern "C" int kscd_append_kv(const kscd_append_kv_params* p, void* stream) {
   a.v_caches = (__nv_bfloat16* const*)p->v_caches;
   a.stride_b = p->kv_stride_batch;
   a.stride_h = p->kv_stride_head;
+  a.lens = p->seq_lens;
   return cuda_status(kscd::launch_append_kv(a, (cudaStream_t)stream), "kscd_append_kv");
 }
 

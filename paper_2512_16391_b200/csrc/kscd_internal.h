@@ -166,6 +166,7 @@ struct AppendKvArgs {
   __nv_bfloat16* const* k_caches;         // device [L] pointers, rows b*stride_b + h*stride_h + j*128
   __nv_bfloat16* const* v_caches;
   int64_t stride_b, stride_h;             // elements
+  const int* lens;                        // [B] ragged: row at lens[b] - 1 (nullable => pos)
 };
 cudaError_t launch_append_kv(const AppendKvArgs& a, cudaStream_t st);
 

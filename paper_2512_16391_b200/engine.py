@@ -138,14 +138,16 @@ class KascadeDecoder:
         return g
 
     def capture_host_step(self, q_host, kv_host, out_host, q, k_caches, v_caches, seq_len: int,
-                          dense: bool = False) -> torch.cuda.CUDAGraph:
+                          dense: bool = False, seq_lens: Optional[torch.Tensor] = None) -> torch.cuda.CUDAGraph:
         """A whole serving decode step from and to pinned host memory as ONE
         CUDA graph: H2D of the step's queries (``q_host`` [L][B][Hq][128]) and
         new K/V rows (``kv_host`` [L][2][B][Hkv][128]), one append launch that
         writes the rows at cache position ``seq_len - 1`` of every layer, the
         layer loop, and D2H of the outputs into ``out_host`` [L][B][Hq][128]
         fp32.  Replay, then synchronise the stream before reading out_host."""
-        self.seq_lens = None                # one shared append position: uniform lengths
+        # ragged batch: sequence b appends at seq_lens[b] - 1 and attends its
+        # own prefix; the graph reads seq_lens (device) at every replay
+        self.seq_lens = seq_lens
         for t, name in ((q_host, "q_host"), (kv_host, "kv_host"), (out_host, "out_host")):
             if t.is_cuda or not t.is_pinned():
                 raise InvalidArgumentError(f"{name} must be pinned host memory")
@@ -179,12 +181,12 @@ class KascadeDecoder:
                     q[1:].copy_(q_host[1:], non_blocking=True)
                 ev_rest.record(h2d)
             main.wait_event(ev_first)
-            ops.append_kv(kv_dev[:1], seq_len - 1, tables0)
+            ops.append_kv(kv_dev[:1], seq_len - 1, tables0, seq_lens)
             start = 0
             for l in range(self.L):
                 if l == 1:
                     main.wait_event(ev_rest)
-                    ops.append_kv(kv_dev[1:], seq_len - 1, tables_rest)
+                    ops.append_kv(kv_dev[1:], seq_len - 1, tables_rest, seq_lens)
                 layer(l, q, k_caches, v_caches, seq_len)
                 if l + 1 in ends:
                     c = ends.index(l + 1)

@@ -292,9 +292,10 @@ def cache_pointer_tables(k_caches, v_caches, device) -> Tuple[torch.Tensor, torc
     return kp, vp, ref.stride(0), ref.stride(1)
 
 
-def append_kv(kv_new: torch.Tensor, position: int, tables) -> None:
+def append_kv(kv_new: torch.Tensor, position: int, tables, seq_lens: Optional[torch.Tensor] = None) -> None:
     """Write the step's new rows (bf16 [L][2][B][Hkv][128], device) into
-    every layer's cache at row ``position`` with one launch."""
+    every layer's cache at row ``position`` with one launch -- or, for a
+    ragged batch, sequence b's rows at seq_lens[b] - 1 (device int32 [B])."""
     kp, vp, sb, sh = tables
     _need_cuda(kv_new, "kv_new")
     if kv_new.dtype != torch.bfloat16 or kv_new.dim() != 5 or kv_new.shape[1] != 2 or kv_new.shape[4] != HEAD_DIM \
@@ -304,6 +305,8 @@ def append_kv(kv_new: torch.Tensor, position: int, tables) -> None:
     p = _lib.AppendKvParams(num_layers=L, batch=B, num_kv_heads=Hkv, head_dim=HEAD_DIM, position=position,
                             kv_new=kv_new.data_ptr(), k_caches=kp.data_ptr(), v_caches=vp.data_ptr(),
                             kv_stride_batch=sb, kv_stride_head=sh)
+    _check_seq_lens(seq_lens, B, position + 1)
+    p.seq_lens = _ptr(seq_lens)
     _lib.call("kscd_append_kv", p, _stream())
 
 

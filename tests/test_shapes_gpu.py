@@ -100,3 +100,43 @@ def test_decode_engine_ragged_batch(cuda_ok):
     g.replay()
     torch.cuda.synchronize()
     check(dec.out.cpu().numpy(), lens2)
+
+
+def test_host_step_graph_ragged_batch(cuda_ok):
+    """capture_host_step with seq_lens: every sequence's new K/V rows land at
+    its own seq_lens[b] - 1, and the outputs equal appending by hand and
+    running the ragged eager step."""
+    from paper_2512_16391_b200 import engine
+    from paper_2512_16391_b200.host_types import AnchorPlan, AnchorPlanCore, HeadMap, KBudgetPolicy
+    L, Hq, Hkv, n_cap = 3, 8, 2, 900
+    lens = [700, 33, 899]
+    B = len(lens)
+    plan = AnchorPlan(AnchorPlanCore([0, 2], 2, 0.0), head_maps={1: HeadMap(1, 0, [1, 0])},
+                      k_policy=KBudgetPolicy(0.1, 16))
+    g = torch.Generator(device="cuda").manual_seed(9)
+    Ks = [torch.randn(B, Hkv, n_cap, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(L)]
+    Vs = [torch.randn(B, Hkv, n_cap, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(L)]
+    Kr, Vr = [x.clone() for x in Ks], [x.clone() for x in Vs]
+    q_host = torch.randn(L, B, Hq, 128).to(torch.bfloat16).pin_memory()
+    kv_host = torch.randn(L, 2, B, Hkv, 128).to(torch.bfloat16).pin_memory()
+    out_host = torch.zeros(L, B, Hq, 128).pin_memory()
+    sl = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    dec = engine.KascadeDecoder(plan, L, B, Hq, Hkv, n_cap)
+    q = torch.empty(L, B, Hq, 128, dtype=torch.bfloat16, device="cuda")
+    graph = dec.capture_host_step(q_host, kv_host, out_host, q, Ks, Vs, n_cap, seq_lens=sl)
+    for l in range(L):                       # the capture's warm-up run appended once; restore
+        Ks[l].copy_(Kr[l])
+        Vs[l].copy_(Vr[l])
+    out_host.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    for l in range(L):
+        for b, n in enumerate(lens):
+            assert torch.equal(Ks[l][b, :, n - 1].cpu(), kv_host[l, 0, b])
+            assert torch.equal(Vs[l][b, :, n - 1].cpu(), kv_host[l, 1, b])
+            Kr[l][b, :, n - 1] = kv_host[l, 0, b].cuda()
+            Vr[l][b, :, n - 1] = kv_host[l, 1, b].cuda()
+        assert torch.equal(Ks[l], Kr[l]) and torch.equal(Vs[l], Vr[l])
+    ref = engine.KascadeDecoder(plan, L, B, Hq, Hkv, n_cap)
+    want = ref.step(q_host.cuda(), Kr, Vr, n_cap, seq_lens=sl).cpu()
+    assert torch.equal(out_host, want)
