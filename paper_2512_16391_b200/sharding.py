@@ -162,7 +162,9 @@ class ShardedKascadeDecoder:
         self.full_idx = torch.empty(batch, num_kv_heads, kc, dtype=torch.int32, device=dev)
         self.full_cnt = torch.zeros(batch, num_kv_heads, dtype=torch.int32, device=dev)
 
-    def step(self, q, k_caches, v_caches, seq_len: int) -> torch.Tensor:
+    def step(self, q, k_caches, v_caches, seq_len: int, seq_lens=None) -> torch.Tensor:
+        """One decode step on this rank's heads; ``seq_lens`` (device int32
+        [B]) runs a ragged batch as in KascadeDecoder.step."""
         from . import ops
         from .host_types import KIND_ANCHOR, KIND_ANCHOR0, KIND_REUSE
         loc = self.local
@@ -173,11 +175,12 @@ class ShardedKascadeDecoder:
                 ops.sparse_decode(ql, kl, vl, seq_len, self.full_idx, self.full_cnt, self.maps[l], out=loc.out[l])
                 continue
             if kind == KIND_ANCHOR0:
-                ops.dense_decode(ql, kl, vl, seq_len, out=loc.out[l], lse=loc.lse, scores=loc.scores)
+                ops.dense_decode(ql, kl, vl, seq_len, out=loc.out[l], lse=loc.lse, scores=loc.scores,
+                                 seq_lens=seq_lens)
             else:
-                ops.anchor_scores_decode(ql, kl, seq_len, loc.scores, loc.lse)
+                ops.anchor_scores_decode(ql, kl, seq_len, loc.scores, loc.lse, seq_lens=seq_lens)
             ops.select_decode(loc.scores, loc.lse, seq_len, pol, self.Hloc, indices=loc.indices, counts=loc.counts,
-                              pooled=loc.pooled)
+                              pooled=loc.pooled, seq_lens=seq_lens)
             # the exchange overlaps the anchor's own sparse pass, which only
             # needs this rank's lists
             pending = PendingIndexGather(loc.indices, loc.counts, self.group, head_dim=1)
