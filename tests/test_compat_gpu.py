@@ -286,3 +286,25 @@ def test_head_dim_above_128_rejected(cuda_ok):
     Q, K, V = orc.random_qkv(5, 1, 2, 1, 160, 8)
     with pytest.raises(UnsupportedOperationError):
         compat.dense_attention(trace(Q, K, V), 0)
+
+
+def test_topk_attention_non_causal_matches_oracle(cuda_ok):
+    """causal=False (attention.py:233: every row sees the whole selection,
+    selections may reach past the tile) against the oracle, with the
+    mass recovered from the non-causal dense normaliser."""
+    from paper_2512_16391_b200 import TopKIndexSet, compat, make_tiles
+    t = rand_trace(31, Hq=4, Hkv=2, N=80)
+    tiles = make_tiles(80, "prefill", 4, 2, tile_size=32)
+    rng = np.random.default_rng(5)
+    sels = {}
+    for tl in tiles.tiles:
+        idx = np.sort(rng.choice(80, size=12, replace=False))          # keys past the tile too
+        sels[(tl.kv_head, tl.tile_id)] = TopKIndexSet(tl.kv_head, tl.tile_id, idx, 12)
+    res = compat.topk_attention(t, 0, sels, tiles, causal=False)
+    P, _ = orc.dense_layer(t.Q[0], t.K[0], t.V[0], causal=False)
+    Y, mass, fb = orc.sparse_layer(t.Q[0], t.K[0], t.V[0], {k: v.indices for k, v in sels.items()},
+                                   [(tl.start, tl.end, tl.tile_id) for tl in tiles.tiles if tl.kv_head == 0],
+                                   causal=False, dense_P=P)
+    assert_outputs_close(res.Y, Y)
+    np.testing.assert_allclose(res.mass_recovered, mass, atol=1e-3)
+    assert res.fallback_rows == [] and fb == []
