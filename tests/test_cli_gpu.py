@@ -58,3 +58,19 @@ def test_module_entry_point(tmp_path, cuda_ok):
     assert r.returncode == 0, r.stderr
     assert r.stdout.splitlines()[0] == c["cases"]["t128_prefill_remapped"]["stdout"].splitlines()[0]
     assert "anchor0" in r.stdout
+
+
+def test_cli_workflow_small_head_dim(cuda_ok, tmp_path):
+    """gen -> plan -> run (both phases) -> analyze -> report at head_dim 16,
+    the reference CLI tests' scale (rows zero-padded to 128 on the device)."""
+    from paper_2512_16391_b200 import cli
+    t, p, r = tmp_path / "t.kscd", tmp_path / "p.json", tmp_path / "r.json"
+    assert cli.main(["gen", "--layers", "4", "--q-heads", "4", "--kv-heads", "2", "--dim", "16", "--tokens", "96",
+                     "--seed", "3", "--permute-heads", "--xy", "--out", str(t)]) == 0
+    assert cli.main(["plan", "--trace", str(t), "--out", str(p), "--budget", "2", "--k", "16", "--tile-size", "32",
+                     "--fraction", "0.25", "--k-min", "8"]) == 0
+    assert cli.main(["run", "--trace", str(t), "--plan", str(p), "--out", str(r)]) == 0
+    assert cli.main(["run", "--trace", str(t), "--plan", str(p), "--phase", "decode", "--fail-above", "0.5"]) == 0
+    assert cli.main(["analyze", "--trace", str(t), "--out-dir", str(tmp_path / "an"), "--importance"]) == 0
+    assert (tmp_path / "an" / "similarity.csv").read_text().startswith("row,col,value\n")
+    assert cli.main(["report", str(r)]) == 0
