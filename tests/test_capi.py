@@ -129,3 +129,19 @@ def test_ctypes_structs_match_the_header_layout(tmp_path):
         assert ctypes.sizeof(cls) == c_layout[(cname, "size")], cname
         for m in names:
             assert getattr(cls, m).offset == c_layout[(cname, m)], (cname, m)
+
+
+def test_workspace_covers_virtual_heads_of_large_groups(lib):
+    """Query groups above 16 run as virtual kv heads (G = 32 -> 2 per kv
+    head): the workspace query counts their split counters too."""
+    from paper_2512_16391_b200 import _lib
+
+    def size(hq, hkv):
+        p = _lib.DecodeParams(batch=4, num_q_heads=hq, num_kv_heads=hkv, head_dim=128, seq_len=4096)
+        nb = ctypes.c_size_t(0)
+        assert lib.kscd_decode_workspace_size(ctypes.byref(p), ctypes.byref(nb)) == 0
+        return nb.value
+
+    # same query heads; one kv head with G = 32 needs counters for 2 virtual heads
+    assert size(32, 1) >= 4 * 32 * 130 * 4 + 4 * 2 * 4
+    assert size(32, 2) >= 4 * 32 * 130 * 4 + 4 * 2 * 4
