@@ -596,6 +596,9 @@ def sharded_70b(dev, world, dist, plan, N, B, steps, warm, seed, L=80, Hq=64, Hk
     V = [vs[l % nd] for l in range(L)]
     m_pa = _timed(lambda: pf.forward(Q, K, V), 1, 1, world, dist, dev)
     m_pd = _timed(lambda: pf.local.dense_forward(Q, K, V), 1, 1, world, dist, dev)
+    # one layer's head-sharded output reassembly ([N][Hq][d] bf16 per layer)
+    from paper_2512_16391_b200.sharding import gather_head_outputs
+    m_pg = _timed(lambda: gather_head_outputs(pf.local.out[0], head_dim=0), 2, 1, world, dist, dev)
     del pf, qs, ks, vs, Q, K, V
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
@@ -606,6 +609,7 @@ def sharded_70b(dev, world, dist, plan, N, B, steps, warm, seed, L=80, Hq=64, Hk
     if n_distinct_max:
         ndd = min(ndd, n_distinct_max)
     dec = sharding.ShardedKascadeDecoder(plan, L, B, Hq, Hkv, N)
+    nccl = dist.get_backend() == "nccl"
     Kc, Vc = [], []
     for i in range(ndd):
         gen.manual_seed(seed + 500 + i)
@@ -614,8 +618,16 @@ def sharded_70b(dev, world, dist, plan, N, B, steps, warm, seed, L=80, Hq=64, Hk
     Ks = [Kc[l % ndd] for l in range(L)]
     Vs = [Vc[l % ndd] for l in range(L)]
     q = (torch.randn(L, B, Hql, 128, device=dev, generator=gen) * 2.0).to(torch.bfloat16)
-    m_da = _timed(lambda: dec.step(q, Ks, Vs, N), steps, warm, world, dist, dev)
-    m_dd = _timed(lambda: dec.local.dense_step(q, Ks, Vs, N), steps, warm, world, dist, dev)
+    if nccl:   # the whole sharded step, NCCL all-gathers included, is one CUDA graph
+        g_a, g_d = dec.capture(q, Ks, Vs, N), dec.capture(q, Ks, Vs, N, dense=True)
+        m_da = _timed(g_a.replay, steps, warm, world, dist, dev)
+        m_dd = _timed(g_d.replay, steps, warm, world, dist, dev)
+        del g_a, g_d
+    else:      # gloo (CPU-staged exchange, tests): eager
+        m_da = _timed(lambda: dec.step(q, Ks, Vs, N), steps, warm, world, dist, dev)
+        m_dd = _timed(lambda: dec.local.dense_step(q, Ks, Vs, N), steps, warm, world, dist, dev)
+    # head-sharded output reassembly, timed on its own (once per step)
+    m_dg = _timed(dec.gather_outputs, steps, warm, world, dist, dev)
     del dec, Kc, Vc, Ks, Vs, q
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
@@ -629,12 +641,31 @@ def sharded_70b(dev, world, dist, plan, N, B, steps, warm, seed, L=80, Hq=64, Hk
             "decode_kascade_us_per_token": round(m_da * 1e3 / B, 2),
             "decode_dense_us_per_token": round(m_dd * 1e3 / B, 2),
             "decode_speedup_vs_dense": round(m_dd / m_da, 3), "decode_batch": B,
+            "decode_cuda_graph": nccl,
+            "reassembly": {"prefill_ms_per_layer": round(m_pg, 3), "decode_ms_per_step": round(m_dg, 4),
+                           "note": "all-gather of the head-sharded outputs, timed separately (not in the "
+                                   "attention times above)"},
             "layers_distinct": {"prefill": nd, "decode": ndd}}
 
 
 # ------------------------------------------------------------------ GPU arm
+def spawn_ranks(n):
+    """`bench.py --gpus N` outside torchrun: relaunch under torchrun with N
+    ranks (one per GPU, rendezvous on 127.0.0.1) and return its exit code."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

@@ -47,7 +47,7 @@ extern "C" {
 #define KSCD_UNSUPPORTED 2
 #define KSCD_CUDA_ERROR 3
 
-#define KSCD_ABI_VERSION 1
+#define KSCD_ABI_VERSION 2
 
 /* One decode step of one layer for a batch of sequences (the reference's
  * decode tile [t, t+1) with causal bound n = t + 1, tiles.py:145-150). */
@@ -200,6 +200,8 @@ typedef struct kscd_append_kv_params {
   int64_t kv_stride_batch, kv_stride_head;   /* elements, shared by every layer's cache */
   const int32_t* seq_lens;      /* device int32 [B] or NULL: ragged batch, sequence b's row goes to
                                    seq_lens[b] - 1 (position is then ignored) */
+  int32_t cache_capacity;       /* n_cap: rows per (sequence, kv head) of every cache; position must be
+                                   < n_cap, and a ragged row outside [0, n_cap) is skipped (never written) */
 } kscd_append_kv_params;
 
 int kscd_abi_version(void);

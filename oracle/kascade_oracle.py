@@ -238,8 +238,8 @@ def sparse_tile(Ql, Kl, Vl, g: int, G: int, start: int, end: int, sel: np.ndarra
     rows = np.arange(start, end)
     nvis = np.searchsorted(sel, rows, side="right") if causal else np.full(T, sel.size)
     vis = np.arange(sel.size)[None, :] < nvis[:, None]
-    ks = Kl[g, sel].astype(np.float32)
-    vs = Vl[g, sel].astype(np.float32)
+    ks = np.asarray(Kl[g, sel], dtype=np.float32)
+    vs = np.asarray(Vl[g, sel], dtype=np.float32)
     live = nvis > 0
     Y = np.zeros((G, T, d), np.float32)
     mass = np.zeros((G, T), np.float32)
@@ -341,16 +341,19 @@ def run_kascade(Q, K, V, anchors: Sequence[int], head_maps: Dict[int, Sequence[i
 # O(n) drivers for sizes the full reference cannot hold
 # --------------------------------------------------------------------------
 
-def dense_row(q: np.ndarray, Kg: np.ndarray, Vg: np.ndarray):
+def dense_row(q: np.ndarray, Kg: np.ndarray, Vg: np.ndarray, want_y: bool = True):
     """Post-softmax row and output of one query over all keys of its kv head
     (the last causal row).  Uses 4-row GEMMs: on OpenBLAS a 1-row sgemm
     (and, for P@V, a 2-row one) rounds differently from the rows of the
     reference's full GEMMs; 4-row blocks are bit-equal (tests pin this)."""
     d = q.shape[-1]
     q4 = np.stack([q] * 4).astype(np.float32)
-    s = ((q4 @ Kg.astype(np.float32).T) * _scale(d))[:1]
+    # no-copy views of fp32 K/V, as the reference's np.asarray(..., float32)
+    s = ((q4 @ np.asarray(Kg, dtype=np.float32).T) * _scale(d))[:1]
     p = masked_softmax(s, np.ones_like(s, dtype=bool))
-    y = (np.concatenate([p] * 4) @ Vg.astype(np.float32))[0]
+    if not want_y:
+        return p[0], None
+    y = (np.concatenate([p] * 4) @ np.asarray(Vg, dtype=np.float32))[0]
     return p[0], y
 
 
@@ -386,7 +389,9 @@ def decode_step(q: np.ndarray, K: np.ndarray, V: np.ndarray, anchors: Sequence[i
         Yd = np.zeros((Hq, d), np.float32)
         if l == 0 or want_mass or (is_anchor and pooling == POST):
             for h in range(Hq):
-                P[h, 0], Yd[h] = dense_row(q[l, h], K[l, h // G], V[l, h // G])
+                P[h, 0], y = dense_row(q[l, h], K[l, h // G], V[l, h // G], want_y=l == 0)
+                if y is not None:
+                    Yd[h] = y
         if is_anchor:
             pooled = {}
             for g in range(Hkv):
@@ -414,8 +419,8 @@ def decode_step(q: np.ndarray, K: np.ndarray, V: np.ndarray, anchors: Sequence[i
             continue
         for g in range(Hkv):
             sel = sels[(g, n - 1)]
-            ks = K[l, g, sel].astype(np.float32)
-            vs = V[l, g, sel].astype(np.float32)
+            ks = np.asarray(K[l, g, sel], dtype=np.float32)     # the gather is the only copy
+            vs = np.asarray(V[l, g, sel], dtype=np.float32)
             for j in range(G):
                 h = g * G + j
                 s = (q[l, h][None].astype(np.float32) @ ks.T) * _scale(d)
@@ -437,7 +442,7 @@ def prefill_tile_rows(Ql, Kl, g: int, G: int, start: int, end: int) -> np.ndarra
     N = Kl.shape[1]
     rows = np.arange(start, end)
     vis = np.arange(N)[None, :] <= rows[:, None]
-    kk = Kl[g].astype(np.float32)
+    kk = np.asarray(Kl[g], dtype=np.float32)
     return np.stack([masked_softmax((Ql[g * G + j, start:end].astype(np.float32) @ kk.T) * _scale(d), vis)
                      for j in range(G)])
 

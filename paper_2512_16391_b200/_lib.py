@@ -102,7 +102,7 @@ class AppendKvParams(ctypes.Structure):
         ("num_layers", c_i32), ("batch", c_i32), ("num_kv_heads", c_i32), ("head_dim", c_i32),
         ("position", c_i32), ("kv_new", c_vp), ("k_caches", c_vp), ("v_caches", c_vp),
         ("kv_stride_batch", c_i64), ("kv_stride_head", c_i64),
-        ("seq_lens", c_vp),
+        ("seq_lens", c_vp), ("cache_capacity", c_i32),
     ]
 
 
@@ -136,6 +136,9 @@ _lock = threading.Lock()
 _lib = None
 
 
+ABI_VERSION = 2   # include/kascade_b200.h KSCD_ABI_VERSION
+
+
 def load(path: str = LIB_PATH) -> ctypes.CDLL:
     """Load (once) the CUDA library; raises KascadeError when it is absent."""
     global _lib
@@ -156,6 +159,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.kscd_last_error.restype = ctypes.c_char_p
         lib.kscd_last_error.argtypes = []
         lib.kscd_abi_version.restype = ctypes.c_int
+        if lib.kscd_abi_version() != ABI_VERSION:
+            raise KascadeError(f"{path} has ABI version {lib.kscd_abi_version()}, the binding expects "
+                               f"{ABI_VERSION}: rebuild with `python -m paper_2512_16391_b200.build`")
         lib.kscd_k_budget.restype = c_i32
         lib.kscd_k_budget.argtypes = [c_f64, c_i32, c_i32]
         lib.kscd_decode_workspace_size.restype = ctypes.c_int

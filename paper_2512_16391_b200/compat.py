@@ -307,10 +307,9 @@ def run_kascade(trace, plan, phase: str = PREFILL) -> Tuple[np.ndarray, RunRepor
     layer 0 dense (+ selections), anchors select fresh sets and attend
     sparsely, reuse layers route the latest anchor's sets through their head
     map.  Fidelity (rel-L2 vs dense, recovered mass, fallback rows) per layer."""
-    try:
-        validate_plan(plan, trace)
-    except InvalidArgumentError as e:
-        raise InvalidPlanError(str(e)) from None
+    # runner.py:236 -- plan errors raise InvalidPlanError, head-map errors the
+    # reference HeadMap's own InvalidArgumentError (heads.py:37-47), unchanged
+    validate_plan(plan, trace)
     L, Hq, Hkv, N = trace.num_layers, trace.num_query_heads, trace.num_kv_heads, trace.seq_len
     G = Hq // Hkv
     tiles = make_tiles(N, phase, Hq, Hkv, plan.tile_size)

@@ -467,6 +467,10 @@ extern "C" int kscd_append_kv(const kscd_append_kv_params* p, void* stream) {
   if (bad_head_dim(p->head_dim)) return fail(KSCD_UNSUPPORTED, KSCD_HEAD_DIM_MSG, p->head_dim);
   if (p->num_layers < 1 || p->batch < 1 || p->num_kv_heads < 1 || p->position < 0)
     return fail(KSCD_INVALID_ARGUMENT, "bad shape");
+  if (p->cache_capacity < 1) return fail(KSCD_INVALID_ARGUMENT, "cache_capacity must be >= 1");
+  if (!p->seq_lens && p->position >= p->cache_capacity)
+    return fail(KSCD_INVALID_ARGUMENT, "position %d outside the cache (capacity %d)", p->position,
+                p->cache_capacity);
   if (!p->kv_new || !p->k_caches || !p->v_caches) return fail(KSCD_INVALID_ARGUMENT, "NULL buffer");
   if (((uintptr_t)p->kv_new & 15) || (p->kv_stride_batch & 7) || (p->kv_stride_head & 7))
     return fail(KSCD_INVALID_ARGUMENT, "kv_new and cache strides must be 16-byte aligned");
@@ -481,6 +485,7 @@ extern "C" int kscd_append_kv(const kscd_append_kv_params* p, void* stream) {
   a.stride_b = p->kv_stride_batch;
   a.stride_h = p->kv_stride_head;
   a.lens = p->seq_lens;
+  a.n_cap = p->cache_capacity;
   return cuda_status(kscd::launch_append_kv(a, (cudaStream_t)stream), "kscd_append_kv");
 }
 

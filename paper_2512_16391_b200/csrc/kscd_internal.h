@@ -167,6 +167,7 @@ struct AppendKvArgs {
   __nv_bfloat16* const* v_caches;
   int64_t stride_b, stride_h;             // elements
   const int* lens;                        // [B] ragged: row at lens[b] - 1 (nullable => pos)
+  int n_cap;                              // rows per cache; rows outside [0, n_cap) are skipped
 };
 cudaError_t launch_append_kv(const AppendKvArgs& a, cudaStream_t st);
 

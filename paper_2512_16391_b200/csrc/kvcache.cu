@@ -24,6 +24,7 @@ __global__ void append_kv_kernel(AppendKvArgs a) {
     const uint4 v = reinterpret_cast<const uint4*>(a.kv_new)[t];
     __nv_bfloat16* base = kv ? a.v_caches[l] : a.k_caches[l];
     const long long pos = a.lens ? (long long)__ldg(a.lens + b) - 1 : (long long)a.pos;
+    if (pos < 0 || pos >= a.n_cap) continue;   // a bad ragged length never writes outside its rows
     __nv_bfloat16* dst = base + (long long)b * a.stride_b + (long long)h * a.stride_h + pos * 128;
     reinterpret_cast<uint4*>(dst)[chunk] = v;
   }

@@ -73,6 +73,9 @@ class KascadeDecoder:
         self.indices = torch.empty(batch, Hsrc, k_cap, dtype=torch.int32, device=dev)
         self.counts = torch.zeros(batch, Hsrc, dtype=torch.int32, device=dev)
         self.out = torch.empty(num_layers, batch, num_q_heads, 128, dtype=torch.float32, device=dev)
+        # the executor's own split-K workspace: its layers run stream-ordered,
+        # so they share it; no other executor, stream or graph touches it
+        self.ws = ops.new_decode_workspace(dev, batch, num_q_heads, num_kv_heads)
         self._graphs = {}
         self.seq_lens: Optional[torch.Tensor] = None     # ragged batch (step / dense_step)
 
@@ -98,21 +101,24 @@ class KascadeDecoder:
         kind = self.kinds[l]
         ql, kl, vl = q[l], k_caches[l], v_caches[l]
         if kind == KIND_REUSE:
-            ops.sparse_decode(ql, kl, vl, seq_len, self.indices, self.counts, self.head_maps[l], out=self.out[l])
+            ops.sparse_decode(ql, kl, vl, seq_len, self.indices, self.counts, self.head_maps[l], out=self.out[l],
+                              workspace=self.ws)
             return
         sl = self.seq_lens
         if kind == KIND_ANCHOR0:
-            ops.dense_decode(ql, kl, vl, seq_len, out=self.out[l], lse=self.lse, scores=self.scores, seq_lens=sl)
+            ops.dense_decode(ql, kl, vl, seq_len, out=self.out[l], lse=self.lse, scores=self.scores, seq_lens=sl,
+                             workspace=self.ws)
         else:
-            ops.anchor_scores_decode(ql, kl, seq_len, self.scores, self.lse, seq_lens=sl)
+            ops.anchor_scores_decode(ql, kl, seq_len, self.scores, self.lse, seq_lens=sl, workspace=self.ws)
         ops.select_decode(self.scores, self.lse, seq_len, pol, self.Hkv, indices=self.indices,
                           counts=self.counts, pooled=self.pooled, all_heads=self.all_heads, seq_lens=sl)
         if kind == KIND_ANCHOR:
-            ops.sparse_decode(ql, kl, vl, seq_len, self.indices, self.counts, self.shared_map, out=self.out[l])
+            ops.sparse_decode(ql, kl, vl, seq_len, self.indices, self.counts, self.shared_map, out=self.out[l],
+                              workspace=self.ws)
 
     def _dense_layer(self, l: int, q, k_caches, v_caches, seq_len: int) -> None:
         ops.dense_decode(q[l], k_caches[l], v_caches[l], seq_len, out=self.out[l], lse=self.lse,
-                         seq_lens=self.seq_lens)
+                         seq_lens=self.seq_lens, workspace=self.ws)
 
     def dense_step(self, q, k_caches, v_caches, seq_len: int, seq_lens: Optional[torch.Tensor] = None
                    ) -> torch.Tensor:
@@ -151,9 +157,14 @@ class KascadeDecoder:
         for t, name in ((q_host, "q_host"), (kv_host, "kv_host"), (out_host, "out_host")):
             if t.is_cuda or not t.is_pinned():
                 raise InvalidArgumentError(f"{name} must be pinned host memory")
+        kp, vp, sb, sh, n_cap = ops.cache_pointer_tables(k_caches, v_caches, self.device)
+        # every append lands inside the caches: validated before anything is enqueued
+        # (a ragged row outside [0, n_cap) is skipped by the kernel as well)
+        if not 1 <= seq_len <= min(self.n_max, n_cap):
+            raise InvalidArgumentError(f"seq_len {seq_len} outside [1, min(max_seq_len {self.n_max}, "
+                                       f"cache capacity {n_cap})]")
         kv_dev = torch.empty(kv_host.shape, dtype=torch.bfloat16, device=self.device)
-        kp, vp, sb, sh = ops.cache_pointer_tables(k_caches, v_caches, self.device)
-        tables0, tables_rest = (kp[:1], vp[:1], sb, sh), (kp[1:], vp[1:], sb, sh)
+        tables0, tables_rest = (kp[:1], vp[:1], sb, sh, n_cap), (kp[1:], vp[1:], sb, sh, n_cap)
         layer = self._dense_layer if dense else self._layer
         # The copies are pipelined against the layer loop on two side streams
         # (graph branches): layer 0's new K/V rows and queries arrive first

@@ -83,19 +83,35 @@ def _check_kv(k: torch.Tensor, v: Optional[torch.Tensor], B: int) -> Tuple[int, 
     return k.shape[1], k.shape[2], k.stride(0), k.stride(1)
 
 
+def decode_workspace_bytes(B: int, Hq: int, Hkv: int) -> int:
+    p = _lib.DecodeParams(batch=B, num_q_heads=Hq, num_kv_heads=Hkv, head_dim=HEAD_DIM, seq_len=1)
+    nbytes = _lib.c_sz(0)
+    _lib.check(_lib.load().kscd_decode_workspace_size(ctypes.byref(p), ctypes.byref(nbytes)))
+    return nbytes.value
+
+
+def new_decode_workspace(device, B: int, Hq: int, Hkv: int) -> torch.Tensor:
+    """A zero-filled split-K workspace (partials + arrival counters).  The
+    kernels leave it re-armed, so one workspace serves any number of
+    stream-ordered calls; it must NOT be shared by calls that can run
+    concurrently (other streams, other graphs).  The executors own one each."""
+    return torch.zeros(decode_workspace_bytes(B, Hq, Hkv), dtype=torch.uint8, device=device)
+
+
 _WS = {}
 
 
 def decode_workspace(device: torch.device, B: int, Hq: int, Hkv: int) -> torch.Tensor:
-    """Zero-filled split-K workspace, cached per (device, shape); the kernels
-    leave it re-armed so it is reused across calls and graph replays."""
-    key = (device.index if device.index is not None else torch.cuda.current_device(), B, Hq, Hkv)
+    """Workspace for standalone op calls that pass none: one per (device,
+    current stream, shape), so calls on different streams never share
+    arrival counters.  Graph captures and executors pass their own."""
+    dev = device.index if device.index is not None else torch.cuda.current_device()
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream, B, Hq, Hkv)
     ws = _WS.get(key)
     if ws is None:
-        p = _lib.DecodeParams(batch=B, num_q_heads=Hq, num_kv_heads=Hkv, head_dim=HEAD_DIM, seq_len=1)
-        nbytes = _lib.c_sz(0)
-        _lib.check(_lib.load().kscd_decode_workspace_size(ctypes.byref(p), ctypes.byref(nbytes)))
-        ws = torch.zeros(nbytes.value, dtype=torch.uint8, device=device)
+        if torch.cuda.is_current_stream_capturing():
+            raise InvalidArgumentError("pass workspace= when capturing a CUDA graph (the executors own one)")
+        ws = new_decode_workspace(device, B, Hq, Hkv)
         _WS[key] = ws
     return ws
 
@@ -110,14 +126,20 @@ def _check_seq_lens(seq_lens: Optional[torch.Tensor], B: int, n: int) -> None:
         raise InvalidArgumentError(f"seq_lens must be a contiguous CUDA int32 [B={B}] tensor")
 
 
-def _decode_params(q, k, v, n, out, lse, scores, scale, num_splits, seq_lens=None) -> _lib.DecodeParams:
+def _decode_params(q, k, v, n, out, lse, scores, scale, num_splits, seq_lens=None, workspace=None
+                   ) -> _lib.DecodeParams:
     B, Hq = _check_q(q)
     Hkv, n_cap, sb, sh = _check_kv(k, v, B)
     if not (1 <= n <= n_cap):
         raise InvalidArgumentError(f"seq_len {n} outside [1, {n_cap}]")
     if Hq % Hkv:
         raise InvalidArgumentError(f"num_query_heads ({Hq}) must be divisible by num_kv_heads ({Hkv})")
-    ws = decode_workspace(q.device, B, Hq, Hkv)
+    if workspace is None:
+        ws = decode_workspace(q.device, B, Hq, Hkv)
+    else:
+        if workspace.dtype != torch.uint8 or not workspace.is_cuda or not workspace.is_contiguous():
+            raise InvalidArgumentError("workspace must be a contiguous CUDA uint8 tensor (new_decode_workspace)")
+        ws = workspace
     p = _lib.DecodeParams(
         batch=B, num_q_heads=Hq, num_kv_heads=Hkv, head_dim=HEAD_DIM, seq_len=int(n),
         q=q.data_ptr(), k_cache=k.data_ptr(), v_cache=_ptr(v), kv_stride_batch=sb, kv_stride_head=sh,
@@ -146,7 +168,8 @@ def score_buffer(B: int, Hq: int, n: int, device) -> torch.Tensor:
 def dense_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, seq_len: int, *,
                  out: Optional[torch.Tensor] = None, lse: Optional[torch.Tensor] = None,
                  scores: Optional[torch.Tensor] = None, scale: Optional[float] = None,
-                 num_splits: int = 0, seq_lens: Optional[torch.Tensor] = None):
+                 num_splits: int = 0, seq_lens: Optional[torch.Tensor] = None,
+                 workspace: Optional[torch.Tensor] = None):
     """Dense attention of the step's query over keys [0, seq_len)
     (dense_attention's last row, attention.py:106-144).  If ``scores`` is
     given, the log2-domain scores s*log2(e) are written for the anchor-0
@@ -156,22 +179,23 @@ def dense_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, 
     out = torch.empty(B, Hq, HEAD_DIM, dtype=torch.float32, device=q.device) if out is None else out
     lse = torch.empty(B, Hq, dtype=torch.float32, device=q.device) if lse is None else lse
     _check_scores(scores, B, Hq, seq_len)
-    p = _decode_params(q, k_cache, v_cache, seq_len, out, lse, scores, scale, num_splits, seq_lens)
+    p = _decode_params(q, k_cache, v_cache, seq_len, out, lse, scores, scale, num_splits, seq_lens, workspace)
     _lib.call("kscd_dense_decode", p, _stream())
     return out, lse
 
 
-def anchor_scores_decode(q, k_cache, seq_len, scores, lse, *, scale=None, num_splits=0, seq_lens=None):
+def anchor_scores_decode(q, k_cache, seq_len, scores, lse, *, scale=None, num_splits=0, seq_lens=None,
+                         workspace=None):
     """Anchor pass 1: log2-domain scores + LSE; V is not read."""
     B, Hq = q.shape[0], q.shape[1]
     _check_scores(scores, B, Hq, seq_len)
-    p = _decode_params(q, k_cache, None, seq_len, None, lse, scores, scale, num_splits, seq_lens)
+    p = _decode_params(q, k_cache, None, seq_len, None, lse, scores, scale, num_splits, seq_lens, workspace)
     _lib.call("kscd_anchor_scores_decode", p, _stream())
     return scores, lse
 
 
 def sparse_decode(q, k_cache, v_cache, seq_len, indices, counts, head_map=None, *, out=None, lse=None,
-                  scale=None, num_splits=0):
+                  scale=None, num_splits=0, workspace=None):
     """topk_attention over a decode tile (attention.py:185-253): kv head g of
     sequence b attends the keys indices[b][head_map[g]][:counts[b][head_map[g]]]
     (runner.py:210-225).  ``head_map`` is a device int32 [Hkv] tensor (None =
@@ -182,7 +206,7 @@ def sparse_decode(q, k_cache, v_cache, seq_len, indices, counts, head_map=None, 
             or counts.shape != indices.shape[:2] or indices.shape[0] != B:
         raise InvalidArgumentError("indices must be int32 [B][Hsrc][k_cap], counts int32 [B][Hsrc]")
     out = torch.empty(B, Hq, HEAD_DIM, dtype=torch.float32, device=q.device) if out is None else out
-    p = _decode_params(q, k_cache, v_cache, seq_len, out, lse, None, scale, num_splits)
+    p = _decode_params(q, k_cache, v_cache, seq_len, out, lse, None, scale, num_splits, workspace=workspace)
     if head_map is not None:
         if head_map.dtype != torch.int32 or head_map.numel() != p.num_kv_heads or not head_map.is_cuda:
             raise InvalidArgumentError("head_map must be a CUDA int32 tensor with one entry per kv head")
@@ -289,14 +313,17 @@ def cache_pointer_tables(k_caches, v_caches, device) -> Tuple[torch.Tensor, torc
             raise InvalidArgumentError("caches must be bf16 [B][Hkv][n_cap][128] with one shared stride layout")
     kp = torch.tensor([t.data_ptr() for t in k_caches], dtype=torch.int64, device=device)
     vp = torch.tensor([t.data_ptr() for t in v_caches], dtype=torch.int64, device=device)
-    return kp, vp, ref.stride(0), ref.stride(1)
+    return kp, vp, ref.stride(0), ref.stride(1), ref.shape[2]
 
 
 def append_kv(kv_new: torch.Tensor, position: int, tables, seq_lens: Optional[torch.Tensor] = None) -> None:
     """Write the step's new rows (bf16 [L][2][B][Hkv][128], device) into
     every layer's cache at row ``position`` with one launch -- or, for a
-    ragged batch, sequence b's rows at seq_lens[b] - 1 (device int32 [B])."""
-    kp, vp, sb, sh = tables
+    ragged batch, sequence b's rows at seq_lens[b] - 1 (device int32 [B]);
+    the kernel skips a ragged row outside the cache capacity."""
+    kp, vp, sb, sh, n_cap = tables
+    if not 0 <= position < n_cap:
+        raise InvalidArgumentError(f"append position {position} outside the cache (capacity {n_cap})")
     _need_cuda(kv_new, "kv_new")
     if kv_new.dtype != torch.bfloat16 or kv_new.dim() != 5 or kv_new.shape[1] != 2 or kv_new.shape[4] != HEAD_DIM \
             or not kv_new.is_contiguous() or kv_new.shape[0] != kp.numel():
@@ -304,7 +331,7 @@ def append_kv(kv_new: torch.Tensor, position: int, tables, seq_lens: Optional[to
     L, _, B, Hkv, _ = kv_new.shape
     p = _lib.AppendKvParams(num_layers=L, batch=B, num_kv_heads=Hkv, head_dim=HEAD_DIM, position=position,
                             kv_new=kv_new.data_ptr(), k_caches=kp.data_ptr(), v_caches=vp.data_ptr(),
-                            kv_stride_batch=sb, kv_stride_head=sh)
+                            kv_stride_batch=sb, kv_stride_head=sh, cache_capacity=n_cap)
     _check_seq_lens(seq_lens, B, position + 1)
     p.seq_lens = _ptr(seq_lens)
     _lib.call("kscd_append_kv", p, _stream())

@@ -133,12 +133,71 @@ def local_head_map(head_map, g0: int, g1: int, device=None) -> torch.Tensor:
     return torch.tensor(m[g0:g1], dtype=torch.int32, device=device)
 
 
+class IndexExchange:
+    """The head-remap exchange of one sharded executor with every buffer
+    preallocated, so a decode step that contains it can be captured in a
+    CUDA graph (NCCL collectives are graph-capturable once the communicator
+    exists; the executors run one eager step before capturing).
+
+    ``local_idx`` / ``local_cnt`` are the executor's per-kv-head lists with
+    the kv-head axis at ``head_dim``; ``full_idx`` / ``full_cnt`` receive
+    the lists of ALL kv heads (global head order = rank order).  With the
+    kv-head axis leading (prefill, head_dim 0) the all-gather writes straight
+    into ``full_*``; otherwise (decode, head_dim 1) one small copy on each
+    side moves the axis."""
+
+    def __init__(self, local_idx, local_cnt, full_idx, full_cnt, group=None, head_dim: int = 1):
+        self.group, self.head_dim = group, head_dim
+        self.world, _ = _world(group)
+        self.local, self.full = (local_idx, local_cnt), (full_idx, full_cnt)
+        self.staged = self.world > 1 and (not local_idx.is_cuda or dist.get_backend(group) == "gloo")
+        self.works = []
+        if self.world == 1 or self.staged:
+            return
+        if head_dim == 0:
+            self.send = self.local
+            self.recv = self.full
+        else:
+            self.send = tuple(torch.empty_like(t.movedim(head_dim, 0).contiguous()) for t in self.local)
+            self.recv = tuple(torch.empty((self.world * s.shape[0],) + tuple(s.shape[1:]), dtype=s.dtype,
+                                          device=s.device) for s in self.send)
+
+    def start(self) -> None:
+        """Enqueue the all-gather behind the select that wrote the local lists."""
+        if self.world == 1:
+            for f, t in zip(self.full, self.local):
+                f.copy_(t)
+            return
+        if self.staged:                 # gloo (CPU tests): host-staged, synchronous
+            idx, cnt = gather_index_lists(*self.local, self.group, self.head_dim)
+            self.full[0].copy_(idx)
+            self.full[1].copy_(cnt)
+            return
+        if self.head_dim != 0:
+            for s, t in zip(self.send, self.local):
+                s.copy_(t.movedim(self.head_dim, 0))
+        self.works = [dist.all_gather_into_tensor(r, s, group=self.group, async_op=True)
+                      for r, s in zip(self.recv, self.send)]
+
+    def finish(self) -> None:
+        """Make the current stream wait for the exchange; full_* then hold it."""
+        for w in self.works:
+            w.wait()
+        self.works = []
+        if self.world > 1 and not self.staged and self.head_dim != 0:
+            for f, r in zip(self.full, self.recv):
+                f.copy_(r.movedim(0, self.head_dim))
+
+
 class ShardedKascadeDecoder:
     """KV-head-sharded decode executor (one rank's share).
 
     Anchor layers select on the local kv heads, then all-gather the index
     lists; reuse layers gather through the GLOBAL head map from the gathered
-    lists.  q / caches passed to ``step`` are the rank's local head slices."""
+    lists.  q / caches passed to ``step`` are the rank's local head slices.
+    Every buffer (including the exchange's) is preallocated, so ``capture``
+    records the whole step -- kernels and NCCL all-gathers -- as one CUDA
+    graph."""
 
     def __init__(self, plan, num_layers: int, batch: int, num_q_heads: int, num_kv_heads: int,
                  max_seq_len: int, group=None, device=None):
@@ -161,6 +220,9 @@ class ShardedKascadeDecoder:
         kc = k_budget(plan.k_policy, max_seq_len)
         self.full_idx = torch.empty(batch, num_kv_heads, kc, dtype=torch.int32, device=dev)
         self.full_cnt = torch.zeros(batch, num_kv_heads, dtype=torch.int32, device=dev)
+        self.exchange = IndexExchange(self.local.indices, self.local.counts, self.full_idx, self.full_cnt,
+                                      group, head_dim=1)
+        self._graphs = {}
 
     def step(self, q, k_caches, v_caches, seq_len: int, seq_lens=None) -> torch.Tensor:
         """One decode step on this rank's heads; ``seq_lens`` (device int32
@@ -169,27 +231,42 @@ class ShardedKascadeDecoder:
         from .host_types import KIND_ANCHOR, KIND_ANCHOR0, KIND_REUSE
         loc = self.local
         pol = loc.plan.k_policy
+        ws = loc.ws
         for l, kind in enumerate(self.kinds):
             ql, kl, vl = q[l], k_caches[l], v_caches[l]
             if kind == KIND_REUSE:
-                ops.sparse_decode(ql, kl, vl, seq_len, self.full_idx, self.full_cnt, self.maps[l], out=loc.out[l])
+                ops.sparse_decode(ql, kl, vl, seq_len, self.full_idx, self.full_cnt, self.maps[l], out=loc.out[l],
+                                  workspace=ws)
                 continue
             if kind == KIND_ANCHOR0:
                 ops.dense_decode(ql, kl, vl, seq_len, out=loc.out[l], lse=loc.lse, scores=loc.scores,
-                                 seq_lens=seq_lens)
+                                 seq_lens=seq_lens, workspace=ws)
             else:
-                ops.anchor_scores_decode(ql, kl, seq_len, loc.scores, loc.lse, seq_lens=seq_lens)
+                ops.anchor_scores_decode(ql, kl, seq_len, loc.scores, loc.lse, seq_lens=seq_lens, workspace=ws)
             ops.select_decode(loc.scores, loc.lse, seq_len, pol, self.Hloc, indices=loc.indices, counts=loc.counts,
                               pooled=loc.pooled, seq_lens=seq_lens)
             # the exchange overlaps the anchor's own sparse pass, which only
             # needs this rank's lists (SURVEY.md 8(e))
-            pending = PendingIndexGather(loc.indices, loc.counts, self.group, head_dim=1)
+            self.exchange.start()
             if kind == KIND_ANCHOR:
-                ops.sparse_decode(ql, kl, vl, seq_len, loc.indices, loc.counts, None, out=loc.out[l])
-            idx, cnt = pending.wait()
-            self.full_idx[:, :, :idx.shape[2]].copy_(idx)
-            self.full_cnt.copy_(cnt)
+                ops.sparse_decode(ql, kl, vl, seq_len, loc.indices, loc.counts, None, out=loc.out[l], workspace=ws)
+            self.exchange.finish()
         return loc.out
+
+    def capture(self, q, k_caches, v_caches, seq_len: int, dense: bool = False, seq_lens=None):
+        """The whole sharded step (kernels + index-list all-gathers) as one
+        CUDA graph; ``dense`` captures the local Top-k = 100% baseline."""
+        if dense:
+            return self.local.capture(q, k_caches, v_caches, seq_len, dense=True, seq_lens=seq_lens)
+        self.step(q, k_caches, v_caches, seq_len, seq_lens)   # communicator + kernel attributes outside capture
+        torch.cuda.synchronize()
+        if self.exchange.staged:
+            raise InvalidArgumentError("a gloo-staged exchange cannot be captured (NCCL only)")
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step(q, k_caches, v_caches, seq_len, seq_lens)
+        self._graphs[(seq_len, dense)] = g
+        return g
 
     def gather_outputs(self) -> torch.Tensor:
         """[L][B][Hq][d] reassembled from every rank's heads."""
@@ -200,12 +277,13 @@ class ShardedKascadePrefill:
     """KV-head-sharded prefill executor (one rank's share; SURVEY.md 8(e)
     prefill partitioning).  Each anchor layer selects on the local kv heads
     and all-gathers its per-(kv head, tile) lists (<= 205 MiB per layer at
-    128K over 8 heads); reuse layers gather through the GLOBAL head map."""
+    128K over 8 heads) straight into the all-heads list buffer; reuse layers
+    gather through the GLOBAL head map."""
 
     def __init__(self, plan, num_layers: int, num_q_heads: int, num_kv_heads: int, seq_len: int, group=None,
                  device=None):
         from . import engine
-        from .host_types import KIND_REUSE, MODE_ALL_HEADS_POOLED, k_budget, validate_plan
+        from .host_types import KIND_REUSE, MODE_ALL_HEADS_POOLED, validate_plan
         validate_plan(plan, num_layers, num_kv_heads)
         if plan.mode == MODE_ALL_HEADS_POOLED:
             raise InvalidArgumentError("all-heads-pooled mode needs every kv head's pooled vectors; "
@@ -220,10 +298,11 @@ class ShardedKascadePrefill:
         self.kinds = self.local.kinds
         self.maps = {l: local_head_map(plan.head_maps[l].map, self.g0, self.g1, dev)
                      for l, kind in enumerate(self.kinds) if kind == KIND_REUSE}
-        T = self.local.indices.shape[1]
-        kc = k_budget(plan.k_policy, seq_len)
+        T, kc = self.local.indices.shape[1], self.local.indices.shape[2]
         self.full_idx = torch.empty(num_kv_heads, T, kc, dtype=torch.int32, device=dev)
         self.full_cnt = torch.zeros(num_kv_heads, T, dtype=torch.int32, device=dev)
+        self.exchange = IndexExchange(self.local.indices, self.local.counts, self.full_idx, self.full_cnt,
+                                      group, head_dim=0)
 
     def forward(self, qs, ks, vs) -> torch.Tensor:
         """qs/ks/vs: this rank's head slices per layer ([Hq_loc][N][128] and
@@ -242,10 +321,12 @@ class ShardedKascadePrefill:
             else:
                 ops.anchor_lse_prefill(q, k, lse=loc.lse)
             ops.select_prefill(q, k, loc.lse, pol, indices=loc.indices, counts=loc.counts, pooled=loc.pooled)
-            pending = PendingIndexGather(loc.indices, loc.counts, self.group, head_dim=0)
+            self.exchange.start()
             if kind == KIND_ANCHOR:           # overlaps the exchange: own lists only
                 ops.sparse_prefill(q, k, v, loc.indices, loc.counts, None, out=loc.out[l])
-            idx, cnt = pending.wait()
-            self.full_idx.copy_(idx)
-            self.full_cnt.copy_(cnt)
+            self.exchange.finish()
         return loc.out
+
+    def gather_outputs(self) -> torch.Tensor:
+        """[L][Hq][N][d] reassembled from every rank's heads."""
+        return gather_head_outputs(self.local.out, self.group, head_dim=1)

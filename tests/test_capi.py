@@ -33,7 +33,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 
 def test_abi_version_and_k_budget(lib):
-    assert lib.kscd_abi_version() == 1
+    assert lib.kscd_abi_version() == 2
     # tiles.py:81-89 pins (pkg/tests/test_tiles.py:18-23)
     for n, k in ((64, 64), (1000, 128), (1280, 128), (4096, 409)):
         assert lib.kscd_k_budget(0.1, 128, n) == k
@@ -145,3 +145,28 @@ def test_workspace_covers_virtual_heads_of_large_groups(lib):
     # same query heads; one kv head with G = 32 needs counters for 2 virtual heads
     assert size(32, 1) >= 4 * 32 * 130 * 4 + 4 * 2 * 4
     assert size(32, 2) >= 4 * 32 * 130 * 4 + 4 * 2 * 4
+
+
+def test_integration_stub_matches_header():
+    """INTEGRATION.md's raw ctypes stub for kscd_decode_params lists every
+    member of the header's struct, in order (a short stub would make the
+    library read past the caller's struct)."""
+    from paper_2512_16391_b200 import _lib
+    text = open(os.path.join(REPO, "INTEGRATION.md")).read()
+    body = text[text.index("class kscd_decode_params"):]
+    body = body[:body.index("lib.kscd_sparse_decode.argtypes")]
+    stub = re.findall(r'\("(\w+)",', body)
+    assert stub == [f[0] for f in _lib.DecodeParams._fields_]
+
+
+def test_append_kv_rejects_positions_outside_the_cache(lib):
+    from paper_2512_16391_b200 import _lib
+    from paper_2512_16391_b200.exceptions import InvalidArgumentError
+    p = _lib.AppendKvParams(num_layers=1, batch=1, num_kv_heads=1, head_dim=128, position=16, kv_new=16,
+                            k_caches=16, v_caches=16, kv_stride_batch=128, kv_stride_head=128,
+                            cache_capacity=16)
+    with pytest.raises(InvalidArgumentError, match="outside the cache"):
+        _lib.call("kscd_append_kv", p, 0)
+    p.cache_capacity = 0
+    with pytest.raises(InvalidArgumentError, match="cache_capacity"):
+        _lib.call("kscd_append_kv", p, 0)

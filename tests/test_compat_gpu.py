@@ -240,6 +240,14 @@ def test_invalid_plans(cuda_ok):
     maps = {1: identity_head_map(2, reuse_layer=1, anchor_layer=2)}
     with pytest.raises(InvalidPlanError):
         compat.run_kascade(t, AnchorPlan(AnchorPlanCore([0, 2], 2, 0.0), head_maps=maps))
+    # a malformed head map raises HeadMap.validate's InvalidArgumentError
+    # unchanged, as runner.py:236 -> heads.py:37-47 does
+    from paper_2512_16391_b200 import HeadMap, InvalidArgumentError
+    for bad in ([0, 1, 0], [0, 2]):
+        maps = {1: HeadMap(1, 0, bad), 2: HeadMap(2, 0, [0, 1])}
+        with pytest.raises(InvalidArgumentError) as ei:
+            compat.run_kascade(t, AnchorPlan(AnchorPlanCore([0], 1, 0.0), head_maps=maps))
+        assert not isinstance(ei.value, InvalidPlanError)
 
 
 # ---------------------------------------------------------- head_dim < 128

@@ -21,13 +21,17 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, errq):
+def _worker(rank, world, port, errq, backend="gloo"):
     import torch.distributed as dist
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
-        dist.init_process_group("gloo", rank=rank, world_size=world)
-        torch.cuda.set_device(0)
+        dev = 0 if backend == "gloo" else rank          # NCCL: one GPU per rank
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo", rank=rank, world_size=world)
         from oracle import kascade_oracle as orc
         from paper_2512_16391_b200 import engine, sharding
         from paper_2512_16391_b200.host_types import AnchorPlan, AnchorPlanCore, HeadMap, KBudgetPolicy
@@ -42,14 +46,27 @@ def _worker(rank, world, port, errq):
         t = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)  # noqa: E731
         g0, g1 = sharding.kv_head_shard(Hkv)
         dec = sharding.ShardedKascadeDecoder(plan, L, B, Hq, Hkv, n)
-        dec.step(t(q[:, :, g0 * G:g1 * G]), [t(K[l][:, g0:g1]) for l in range(L)],
-                 [t(V[l][:, g0:g1]) for l in range(L)], n)
+        qs_, Ks_, Vs_ = t(q[:, :, g0 * G:g1 * G]), [t(K[l][:, g0:g1]) for l in range(L)], \
+            [t(V[l][:, g0:g1]) for l in range(L)]
+        if backend == "nccl":
+            # the whole sharded step, NCCL all-gathers included, as one CUDA graph
+            dec.capture(qs_, Ks_, Vs_, n).replay()
+        else:
+            dec.step(qs_, Ks_, Vs_, n)
         full = dec.gather_outputs().cpu().numpy()
         if rank == 0:
             ref = engine.KascadeDecoder(plan, L, B, Hq, Hkv, n)
             want = ref.step(t(q), [t(K[l]) for l in range(L)], [t(V[l]) for l in range(L)], n).cpu().numpy()
+            # the split-K factor follows the local (sequence, kv head) count,
+            # so outputs agree to the bf16 rounding of P per split
             err = np.abs(full - want).max()
             assert err < 2e-3, f"sharded decode differs from unsharded by {err}"
+            # the gathered lists of the last anchor ARE the unsharded lists
+            assert torch.equal(dec.full_cnt, ref.counts)
+            for b in range(B):
+                for g in range(Hkv):
+                    c = int(ref.counts[b, g])
+                    assert torch.equal(dec.full_idx[b, g, :c], ref.indices[b, g, :c]), (b, g)
         # prefill: [L][H][N][d]
         N = 600
         Qp = orc.bf16_round(rng.standard_normal((L, Hq, N, 128)).astype(np.float32))
@@ -58,13 +75,16 @@ def _worker(rank, world, port, errq):
         pf = sharding.ShardedKascadePrefill(plan, L, Hq, Hkv, N)
         loc = pf.forward([t(Qp[l, g0 * G:g1 * G]) for l in range(L)], [t(Kp[l, g0:g1]) for l in range(L)],
                          [t(Vp[l, g0:g1]) for l in range(L)])
-        allp = sharding.gather_head_outputs(loc, head_dim=1).float().cpu().numpy()
+        allp = pf.gather_outputs().float().cpu().numpy()
         if rank == 0:
             ref = engine.KascadePrefill(plan, L, Hq, Hkv, N)
             want = ref.forward([t(Qp[l]) for l in range(L)], [t(Kp[l]) for l in range(L)],
                                [t(Vp[l]) for l in range(L)]).float().cpu().numpy()
-            err = np.abs(allp - want).max()
-            assert err < 2e-2, f"sharded prefill differs from unsharded by {err}"
+            # every (head, tile) runs the same CTA program on the same inputs
+            # with or without sharding: outputs and lists are bit-exact
+            assert np.array_equal(allp, want), f"sharded prefill differs by {np.abs(allp - want).max()}"
+            assert torch.equal(pf.full_cnt, ref.counts)
+            assert torch.equal(pf.full_idx, ref.indices)
         dist.barrier()
         dist.destroy_process_group()
     except Exception as e:  # reported to the parent
@@ -78,6 +98,27 @@ def test_kv_head_sharded_executors_match_unsharded(cuda_ok):
     errq = ctx.SimpleQueue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, 2, port, errq)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    msgs = []
+    while not errq.empty():
+        msgs.append(errq.get())
+    assert not msgs, msgs
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="NCCL across ranks needs >= 2 GPUs (NCCL rejects two ranks on one device)")
+def test_kv_head_sharded_executors_nccl_two_gpus(cuda_ok):
+    """The same check over NCCL on two GPUs, with the sharded decode step
+    captured as one CUDA graph (kernels + index-list all-gathers)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    errq = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, errq, "nccl")) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:
