@@ -360,7 +360,8 @@ def dense_row(q: np.ndarray, Kg: np.ndarray, Vg: np.ndarray, want_y: bool = True
 def decode_step(q: np.ndarray, K: np.ndarray, V: np.ndarray, anchors: Sequence[int],
                 head_maps: Dict[int, Sequence[int]], fraction: float, k_min: int,
                 pooling: str = POST, mode: str = REMAPPED, want_mass: bool = True,
-                layers: Optional[Iterable[int]] = None, timings: Optional[Dict[int, float]] = None):
+                layers: Optional[Iterable[int]] = None, timings: Optional[Dict[int, float]] = None,
+                pooled_out: Optional[Dict[int, List[np.ndarray]]] = None):
     """One decode step (the last token t = n-1) of ``run_kascade(phase=
     'decode')`` for one sequence, in O(n) per layer.
 
@@ -368,7 +369,13 @@ def decode_step(q: np.ndarray, K: np.ndarray, V: np.ndarray, anchors: Sequence[i
     the token itself.  Returns (Y [L][Hq][d], sels {layer: [Hkv] arrays of the
     selection used by that layer}, mass [L][Hq]).  Tile = [n-1, n), causal
     bound n, k = k_budget(n) (runner.py:199-206, tiles.py:145-150).
-    ``timings`` (optional) receives the wall time of every layer."""
+    ``timings`` (optional) receives the wall time of every layer;
+    ``pooled_out`` (optional) the pooled vector of every kv head of every
+    anchor layer (the ranking the selection was taken from).
+
+    K and V are only indexed as K[l, g] (one head's rows) and K[l, g, sel]
+    (a gather), so any object with that indexing and a ``shape`` works --
+    the scale tests pass lazy views of device caches."""
     L, Hq, d = q.shape
     Hkv, n = K.shape[1], K.shape[2]
     G = Hq // Hkv
@@ -389,7 +396,7 @@ def decode_step(q: np.ndarray, K: np.ndarray, V: np.ndarray, anchors: Sequence[i
         Yd = np.zeros((Hq, d), np.float32)
         if l == 0 or want_mass or (is_anchor and pooling == POST):
             for h in range(Hq):
-                P[h, 0], y = dense_row(q[l, h], K[l, h // G], V[l, h // G], want_y=l == 0)
+                P[h, 0], y = dense_row(q[l, h], K[l, h // G], V[l, h // G] if l == 0 else None, want_y=l == 0)
                 if y is not None:
                     Yd[h] = y
         if is_anchor:
@@ -399,9 +406,11 @@ def decode_step(q: np.ndarray, K: np.ndarray, V: np.ndarray, anchors: Sequence[i
                     pooled[(g, n - 1)] = P[g * G:(g + 1) * G, 0:1, :n].mean(axis=(0, 1), dtype=np.float64)
                 else:
                     qbar = q[l, g * G:(g + 1) * G].astype(np.float32).mean(axis=0, dtype=np.float64)
-                    s = (K[l, g].astype(np.float64) @ qbar) / math.sqrt(d)
+                    s = (np.asarray(K[l, g], dtype=np.float64) @ qbar) / math.sqrt(d)
                     pooled[(g, n - 1)] = softmax_vec(s).astype(np.float64)
             cur = select(pooled, {n - 1: n}, fraction, k_min, mode, Hkv)
+            if pooled_out is not None:
+                pooled_out[l] = [pooled[(g, n - 1)] for g in range(Hkv)]
         if l == 0:
             Y[0] = Yd
             mass[0] = 1.0

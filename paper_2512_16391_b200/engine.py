@@ -258,11 +258,14 @@ class KascadePrefill:
         self.out = torch.empty(num_layers, num_q_heads, seq_len, 128, dtype=torch.bfloat16, device=dev)
 
     def forward(self, qs: Sequence[torch.Tensor], ks: Sequence[torch.Tensor], vs: Sequence[torch.Tensor],
-                layers: Optional[Sequence[int]] = None) -> torch.Tensor:
+                stop_after: Optional[int] = None) -> torch.Tensor:
         """qs/ks/vs: per-layer [Hq][N][128] / [Hkv][N][128] bf16.  Returns the
-        bf16 outputs [L][Hq][N][128]."""
+        bf16 outputs [L][Hq][N][128].  ``stop_after`` ends the loop after that
+        layer (the index lists then hold that layer's latest anchor sets)."""
         pol = self.plan.k_policy
         for l, kind in enumerate(self.kinds):
+            if stop_after is not None and l > stop_after:
+                break
             q, k, v = qs[l], ks[l], vs[l]
             if kind == KIND_REUSE:
                 ops.sparse_prefill(q, k, v, self.indices, self.counts, self.head_maps[l], out=self.out[l])
