@@ -159,32 +159,48 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- CPU oracle
-class CpuDecodeSample:
-    """The CPU oracle (restating the reference's decode path) on ONE
-    sequence: one layer of each kind (anchor0, reuse, anchor) at the bench
-    context, composed to a 32-layer step.  Inputs are drawn once."""
+class _LayerPool:
+    """K or V of a 32-layer cache for the O(n) oracle, built from a pool of
+    distinct layer buffers cycled over the layers (each 0.5 GB of fp32 at
+    128K, far above the host's last-level cache, so cycling gains nothing)."""
 
-    def __init__(self, ctx, fraction, k_min):
+    def __init__(self, pool, L):
+        self.pool = pool
+        self.shape = (L,) + pool[0].shape
+
+    def __getitem__(self, key):
+        a = self.pool[key[0] % len(self.pool)]
+        return a[key[1]] if len(key) == 2 else a[key[1], key[2]]
+
+
+class CpuDecodeSample:
+    """The CPU oracle (restating the reference's decode path, runner.py:
+    228-297 for one token) on ONE sequence of the bench workload: all 32
+    layers of the Llama plan (anchors [0,2,8,13,14], its head maps) timed,
+    none composed.  Inputs are drawn once."""
+
+    def __init__(self, ctx, fraction, k_min, distinct=4):
         from oracle import kascade_oracle as orc
         self.orc = orc
+        L, Hq, Hkv = CFG["layers"], CFG["Hq"], CFG["Hkv"]
         rng = np.random.default_rng(0)
-        L, Hq, Hkv = 3, CFG["Hq"], CFG["Hkv"]
-        self.q = orc.bf16_round(rng.standard_normal((L, Hq, 128)).astype(np.float32) * 2.0)
-        self.K = orc.bf16_round(rng.standard_normal((L, Hkv, ctx, 128)).astype(np.float32))
-        self.V = orc.bf16_round(rng.standard_normal((L, Hkv, ctx, 128)).astype(np.float32))
-        self.fraction, self.k_min = fraction, k_min
+        self.q = orc.bf16_round(rng.standard_normal((L, Hq, 128), dtype=np.float32) * 2.0)
+        kp = [orc.bf16_round(rng.standard_normal((Hkv, ctx, 128), dtype=np.float32)) for _ in range(distinct)]
+        vp = [orc.bf16_round(rng.standard_normal((Hkv, ctx, 128), dtype=np.float32)) for _ in range(distinct)]
+        self.K, self.V = _LayerPool(kp, L), _LayerPool(vp, L)
+        plan = make_plan(L, Hkv, LLAMA_ANCHORS, fraction, k_min)
+        self.maps = {l: m.map for l, m in plan.head_maps.items()}
+        self.fraction, self.k_min, self.distinct = fraction, k_min, distinct
 
     def step(self):
-        """Seconds per token of a composed 32-layer Kascade step, plus the
-        per-layer-kind times."""
+        """Seconds for one token of one sequence through all 32 layers, plus
+        the per-layer-kind medians (ms)."""
         t = {}
-        Hkv = CFG["Hkv"]
-        self.orc.decode_step(self.q, self.K, self.V, [0, 2], {1: list(range(Hkv))[::-1]}, self.fraction,
-                             self.k_min, want_mass=False, timings=t)
-        n_anchor = len(LLAMA_ANCHORS) - 1
-        n_reuse = CFG["layers"] - len(LLAMA_ANCHORS)
-        return t[0] + n_anchor * t[2] + n_reuse * t[1], {"anchor0_ms": t[0] * 1e3, "reuse_ms": t[1] * 1e3,
-                                                         "anchor_ms": t[2] * 1e3}
+        self.orc.decode_step(self.q, self.K, self.V, LLAMA_ANCHORS, self.maps, self.fraction, self.k_min,
+                             want_mass=False, timings=t)
+        kinds = {"anchor0_ms": [t[0]], "anchor_ms": [t[l] for l in LLAMA_ANCHORS[1:]],
+                 "reuse_ms": [v for l, v in t.items() if l not in LLAMA_ANCHORS]}
+        return sum(t.values()), {k: float(np.median(v)) * 1e3 for k, v in kinds.items()}, len(t)
 
     def dense_layer_s(self):
         """Dense rows of every head of one layer (the Top-k = 100% baseline)."""
@@ -193,6 +209,13 @@ class CpuDecodeSample:
         for h in range(Hq):
             self.orc.dense_row(self.q[0, h], self.K[0, h // G], self.V[0, h // G])
         return time.perf_counter() - t0
+
+    def describe(self, ctx, B):
+        return (f"one of the workload's {B} sequences per step (the CPU cost per token does not depend on the "
+                f"batch): all {CFG['layers']} layers of the Llama plan timed, none composed, at {ctx} ctx, "
+                f"k=k_budget(ctx); K/V from {self.distinct} distinct layer buffers cycled "
+                f"({self.K.pool[0].nbytes / 1e9:.2f} GB each, far above the host LLC); numpy oracle (oracle/kascade_oracle.py) restating the reference, "
+                f"BLAS threads = all host cores")
 
 
 def run_reference(args, rank):
@@ -203,25 +226,26 @@ def run_reference(args, rank):
     for _ in range(args.warmup):
         smp.step()
     per = []
-    detail = None
+    detail, n_layers = None, 0
     for _ in range(args.steps):
-        s_, detail = smp.step()
+        s_, detail, n_layers = smp.step()
         per.append(s_)
     detail["dense_ms"] = smp.dense_layer_s() * 1e3
-    us_tok = float(np.mean(per)) * 1e6
+    ms_step = float(np.mean(per)) * 1e3
+    us_tok = ms_step * 1e3          # one token (one sequence) per step
     line = {
         "metric": "decode-attn us/token @128K ctx (Kascade, Llama-3.1-8B shapes, k=10%)",
         "value": round(us_tok, 1), "unit": "us/token", "impl": "reference", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(us_tok / 1e3, 3),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic N(0,1) bf16-representable",
-        "config": {"workload": f"llama8b-decode-{args.ctx // 1024}k-b1-k{args.fraction:g} (CPU sample)",
-                   "ctx": args.ctx, "batch": 1, "anchors": LLAMA_ANCHORS},
+        "config": {"workload": f"llama8b-decode-{args.ctx // 1024}k-b{args.batch}-k{args.fraction:g}",
+                   "ctx": args.ctx, "batch": args.batch, "anchors": LLAMA_ANCHORS,
+                   "plan": "plans/llama8b.json", "sequences_per_step": 1},
         "cpu_baseline": {"value": round(us_tok, 1), "unit": "us/token", "cores": cores, "kind": "port",
-                         "sample": "one sequence; one anchor0, one reuse and one anchor layer timed per step, "
-                                   "composed to 32 layers (1 anchor0 + 4 anchor + 27 reuse); numpy oracle "
-                                   "restating the reference (BLAS threads = all host cores)",
-                         "per_layer": {k: round(v, 2) for k, v in detail.items()}},
+                         "sample": smp.describe(args.ctx, args.batch),
+                         "layers_timed": n_layers, "layers_composed": 0,
+                         "per_layer_ms": {k: round(v, 2) for k, v in detail.items()}},
         "e2e": {"value": round(us_tok, 1), "unit": "us/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -850,15 +874,13 @@ def main():
     # ---- CPU baseline (rank 0 only at N=1) -------------------------------
     cpu = None
     if not args.no_cpu_baseline and world == 1 and rank == 0:
-        ctx_cpu = n
-        smp = CpuDecodeSample(ctx_cpu, args.fraction, args.k_min)
-        step_s, detail = smp.step()
+        smp = CpuDecodeSample(n, args.fraction, args.k_min)
+        step_s, detail, n_layers = smp.step()
         detail["dense_ms"] = smp.dense_layer_s() * 1e3
-        del smp
         cpu = {"value": round(step_s * 1e6, 1), "unit": "us/token", "cores": os.cpu_count(), "kind": "port",
-               "sample": f"one sequence at {ctx_cpu} ctx: one anchor0, one reuse, one anchor layer timed, "
-                         "composed to 32 layers; numpy oracle with all host BLAS threads",
+               "sample": smp.describe(n, B), "layers_timed": n_layers, "layers_composed": 0,
                "per_layer_ms": {k_: round(v, 2) for k_, v in detail.items()}}
+        del smp
 
     us_tok = ms_kas * 1e3 / (B * world)
     launches_per_step = 3 + 4 * (len(LLAMA_ANCHORS) - 1) + (L - len(LLAMA_ANCHORS))
