@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--k-min", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity-sample", action="store_true",
+                    help="skip checking one sampled sequence / tile of the run against the CPU oracle")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the BASELINE.json configs[1..4] section")
     ap.add_argument("--best-of", action="store_true", help="report the better of two timed regions")
@@ -251,6 +253,105 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------ parity sample (checker)
+class _DeviceKV:
+    """Lazy fp32 view of ONE sequence's per-layer device caches for the
+    oracle's decode_step: K[l, g] -> that head's rows, K[l, g, sel] -> the
+    selected rows gathered on the device."""
+
+    def __init__(self, caches, b, n):
+        self.caches, self.b, self.n = caches, b, n
+        self.shape = (len(caches), caches[0].shape[1], n, 128)
+        self._memo = None
+
+    def __getitem__(self, key):
+        import torch
+        l, g = key[0], key[1]
+        if len(key) == 2:
+            if self._memo is None or self._memo[0] != (l, g):
+                self._memo = ((l, g), self.caches[l][self.b, g, :self.n].float().cpu().numpy())
+            return self._memo[1]
+        sel = torch.from_numpy(np.ascontiguousarray(key[2], dtype=np.int64)).to(self.caches[l].device)
+        return self.caches[l][self.b, g].index_select(0, sel).float().cpu().numpy()
+
+
+def _close(got, ref):
+    err = np.abs(np.asarray(got, np.float64) - np.asarray(ref, np.float64))
+    rel = float(np.linalg.norm(err) / max(np.linalg.norm(np.asarray(ref, np.float64)), 1e-30))
+    return {"max_abs": float(err.max()), "mean_abs": float(err.mean()), "rel_l2": rel,
+            "ok": bool(err.max() <= 2e-2 and err.mean() <= 1e-3)}
+
+
+def _swaps(got, ref, scores, rel=1e-5):
+    """Near-tie swaps between two index sets (tests/parity.py rule); -1 if a
+    difference is not a near-tie of the reference k-th score."""
+    got, ref = np.asarray(got, np.int64), np.asarray(ref, np.int64)
+    diff = np.setxor1d(got, ref)
+    if diff.size == 0 and got.size == ref.size:
+        return 0
+    s = np.asarray(scores, np.float64)
+    kth = np.sort(s[ref])[0]
+    if got.size != ref.size or any(abs(s[j] - kth) > rel * abs(kth) for j in diff):
+        return -1
+    return int(diff.size // 2)
+
+
+def decode_parity_sample(out, q, Ks, Vs, n, plan, idx_last, cnt_last, b):
+    """Checker, outside every timed region: sequence b of the bench's own
+    decode step (all layers, the bench's inputs and index lists) against the
+    O(n) oracle (oracle/kascade_oracle.py decode_step)."""
+    from oracle import kascade_oracle as orc
+    t0 = time.perf_counter()
+    maps = {l: m.map for l, m in plan.head_maps.items()}
+    pooled = {}
+    Y, sels, _ = orc.decode_step(q[:, b].float().cpu().numpy(), _DeviceKV(Ks, b, n), _DeviceKV(Vs, b, n),
+                                 plan.anchors, maps, plan.k_policy.fraction, plan.k_policy.k_min,
+                                 want_mass=False, pooled_out=pooled)
+    la = max(plan.anchors)
+    swaps = [_swaps(idx_last[b, g, :cnt_last[b, g]], sels[la][g], pooled[la][g]) for g in range(idx_last.shape[1])]
+    res = _close(out[:, b], Y)
+    res.update({"sequence": int(b), "layers": int(out.shape[0]), "last_anchor": la,
+                "last_anchor_swaps": swaps, "sets_ok": all(x >= 0 for x in swaps),
+                "oracle_s": round(time.perf_counter() - t0, 1)})
+    return res
+
+
+def prefill_parity_sample(out, Q, K, V, plan, idx, cnt, tile, g, reuse_layer):
+    """Checker: one (kv head, tile) of the bench's own 128K prefill -- the
+    last anchor's selection (prefill_tile_select) and a reuse layer's output
+    on that tile through its head map (sparse_tile)."""
+    from oracle import kascade_oracle as orc
+    t0 = time.perf_counter()
+    la = max(plan.anchors)
+    Hq, N = Q[0].shape[0], Q[0].shape[1]
+    Hkv = K[0].shape[0]
+    G = Hq // Hkv
+    s, e = 128 * tile, min(N, 128 * tile + 128)
+    src = plan.head_maps[reuse_layer].map[g]
+    pol = plan.k_policy
+
+    def host(l, h0, h1, kv_head):
+        # only the heads this tile needs, as [H][N][d] / [1][N][d] fp32
+        return (Q[l][h0:h1].float().cpu().numpy(), K[l][kv_head:kv_head + 1].float().cpu().numpy(),
+                V[l][kv_head:kv_head + 1].float().cpu().numpy())
+
+    swaps = []
+    ref_sets = {}
+    for head in sorted({g, src}):
+        Ql, Kl, _ = host(la, head * G, (head + 1) * G, head)
+        sel, pooled = orc.prefill_tile_select(Ql, Kl, 0, G, s, e, pol.fraction, pol.k_min)
+        c = int(cnt[head, tile])
+        swaps.append(_swaps(idx[head, tile, :c], sel, pooled))
+        ref_sets[head] = sel
+    Ql, Kl, Vl = host(reuse_layer, g * G, (g + 1) * G, g)
+    y, _, _ = orc.sparse_tile(Ql, Kl, Vl, 0, G, s, e, ref_sets[src])
+    res = _close(out[reuse_layer, g * G:(g + 1) * G, s:e].float().cpu().numpy(), y)
+    res.update({"tile": int(tile), "kv_head": int(g), "anchor_layer": la, "anchor_swaps": swaps,
+                "sets_ok": all(x >= 0 for x in swaps), "reuse_layer": int(reuse_layer), "routed_from": int(src),
+                "oracle_s": round(time.perf_counter() - t0, 1)})
+    return res
+
+
 # ------------------------------------------------------------------ prefill
 def cpu_prefill_sample(N, fraction, k_min, tiles=(0.25, 0.5, 0.75, 1.0)):
     """CPU oracle (the reference algorithm) on a bounded sample of one 128K
@@ -375,6 +476,14 @@ def bench_prefill(args, dev, world, dist):
     tpk = float(peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"]))
     n_anchor, n_reuse = len(LLAMA_ANCHORS) - 1, L - len(LLAMA_ANCHORS)
     weighted = (t_a0 + n_anchor * t_anchor + n_reuse * t_reuse) / L
+    parity = None
+    if not args.no_parity_sample and int(os.environ.get("RANK", "0")) == 0:
+        # re-run the forward so the lists are the last anchor's and every
+        # layer's output is this forward's (the timing loops overwrote them)
+        eng.forward(Q, K, V)
+        torch.cuda.synchronize()
+        parity = prefill_parity_sample(eng.out, Q, K, V, plan, eng.indices.cpu().numpy(),
+                                       eng.counts.cpu().numpy(), tile=T - 1, g=3, reuse_layer=L - 1)
     del qs, ks, vs, Q, K, V, eng
     torch.cuda.empty_cache()
     cpu_prefill = None
@@ -413,6 +522,7 @@ def bench_prefill(args, dev, world, dist):
                                 "frac": round(gather_bytes / (t_reuse * 1e-3) / 1e9 / gather_peak, 4)
                                 if gather_peak else None}},
         "gpu_launches_per_step": 1 * 3 + n_anchor * 4 + n_reuse,
+        "parity_sample": parity,
         "cpu_baseline": cpu_prefill,
     }
 
@@ -859,6 +969,14 @@ def main():
                        "of all 32 layers' outputs (copies pipelined against the layers on two graph branches); "
                        "host-synchronised every step"}
 
+    # ---- parity sample (checker; outside every timed region) -------------
+    parity = None
+    if not args.no_parity_sample and rank == 0:
+        g_kas.replay()             # the timed graph's state: outputs and the last anchor's lists
+        torch.cuda.synchronize()
+        parity = decode_parity_sample(dec.out.cpu().numpy(), q, Ks, Vs, n, plan, dec.indices.cpu().numpy(),
+                                      dec.counts.cpu().numpy(), b=B - 1)
+
     # ---- prefill at 128K (secondary metric of the same line) -------------
     del g_kas, g_den, dec, Kc, Vc, Ks, Vs, q
     torch.cuda.synchronize()
@@ -918,6 +1036,7 @@ def main():
                                          "launch's ramp with the previous tail), events around the chain only; "
                                          "achieved/frac above are per isolated launch"}},
         "clocks": clk,
+        "parity_sample": parity,
         "gpu_launches": launches_per_step * args.steps,
         "cpu_baseline": cpu,
         "e2e": e2e,

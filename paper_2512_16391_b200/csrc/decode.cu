@@ -356,9 +356,7 @@ static cudaError_t launch_mode(const DecodeArgs& a, cudaStream_t st) {
       decode_attn_kernel<MODE, false, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (attr_hi != cudaSuccess) return attr_hi;
   if (attr_lo != cudaSuccess) return attr_lo;
-  // programmatic stream serialization (see the kernel's PDL note);
-  // KSCD_NO_PDL=1 (dev knob) launches with plain stream order
-  static const bool pdl = !getenv("KSCD_NO_PDL");
+  // programmatic stream serialization (see the kernel's PDL note)
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kThreads);
@@ -368,21 +366,15 @@ static cudaError_t launch_mode(const DecodeArgs& a, cudaStream_t st) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = 1;
   if (a.G > 8) return cudaLaunchKernelEx(&cfg, decode_attn_kernel<MODE, true, STG>, a);
   return cudaLaunchKernelEx(&cfg, decode_attn_kernel<MODE, false, STG>, a);
 }
 
 cudaError_t launch_decode_attn(int mode, const DecodeArgs& a, cudaStream_t st) {
-  // KSCD_SPARSE_STAGES (dev knob): ring depth of the gather kernel
-  static const int sparse_stages = getenv("KSCD_SPARSE_STAGES") ? atoi(getenv("KSCD_SPARSE_STAGES")) : 3;
   switch (mode) {
     case MODE_DENSE: return launch_mode<MODE_DENSE>(a, st);
-    case MODE_SPARSE:
-      if (sparse_stages == 6) return launch_mode<MODE_SPARSE, 6>(a, st);
-      if (sparse_stages == 4) return launch_mode<MODE_SPARSE, 4>(a, st);
-      if (sparse_stages == 2) return launch_mode<MODE_SPARSE, 2>(a, st);
-      return launch_mode<MODE_SPARSE>(a, st);
+    case MODE_SPARSE: return launch_mode<MODE_SPARSE>(a, st);
     default: return launch_mode<MODE_SCORES>(a, st);
   }
 }

@@ -73,7 +73,6 @@ struct TopkArgs {
   int tile, T;
   double fraction;
   int k_min;
-  int cand_off;                           // 1: skip the on-chip candidate copy (dev knob KSCD_TOPK_NOCAND)
   // ragged decode batch: when seq_div > 0, row r has length
   // min(len, seq_lens[r / seq_div]) and k = k_budget(fraction, k_min, length)
   const int* seq_lens;

@@ -535,7 +535,6 @@ static cudaError_t launch_prefill_mode(const PrefillArgs& a, cudaStream_t st) {
     prefill_attn_kernel<MODE><<<grid, pf::kThreads, pf::kSmemBytes, st>>>(tm, a);
     return cudaGetLastError();
   }
-  static const bool pdl = !getenv("KSCD_NO_PDL");
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(pf::kThreads);
@@ -545,18 +544,12 @@ static cudaError_t launch_prefill_mode(const PrefillArgs& a, cudaStream_t st) {
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, prefill_attn_kernel<MODE>, tm, a);
 }
 
-bool prefill_pair_supported(int mode, const PrefillArgs& a);
-cudaError_t launch_prefill_pair(int mode, const PrefillArgs& a, cudaStream_t st);
-
 cudaError_t launch_prefill_attn(int mode, const PrefillArgs& a, cudaStream_t st) {
-  // CTA pairs (prefill_pair.cu, 2-SM UMMA) are opt-in (KSCD_PREFILL_PAIR=1):
-  // measured slower than the single-CTA ping-pong.
-  static const char* knob = getenv("KSCD_PREFILL_PAIR");
-  if (knob && knob[0] == '1' && prefill_pair_supported(mode, a)) return launch_prefill_pair(mode, a, st);
+  // (a CTA-pair variant on 2-SM UMMA was measured slower and removed)
   switch (mode) {
     case PMODE_DENSE: return launch_prefill_mode<PMODE_DENSE>(a, st);
     case PMODE_SPARSE: return launch_prefill_mode<PMODE_SPARSE>(a, st);

@@ -165,7 +165,7 @@ struct TopkShared {
   uint32_t cand[kRadixCandCap];    // candidate keys (threshold bin of digit 0)
 };
 
-template <int CL, int AGG>
+template <int CL>
 __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
   __shared__ TopkShared sh;
   cg::cluster_group cluster = cg::this_cluster();
@@ -244,15 +244,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
           const uint32_t key = order_key(v[b][i]);
           const bool m = (j + i < seg1) && ((key & pmask) == prefix);
           const uint32_t bin = (key >> shift) & (nb - 1);
-          if (AGG) {
-            const uint32_t act = __ballot_sync(0xffffffffu, m);
-            if (m) {
-              const uint32_t peers = __match_any_sync(act, bin);
-              if (lane == __ffs(peers) - 1) atomicAdd(&sh.hist[bin], (uint32_t)__popc(peers));
-            }
-          } else if (m) {
-            atomicAdd(&sh.hist[bin], 1u);
-          }
+          if (m) atomicAdd(&sh.hist[bin], 1u);
         }
       }
     }
@@ -333,7 +325,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
     // only when the bin's cluster-wide count says the copy will (very
     // likely) fit: long prefill rows of near-uniform attention put most of a
     // row in one bin, and a wasted copy pass costs more than it saves
-    if (pass == 0 && !a.cand_off && sh.sel_cnt <= (uint32_t)(CL == 1 ? kRadixCandCap : kRadixCandCap * CL / 2)) {
+    if (pass == 0 && sh.sel_cnt <= (uint32_t)(CL == 1 ? kRadixCandCap : kRadixCandCap * CL / 2)) {
       // copy the threshold bin's keys on chip and count the keys above it
       const uint32_t hi_key = prefix | 0x000fffffu;
       uint32_t ab = 0;
@@ -460,247 +452,14 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(const TopkArgs a) {
   }
 }
 
-// --------------------------------------------- sample-bracketed Top-k
-// One CTA (1024 threads) per row.  A deterministic sample of 4096 keys is
-// sorted in shared memory and brackets the k-th key: [lo, hi] around the
-// expected rank +- 6 sigma.  ONE pass over the row then counts the keys above
-// hi (ballot/popc, no per-key atomics) and appends the bracketed candidates
-// to shared memory; the exact k-th key is radix-selected among the
-// candidates.  If the bracket misses or overflows (heavy ties, adversarial
-// rows) the kernel falls back to the full-row radix select, so the result
-// is always exact.  The ordered compaction pass is the same as above.
-constexpr int kFastThreads = 1024;
-constexpr int kFastWarps = kFastThreads / 32;
-constexpr int kSample = 4096;
-constexpr int kCandCap = 16384;
-
-struct FastShared {
-  uint32_t sample[kSample];
-  uint32_t cand[kCandCap];
-  uint32_t hist[4096];
-  uint32_t scan_buf[33];
-  uint32_t cnt_above, cnt_cand;
-  uint32_t sel_bin, sel_above;
-};
-
-KSCD_DEV uint32_t block_excl_scan_1024(uint32_t v, uint32_t* warp_tot, uint32_t& total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) warp_tot[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    const uint32_t w = warp_tot[lane];
-    uint32_t wx = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, wx, o);
-      if (lane >= o) wx += y;
-    }
-    warp_tot[lane] = wx - w;
-    if (lane == 31) warp_tot[32] = wx;
-  }
-  __syncthreads();
-  const uint32_t res = warp_tot[warp] + x - v;
-  total = warp_tot[32];
-  __syncthreads();
-  return res;
-}
-
-// Exact radix select of the take-th largest key among n keys key_at(i).
-template <class KeyAt>
-KSCD_DEV void radix_select_block(KeyAt key_at, int n, uint32_t take, FastShared& sh, uint32_t& T, uint32_t& r_eq) {
-  const int tid = threadIdx.x;
-  uint32_t prefix = 0, pmask = 0, remaining = take;
-#pragma unroll 1
-  for (int pass = 0; pass < 3; ++pass) {
-    const int shift = pass == 0 ? 20 : (pass == 1 ? 8 : 0);
-    const int nb = pass == 2 ? 256 : 4096;
-    for (int i = tid; i < nb; i += kFastThreads) sh.hist[i] = 0;
-    __syncthreads();
-    for (int i = tid; i < n; i += kFastThreads) {
-      const uint32_t key = key_at(i);
-      if ((key & pmask) == prefix) atomicAdd(&sh.hist[(key >> shift) & (nb - 1)], 1u);
-    }
-    __syncthreads();
-    uint32_t local = 0;
-    const int top = nb - 1 - 4 * tid;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (top - i >= 0) local += sh.hist[top - i];
-    uint32_t tot;
-    uint32_t above = block_excl_scan_1024(local, sh.scan_buf, tot);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int bin = top - i;
-      if (bin >= 0) {
-        const uint32_t c = sh.hist[bin];
-        if (above < remaining && above + c >= remaining) {
-          sh.sel_bin = bin;
-          sh.sel_above = above;
-        }
-        above += c;
-      }
-    }
-    __syncthreads();
-    prefix |= sh.sel_bin << shift;
-    pmask |= (uint32_t)(nb - 1) << shift;
-    remaining -= sh.sel_above;
-    __syncthreads();
-  }
-  T = prefix;
-  r_eq = remaining;
-}
-
-__global__ void __launch_bounds__(kFastThreads) topk_sample_kernel(const TopkArgs a) {
-  extern __shared__ __align__(16) uint8_t fast_smem[];
-  FastShared& sh = *reinterpret_cast<FastShared*>(fast_smem);
-  const int r = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
-  int n = a.lens ? a.lens[r] : a.len;
-  int k = a.ks ? a.ks[r] : a.k;
-  if (a.tile > 0) {
-    n = min(a.len, a.tile * (r % a.T + 1));
-    long long kk = (long long)floor(a.fraction * (double)n);
-    kk = kk < a.k_min ? a.k_min : kk;
-    k = (int)(kk > n ? n : kk);
-  }
-  const uint32_t take = (uint32_t)(n < k ? n : k);
-  const float* vals = a.vals + (int64_t)r * a.val_stride;
-  const float* vals2 = a.vals2 ? a.vals2 + (int64_t)r * a.val_stride : nullptr;
-  int* out = a.idx + (int64_t)r * a.k_cap;
-  const bool vec = ((reinterpret_cast<uintptr_t>(vals) & 15) == 0);
-  if (tid == 0) a.counts[r] = take;
-  for (int j = take + tid; j < a.k_cap; j += kFastThreads) out[j] = 0x7fffffff;
-  if (take == 0) return;
-  if ((int)take == n) {
-    for (int j = tid; j < n; j += kFastThreads) out[j] = j;
-    return;
-  }
-  auto key_global = [&](int j) -> uint32_t {
-    return order_key(__ldcg(vals + j) + (vals2 ? __ldcg(vals2 + j) : 0.f));
-  };
-  uint32_t T, r_eq;
-  if (n < 4 * kSample) {
-    // short rows (early prefill tiles): the full radix select is already cheap
-    radix_select_block(key_global, n, take, sh, T, r_eq);
-  } else {
-
-  // ---- sample and bracket ------------------------------------------------
-  for (int i = tid; i < kSample; i += kFastThreads) sh.sample[i] = key_global((int)(((int64_t)i * n) / kSample));
-  if (tid == 0) {
-    sh.cnt_above = 0;
-    sh.cnt_cand = 0;
-  }
-  __syncthreads();
-  for (int kk = 2; kk <= kSample; kk <<= 1) {           // bitonic sort, descending
-    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-      for (int i = tid; i < kSample; i += kFastThreads) {
-        const int ixj = i ^ jj;
-        if (ixj > i) {
-          const uint32_t x = sh.sample[i], y = sh.sample[ixj];
-          const bool desc = (i & kk) == 0;
-          if (desc ? (x < y) : (x > y)) {
-            sh.sample[i] = y;
-            sh.sample[ixj] = x;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  const double q = (double)take / (double)n;
-  const double sigma = sqrt((double)kSample * q * (1.0 - q));
-  const int expect = (int)ceil(q * kSample);
-  const int delta = (int)(6.0 * sigma) + 8;
-  const int hi_rank = expect - delta - 1, lo_rank = expect + delta;
-  const uint32_t hi_key = hi_rank < 0 ? 0xffffffffu : sh.sample[hi_rank];
-  const uint32_t lo_key = lo_rank >= kSample ? 0u : sh.sample[lo_rank];
-
-  // ---- one pass: count keys above the bracket, collect the bracket --------
-  uint32_t above_local = 0;
-  const int iters = (n + 4 * kFastThreads - 1) / (4 * kFastThreads);
-  for (int it = 0; it < iters; ++it) {
-    const int j = (it * kFastThreads + tid) * 4;
-    float v4[1][4];
-    load_groups<1>(vals, vals2, j, 0, n, vec, v4);
-    const float (&v)[4] = v4[0];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t key = order_key(v[i]);
-      const bool ok = j + i < n;
-      above_local += ok && key > hi_key;
-      const bool cnd = ok && key <= hi_key && key >= lo_key;
-      const uint32_t m = __ballot_sync(0xffffffffu, cnd);
-      if (m) {
-        uint32_t base = 0;
-        if (lane == __ffs(m) - 1) base = atomicAdd(&sh.cnt_cand, (uint32_t)__popc(m));
-        base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-        const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
-        if (cnd && pos < kCandCap) sh.cand[pos] = key;
-      }
-    }
-  }
-  above_local = warp_sum(above_local);
-  if (lane == 0) atomicAdd(&sh.cnt_above, above_local);
-  __syncthreads();
-  const uint32_t cA = sh.cnt_above, cC = sh.cnt_cand;
-  if (cA < take && take <= cA + cC && cC <= (uint32_t)kCandCap) {
-    radix_select_block([&](int i) -> uint32_t { return sh.cand[i]; }, (int)cC, take - cA, sh, T, r_eq);
-  } else {
-    radix_select_block(key_global, n, take, sh, T, r_eq);     // exact fallback
-  }
-  }  // long rows
-
-  // ---- ordered compaction ------------------------------------------------
-  uint32_t gt_carry = 0, eq_carry = 0;
-  const int chunk = kFastThreads * kTopkItems;
-#pragma unroll 1
-  for (int base = 0; base < n; base += chunk) {
-    uint32_t keys[kTopkItems];
-    uint32_t gt = 0, eq = 0;
-    const int j0 = base + tid * kTopkItems;
-    {
-      float v[kTopkItems / 4][4];
-      load_groups<kTopkItems / 4>(vals, vals2, j0, 4, n, vec, v);
-#pragma unroll
-      for (int h = 0; h < kTopkItems; ++h) keys[h] = order_key(v[h / 4][h % 4]);
-    }
-#pragma unroll
-    for (int i = 0; i < kTopkItems; ++i) {
-      const bool ok = j0 + i < n;
-      gt += (ok && keys[i] > T);
-      eq += (ok && keys[i] == T);
-    }
-    uint32_t tot;
-    const uint32_t pre = block_excl_scan_1024((eq << 16) | gt, sh.scan_buf, tot);
-    uint32_t g_before = gt_carry + (pre & 0xffffu);
-    uint32_t e_before = eq_carry + (pre >> 16);
-#pragma unroll
-    for (int i = 0; i < kTopkItems; ++i) {
-      const int j = j0 + i;
-      if (j >= n) break;
-      const bool is_gt = keys[i] > T, is_eq = keys[i] == T;
-      if (is_gt || (is_eq && e_before < r_eq)) out[g_before + min(e_before, r_eq)] = j;
-      g_before += is_gt;
-      e_before += is_eq;
-    }
-    gt_carry += tot & 0xffffu;
-    eq_carry += tot >> 16;
-  }
-}
-
-template <int CL, int AGG>
+template <int CL>
 static cudaError_t launch_topk_cl(const TopkArgs& a, cudaStream_t st) {
   if (CL == 1) {
-    topk_kernel<1, AGG><<<a.rows, kTopkThreads, 0, st>>>(a);
+    topk_kernel<1><<<a.rows, kTopkThreads, 0, st>>>(a);
     return cudaGetLastError();
   }
   if (CL > 8) {
-    static const cudaError_t np = cudaFuncSetAttribute(topk_kernel<CL, AGG>,
+    static const cudaError_t np = cudaFuncSetAttribute(topk_kernel<CL>,
                                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (np != cudaSuccess) return np;
   }
@@ -716,44 +475,20 @@ static cudaError_t launch_topk_cl(const TopkArgs& a, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, topk_kernel<CL, AGG>, a);
+  return cudaLaunchKernelEx(&cfg, topk_kernel<CL>, a);
 }
 
-cudaError_t launch_topk(const TopkArgs& a_in, cudaStream_t st) {
-  if (a_in.rows <= 0) return cudaSuccess;
-  static const bool nocand = getenv("KSCD_TOPK_NOCAND") != nullptr;
-  TopkArgs a = a_in;
-  a.cand_off = nocand ? 1 : 0;
-  // KSCD_TOPK_VARIANT (dev knob): <cluster><agg>, e.g. "80", "81", "10", "11"
-  static const char* forced = getenv("KSCD_TOPK_VARIANT");
-  int cl = 1, agg = 0;
-  // The sample-bracketed kernel is exact but measured instruction-bound on
-  // B200 (124 us vs 65 us for the 4-CTA cluster on 64 x 128K decode rows), so
-  // it is opt-in (KSCD_TOPK_VARIANT=s) until its shared-memory paths are tuned.
-  const bool sample = forced && forced[0] == 's';
-  if (sample) {
-    static const cudaError_t attr = cudaFuncSetAttribute(topk_sample_kernel,
-                                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                         (int)sizeof(FastShared));
-    if (attr != cudaSuccess) return attr;
-    topk_sample_kernel<<<a.rows, kFastThreads, sizeof(FastShared), st>>>(a);
-    return cudaGetLastError();
-  }
-  if (forced && forced[0]) {
-    cl = forced[0] == 'g' ? 16 : forced[0] == '8' ? 8 : (forced[0] == '4' ? 4 : (forced[0] == '2' ? 2 : 1));
-    agg = forced[1] == '1';
-  } else {
-    // Few long rows (decode: batch x kv heads) -> a cluster of CTAs per row.
-    // Measured on B200 at 128K: 64 rows: 1 CTA 141 us, 2: 83, 4: 65, 8: 85;
-    // 16 rows: 4: 64, 8: 54; 8 rows: 4: 62, 8: 44.  match_any aggregation
-    // costs more than the atomics it saves.
-    cl = a.len < 8192 ? 1 : (a.rows * 8 <= 148 ? 8 : (a.rows <= 148 ? 4 : 1));
-  }
-  if (cl == 16) return agg ? launch_topk_cl<16, 1>(a, st) : launch_topk_cl<16, 0>(a, st);
-  if (cl == 8) return agg ? launch_topk_cl<8, 1>(a, st) : launch_topk_cl<8, 0>(a, st);
-  if (cl == 4) return agg ? launch_topk_cl<4, 1>(a, st) : launch_topk_cl<4, 0>(a, st);
-  if (cl == 2) return agg ? launch_topk_cl<2, 1>(a, st) : launch_topk_cl<2, 0>(a, st);
-  return agg ? launch_topk_cl<1, 1>(a, st) : launch_topk_cl<1, 0>(a, st);
+cudaError_t launch_topk(const TopkArgs& a, cudaStream_t st) {
+  if (a.rows <= 0) return cudaSuccess;
+  // Few long rows (decode: batch x kv heads) -> a cluster of CTAs per row.
+  // Measured on B200 at 128K: 64 rows: 1 CTA 141 us, 2: 83, 4: 65, 8: 85;
+  // 16 rows: 4: 64, 8: 54; 8 rows: 4: 62, 8: 44.  Warp-aggregated
+  // (match_any) histogram atomics and a sample-bracketed single-CTA select
+  // were measured slower and removed.
+  const int cl = a.len < 8192 ? 1 : (a.rows * 8 <= 148 ? 8 : (a.rows <= 148 ? 4 : 1));
+  if (cl == 8) return launch_topk_cl<8>(a, st);
+  if (cl == 4) return launch_topk_cl<4>(a, st);
+  return launch_topk_cl<1>(a, st);
 }
 
 }  // namespace kscd

@@ -16,8 +16,6 @@ dominate the small reuse layers.
 
 from __future__ import annotations
 
-import os
-
 from typing import Dict, List, Optional, Sequence
 
 import torch
@@ -35,11 +33,11 @@ def layer_kinds(plan, num_layers: int) -> List[str]:
 
 
 class KascadeDecoder:
-    # output-copy chunk boundaries of capture_host_step (layers), overridable
-    # for experiments as KSCD_D2H_SPLITS="16,28".  Measured e2e on B200 (32
+    # output-copy chunk boundaries of capture_host_step (layers; a class
+    # attribute, so a caller can set its own).  Measured e2e on B200 (32
     # layers, 128K, b8, same box): 8,16,24 -> 569.7 us/token; 16,24,28,30 ->
     # 568.0; 24,31 -> 567.2 (one copy of the last layer left after the loop).
-    D2H_SPLITS = tuple(int(x) for x in os.environ.get("KSCD_D2H_SPLITS", "24,31").split(",") if x)
+    D2H_SPLITS = (24, 31)
 
     def __init__(self, plan, num_layers: int, batch: int, num_q_heads: int, num_kv_heads: int,
                  max_seq_len: int, device=None, validate: bool = True):
