@@ -27,3 +27,20 @@ for s in "$@"; do
       echo "launches rc=$?" ;;
   esac
 done
+# (appended) profiling steps: PROF=1 bash scripts/gpu_r02.sh TAG topk_ncu shard_ncu
+for s in "$@"; do
+  case $s in
+    topk_ncu)
+      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+        -k 'regex:topk_kernel' -s 1 -c 1 -o $O/topk_$TAG -f python scripts/prof_kernels.py decode > $O/topk_ncu_$TAG.out 2>&1
+      echo "topk ncu rc=$?" ;;
+    shard_ncu)
+      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+        -k 'regex:decode_attn_kernel<1' -s 1 -c 1 -o $O/shard_sparse_$TAG -f python scripts/prof_kernels.py decode_shard \
+        > $O/shard_ncu_$TAG.out 2>&1
+      echo "shard ncu rc=$?"
+      timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/shard_launches_$TAG.csv \
+        python scripts/prof_kernels.py decode_shard > /dev/null 2>&1
+      echo "shard launches rc=$?" ;;
+  esac
+done

@@ -17,7 +17,7 @@ def decode(n=131072, B=8, Hq=32, Hkv=8):
     v = torch.randn(B, Hkv, n, 128, device="cuda", generator=g).to(torch.bfloat16)
     pol = KBudgetPolicy(0.1, 128)
     out, lse, idx, cnt = ops.anchor_decode(q, k, v, n, pol, layer0=True)
-    hm = torch.tensor([3, 1, 0, 2, 7, 5, 6, 4], dtype=torch.int32, device="cuda")
+    hm = torch.arange(Hkv - 1, -1, -1, dtype=torch.int32, device="cuda")
     for _ in range(3):
         ops.reuse_decode(q, k, v, n, idx, cnt, hm, out=out)
     for _ in range(2):
@@ -40,7 +40,12 @@ def prefill(N=32768, Hq=32, Hkv=8):
     torch.cuda.synchronize()
 
 
+def decode_shard(n=131072, B=8):
+    """One rank of the 8-way kv-head-sharded 70B decode: 1 KV + 8 Q heads."""
+    decode(n, B, 8, 1)
+
+
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "decode"
     args = [int(a) for a in sys.argv[2:]]
-    (decode if which == "decode" else prefill)(*args)
+    {"decode": decode, "prefill": prefill, "decode_shard": decode_shard}[which](*args)
