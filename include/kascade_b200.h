@@ -161,6 +161,38 @@ typedef struct kscd_select_prefill_params {
   int32_t tile_size;       /* must be 128 */
 } kscd_select_prefill_params;
 
+/* Pre-softmax pooled selection at engine scale (runner.py:155-161, the
+ * comparison mode SPEC.md:370): per (kv head, tile) q_bar = the fp64 mean of
+ * the tile's G x T query rows, scores = K[:t1] q_bar * scale, pooled =
+ * softmax(scores) (fp32 result, as softmax_row, attention.py:77-90), then the
+ * exact Top-k with k = k_budget(t1).  Decode: the tile is the step's token
+ * (T = 1 row per sequence, t1 = n); prefill: 128-row tiles.  all_heads: the
+ * kv heads' pooled vectors are averaged into one shared set (runner.py:180-197).
+ * No attention pass is needed (anchor layers skip pass A / the score pass). */
+typedef struct kscd_select_pre_params {
+  int32_t batch;           /* decode: B; prefill: must be 1 */
+  int32_t num_q_heads, num_kv_heads, head_dim;
+  int32_t seq_len;         /* decode: n (keys 0..n-1 visible); prefill: N */
+  int32_t tile_size;       /* 0: decode (one query token per sequence); 128: prefill tiles */
+  const void* q;           /* decode bf16 [B][Hq][128] contiguous; prefill bf16 [Hq][N][128] */
+  int64_t q_stride_head;   /* prefill: elements between heads (decode: ignored) */
+  const void* k;           /* decode: cache bf16 [B][Hkv][n_cap][128]; prefill bf16 [Hkv][N][128] */
+  int64_t kv_stride_batch, kv_stride_head;   /* elements (kv_stride_batch: decode only) */
+  float softmax_scale;     /* <= 0 selects 1/sqrt(head_dim) */
+  float* pooled;           /* scratch fp32 rows: decode [B*Hkv (+B)][pooled_stride],
+                              prefill [Hkv*T (+T)][pooled_stride] (+ rows: all_heads) */
+  int64_t pooled_stride;   /* >= seq_len, multiple of 4 */
+  void* workspace;         /* kscd_select_pre_workspace_size bytes, any content */
+  size_t workspace_bytes;
+  double topk_fraction;
+  int32_t k_min;
+  int32_t all_heads;
+  int32_t* indices;        /* int32 [rows][k_cap]; rows = B*Hkv or Hkv*T (B or T with all_heads) */
+  int32_t* counts;         /* int32 [rows] */
+  int32_t k_cap;           /* >= k_budget(seq_len) */
+  const int32_t* seq_lens; /* decode: device int32 [B] or NULL (ragged batch, k = k_budget(seq_lens[b])) */
+} kscd_select_pre_params;
+
 /* Reference-scale helpers for the trace-level API (small N only). */
 typedef struct kscd_probs_params {
   int32_t num_q_heads, num_kv_heads, head_dim, seq_len, causal;
@@ -258,6 +290,11 @@ int kscd_dense_probs(const kscd_probs_params* p, void* stream);
 int kscd_pool_tiles(const kscd_pool_tiles_params* p, void* stream);
 
 int kscd_append_kv(const kscd_append_kv_params* p, void* stream);
+
+/* Pre-softmax pooled selection (see kscd_select_pre_params): q_bar, the
+ * scores against K, the row softmax and the exact Top-k, stream-ordered. */
+int kscd_select_pre(const kscd_select_pre_params* p, void* stream);
+int kscd_select_pre_workspace_size(const kscd_select_pre_params* p, size_t* bytes);
 
 /* Offline calibration gather-sum: mass[i][j][r] =
  * fp64 sum over t < counts[i][r] of dist[j][r][indices[i][r][t]] -- the

@@ -313,7 +313,7 @@ def run_kascade(trace, plan, phase: str = PREFILL) -> Tuple[np.ndarray, RunRepor
     L, Hq, Hkv, N = trace.num_layers, trace.num_query_heads, trace.num_kv_heads, trace.seq_len
     G = Hq // Hkv
     tiles = make_tiles(N, phase, Hq, Hkv, plan.tile_size)
-    fast = phase == PREFILL and plan.tile_size == ops.TILE and plan.pooling == POOL_POST
+    fast = phase == PREFILL and plan.tile_size == ops.TILE   # the engine's prefill kernels (both poolings)
     anchors = set(plan.core.anchors)
     outputs = np.empty((L, Hq, N, trace.head_dim), np.float32)
     reports: List[LayerReport] = []
@@ -326,7 +326,10 @@ def run_kascade(trace, plan, phase: str = PREFILL) -> Tuple[np.ndarray, RunRepor
         _check_finite(Yd, layer)
         is_anchor = layer == 0 or layer in anchors
         if is_anchor:
-            if fast:
+            if fast and plan.pooling == POOL_PRE:
+                cur = ops.select_prefill_pre(q, k, plan.k_policy, all_heads=plan.mode == MODE_ALL_HEADS_POOLED,
+                                             scale=sc)
+            elif fast:
                 cur = ops.select_prefill(q, k, lse_d, plan.k_policy, all_heads=plan.mode == MODE_ALL_HEADS_POOLED,
                                          scale=sc)
             else:

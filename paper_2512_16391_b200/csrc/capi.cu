@@ -510,3 +510,114 @@ int kscd_masked_mass(const kscd_masked_mass_params* p, void* stream) {
   a.mass = p->mass;
   return cuda_status(kscd::launch_masked_mass(a, (cudaStream_t)stream), "kscd_masked_mass");
 }
+
+// ------------------------------------------------ pre-softmax selection
+namespace kscd {
+int pre_pool_chunk_keys(bool prefill);
+}
+
+namespace {
+
+struct PreShape {
+  bool prefill;
+  int rows, T, chunks, chunk_keys;
+};
+
+int check_pre(const kscd_select_pre_params* p, PreShape* sh) {
+  if (!p) return fail(KSCD_INVALID_ARGUMENT, "params is NULL");
+  if (bad_head_dim(p->head_dim)) return fail(KSCD_UNSUPPORTED, KSCD_HEAD_DIM_MSG, p->head_dim);
+  if (p->tile_size != 0 && p->tile_size != 128)
+    return fail(KSCD_UNSUPPORTED, "tile_size %d unsupported (0 = decode, 128 = prefill)", p->tile_size);
+  if (p->batch < 1 || p->num_q_heads < 1 || p->num_kv_heads < 1 || p->num_q_heads % p->num_kv_heads)
+    return fail(KSCD_INVALID_ARGUMENT, "bad head/batch shape");
+  if (p->tile_size == 128 && p->batch != 1) return fail(KSCD_INVALID_ARGUMENT, "prefill batch must be 1");
+  if (p->seq_len < 1) return fail(KSCD_INVALID_ARGUMENT, "seq_len must be >= 1");
+  sh->prefill = p->tile_size == 128;
+  sh->T = sh->prefill ? (p->seq_len + 127) / 128 : 1;
+  sh->rows = sh->prefill ? p->num_kv_heads * sh->T : p->batch * p->num_kv_heads;
+  sh->chunk_keys = kscd::pre_pool_chunk_keys(sh->prefill);
+  sh->chunks = (p->seq_len + sh->chunk_keys - 1) / sh->chunk_keys;
+  return KSCD_OK;
+}
+
+size_t pre_ws_bytes(const PreShape& sh) {
+  size_t bytes = (size_t)sh.rows * 128 * sizeof(float);
+  bytes = (bytes + 255) & ~(size_t)255;
+  return bytes + (size_t)sh.rows * sh.chunks * 2 * sizeof(float);
+}
+
+}  // namespace
+
+extern "C" int kscd_select_pre_workspace_size(const kscd_select_pre_params* p, size_t* bytes) {
+  PreShape sh;
+  int rc = check_pre(p, &sh);
+  if (rc) return rc;
+  if (!bytes) return fail(KSCD_INVALID_ARGUMENT, "bytes is NULL");
+  *bytes = pre_ws_bytes(sh);
+  return KSCD_OK;
+}
+
+extern "C" int kscd_select_pre(const kscd_select_pre_params* p, void* stream) {
+  PreShape sh;
+  int rc = check_pre(p, &sh);
+  if (rc) return rc;
+  if (!(p->topk_fraction > 0.0 && p->topk_fraction <= 1.0))
+    return fail(KSCD_INVALID_ARGUMENT, "fraction must be in (0, 1], got %g", p->topk_fraction);
+  if (p->k_min < 1) return fail(KSCD_INVALID_ARGUMENT, "k_min must be >= 1, got %d", p->k_min);
+  if (!p->q || !p->k || !p->pooled || !p->indices || !p->counts || !p->workspace)
+    return fail(KSCD_INVALID_ARGUMENT, "NULL buffer");
+  if (p->workspace_bytes < pre_ws_bytes(sh))
+    return fail(KSCD_INVALID_ARGUMENT, "workspace too small (%zu < %zu bytes)", p->workspace_bytes, pre_ws_bytes(sh));
+  if (p->pooled_stride < p->seq_len || (p->pooled_stride & 3) || ((uintptr_t)p->pooled & 15))
+    return fail(KSCD_INVALID_ARGUMENT, "pooled_stride must be >= seq_len and a multiple of 4, pooled 16-byte aligned");
+  if ((((uintptr_t)p->q | (uintptr_t)p->k) & 15) || (p->kv_stride_batch & 7) || (p->kv_stride_head & 7) ||
+      (p->q_stride_head & 7))
+    return fail(KSCD_INVALID_ARGUMENT, "q/k must be 16-byte aligned with strides multiple of 8 elements");
+  const int k = kscd_k_budget(p->topk_fraction, p->k_min, p->seq_len);
+  if (p->k_cap < k) return fail(KSCD_INVALID_ARGUMENT, "k_cap %d < k_budget %d", p->k_cap, k);
+  kscd::PrePoolArgs a{};
+  a.B = p->batch;
+  a.Hq = p->num_q_heads;
+  a.Hkv = p->num_kv_heads;
+  a.G = p->num_q_heads / p->num_kv_heads;
+  a.n = p->seq_len;
+  a.T = sh.T;
+  a.prefill = sh.prefill;
+  a.q = (const __nv_bfloat16*)p->q;
+  a.q_sh = p->q_stride_head;
+  a.k = (const __nv_bfloat16*)p->k;
+  a.kv_sb = p->kv_stride_batch;
+  a.kv_sh = p->kv_stride_head;
+  a.scale = p->softmax_scale > 0.f ? p->softmax_scale : (float)(1.0 / sqrt((double)p->head_dim));
+  a.pooled = p->pooled;
+  a.pool_stride = p->pooled_stride;
+  a.qbar = (float*)p->workspace;
+  size_t off = ((size_t)sh.rows * 128 * sizeof(float) + 255) & ~(size_t)255;
+  a.part = (float2*)((char*)p->workspace + off);
+  a.chunks = sh.chunks;
+  a.chunk_keys = sh.chunk_keys;
+  a.lens = sh.prefill ? nullptr : p->seq_lens;
+  a.mean_out = p->all_heads ? p->pooled + (int64_t)sh.rows * p->pooled_stride : nullptr;
+  cudaStream_t st = (cudaStream_t)stream;
+  rc = cuda_status(kscd::launch_pre_pool(a, st), "pre_pool");
+  if (rc) return rc;
+  kscd::TopkArgs ta{};
+  ta.rows = p->all_heads ? (sh.prefill ? sh.T : p->batch) : sh.rows;
+  ta.vals = p->all_heads ? a.mean_out : p->pooled;
+  ta.val_stride = p->pooled_stride;
+  ta.len = p->seq_len;
+  ta.k = k;
+  ta.idx = p->indices;
+  ta.counts = p->counts;
+  ta.k_cap = p->k_cap;
+  ta.fraction = p->topk_fraction;
+  ta.k_min = p->k_min;
+  if (sh.prefill) {
+    ta.tile = 128;
+    ta.T = sh.T;
+  } else if (p->seq_lens) {
+    ta.seq_lens = p->seq_lens;
+    ta.seq_div = p->all_heads ? 1 : p->num_kv_heads;
+  }
+  return cuda_status(kscd::launch_topk(ta, st), "topk");
+}

@@ -27,6 +27,7 @@
 namespace kscd {
 
 constexpr int kTileKeys = 64;
+constexpr int kMaxSplitsDev = 64;   // = capi.cu kMaxSplits (the workspace and merge bound)
 constexpr int kThreads = 128;
 constexpr int kTileBytes = kTileKeys * kRowBytes;  // 16 KB
 
@@ -317,30 +318,55 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
   __syncthreads();
   if (!is_last) return;
   __threadfence();
+  // The partials are read with every load of a batch in flight: the split
+  // weights exp2(m_sp - M) go to shared memory first (lanes over splits), so
+  // the O loop has no dependent load per split (a serial load chain over 37
+  // splits of the 8-row kv-head-shard case cost ~13 us of L2 latency).
+  float* wsp = reinterpret_cast<float*>(smem) + warp * kMaxSplitsDev;   // reuses the ring
   for (int h = warp; h < G; h += 4) {
     const int64_t p0 = (bh0 + h) * a.splits;
+    float2 ml[kMaxSplitsDev / 32];
+#pragma unroll
+    for (int i = 0; i < kMaxSplitsDev / 32; ++i) {
+      const int sp = lane + 32 * i;
+      ml[i] = sp < a.splits ? __ldcg(reinterpret_cast<const float2*>(a.part_ml + (p0 + sp) * 2))
+                            : make_float2(-INFINITY, 0.f);
+    }
     float M = -INFINITY;
-    for (int sp = lane; sp < a.splits; sp += 32) M = fmaxf(M, __ldcg(a.part_ml + (p0 + sp) * 2));
+#pragma unroll
+    for (int i = 0; i < kMaxSplitsDev / 32; ++i) M = fmaxf(M, ml[i].x);
     M = warp_max(M);
     const float Mu = M == -INFINITY ? 0.f : M;
     float L = 0.f;
-    for (int sp = lane; sp < a.splits; sp += 32) {
-      const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.part_ml + (p0 + sp) * 2));
-      L += fast_exp2(ml.x - Mu) * ml.y;
+#pragma unroll
+    for (int i = 0; i < kMaxSplitsDev / 32; ++i) {
+      const float sc = ml[i].x == -INFINITY ? 0.f : fast_exp2(ml[i].x - Mu);
+      L += sc * ml[i].y;
+      wsp[lane + 32 * i] = sc;
     }
     L = warp_sum(L);
+    __syncwarp();
     if (Cfg::kHasV) {
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int sp = 0; sp < a.splits; ++sp) {
-        const float sc = fast_exp2(__ldcg(a.part_ml + (p0 + sp) * 2) - Mu);
-        const float4 v = __ldcg(reinterpret_cast<const float4*>(a.part + (p0 + sp) * kHeadDim + lane * 4));
-        acc.x += sc * v.x; acc.y += sc * v.y; acc.z += sc * v.z; acc.w += sc * v.w;
+      constexpr int kB = 8;
+      for (int sp0 = 0; sp0 < a.splits; sp0 += kB) {
+        float4 v[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+          v[u] = sp0 + u < a.splits ? __ldcg(reinterpret_cast<const float4*>(a.part + (p0 + sp0 + u) * kHeadDim + lane * 4))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const float sc = sp0 + u < a.splits ? wsp[sp0 + u] : 0.f;
+          acc.x += sc * v[u].x; acc.y += sc * v[u].y; acc.z += sc * v[u].z; acc.w += sc * v[u].w;
+        }
       }
       const float inv = L > 0.f ? 1.f / L : 0.f;
       *reinterpret_cast<float4*>(a.out + (bh0 + h) * kHeadDim + lane * 4) =
           make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
     }
     if (lane == 0 && a.lse) a.lse[bh0 + h] = (M + __log2f(L)) * kLn2;
+    __syncwarp();
   }
 }
 

@@ -170,4 +170,25 @@ struct AppendKvArgs {
 };
 cudaError_t launch_append_kv(const AppendKvArgs& a, cudaStream_t st);
 
+// Pre-softmax pooled selection (pre_pool.cu).  Rows are (b, g) in decode
+// (T = 1) and (g, t) in prefill; a row's visible keys are [0, len(row)).
+struct PrePoolArgs {
+  int B, Hq, Hkv, G, n;                   // n: decode keys / prefill N
+  int T;                                  // prefill tiles (decode: 1)
+  bool prefill;
+  const __nv_bfloat16* q;                 // decode [B][Hq][128]; prefill [Hq][N][128] (q_sh)
+  int64_t q_sh;
+  const __nv_bfloat16* k;                 // decode rows k + b*kv_sb + g*kv_sh + j*128; prefill k + g*kv_sh + j*128
+  int64_t kv_sb, kv_sh;
+  float scale;                            // natural-log softmax scale
+  float* pooled;                          // [rows][pool_stride]: scores, then probabilities
+  int64_t pool_stride;
+  float* qbar;                            // [rows][128] fp32
+  float2* part;                           // [rows][chunks] (max, sum of exp(s - max))
+  int chunks, chunk_keys;                 // per-row partials (prefill: chunk_keys = 128)
+  const int* lens;                        // decode ragged [B] (nullable)
+  float* mean_out;                        // all-heads: [B or T][pool_stride] mean over kv heads (nullable)
+};
+cudaError_t launch_pre_pool(const PrePoolArgs& a, cudaStream_t st);
+
 }  // namespace kscd

@@ -23,7 +23,7 @@ import torch
 from . import ops
 from .exceptions import InvalidArgumentError
 from .host_types import (KIND_ANCHOR, KIND_ANCHOR0, KIND_REUSE, MODE_ALL_HEADS_POOLED, MODE_REMAPPED,
-                         POOL_POST, k_budget, validate_plan)
+                         POOL_PRE, k_budget, validate_plan)
 
 
 def layer_kinds(plan, num_layers: int) -> List[str]:
@@ -43,9 +43,8 @@ class KascadeDecoder:
                  max_seq_len: int, device=None, validate: bool = True):
         if validate:   # sharded executors validate against the GLOBAL head count themselves
             validate_plan(plan, num_layers, num_kv_heads)
-        if plan.pooling != POOL_POST:
-            raise InvalidArgumentError("decode engine implements post-softmax pooling (the paper's mode)")
         self.plan = plan
+        self.pre = plan.pooling == POOL_PRE     # pre-softmax pooling (runner.py:155-161)
         self.L, self.B, self.Hq, self.Hkv = num_layers, batch, num_q_heads, num_kv_heads
         self.n_max = max_seq_len
         self.device = torch.device(device or "cuda")
@@ -65,8 +64,14 @@ class KascadeDecoder:
         self.shared_map = torch.zeros(num_kv_heads, dtype=torch.int32, device=dev) if self.all_heads else None
         k_cap = k_budget(plan.k_policy, max_seq_len)
         n_pad = (max_seq_len + 3) // 4 * 4
-        self.scores = torch.empty(batch, num_q_heads, n_pad, dtype=torch.float32, device=dev)
-        self.pooled = torch.empty(batch * Hsrc, n_pad, dtype=torch.float32, device=dev)
+        if self.pre:   # q_bar scores -> softmax -> Top-k: no score pass, no per-head score scratch
+            self.scores = None
+            self.pooled, self.pre_ws, _, _ = ops.select_pre_buffers(batch, num_kv_heads, max_seq_len, plan.k_policy,
+                                                                    dev, prefill=False, all_heads=self.all_heads,
+                                                                    num_q_heads=num_q_heads)
+        else:
+            self.scores = torch.empty(batch, num_q_heads, n_pad, dtype=torch.float32, device=dev)
+            self.pooled = torch.empty(batch * Hsrc, n_pad, dtype=torch.float32, device=dev)
         self.lse = torch.empty(batch, num_q_heads, dtype=torch.float32, device=dev)
         self.indices = torch.empty(batch, Hsrc, k_cap, dtype=torch.int32, device=dev)
         self.counts = torch.zeros(batch, Hsrc, dtype=torch.int32, device=dev)
@@ -95,24 +100,36 @@ class KascadeDecoder:
 
     def _layer(self, l: int, q, k_caches, v_caches, seq_len: int) -> None:
         """The kernels of layer l (runner.py:250-275 for one decode token)."""
-        pol = self.plan.k_policy
         kind = self.kinds[l]
         ql, kl, vl = q[l], k_caches[l], v_caches[l]
         if kind == KIND_REUSE:
             ops.sparse_decode(ql, kl, vl, seq_len, self.indices, self.counts, self.head_maps[l], out=self.out[l],
                               workspace=self.ws)
             return
-        sl = self.seq_lens
+        self._anchor_select(l, kind, ql, kl, vl, seq_len, self.out[l])
+        if kind == KIND_ANCHOR:
+            ops.sparse_decode(ql, kl, vl, seq_len, self.indices, self.counts, self.shared_map, out=self.out[l],
+                              workspace=self.ws)
+
+    def _anchor_select(self, l: int, kind: str, ql, kl, vl, seq_len: int, out) -> None:
+        """Layer 0's dense output (into ``out``) and the anchor selection of
+        layer l into self.indices / self.counts (runner.py:250-266): post-
+        softmax pooling from the dense or score pass, or pre-softmax pooling
+        from q_bar with no attention pass."""
+        pol, sl = self.plan.k_policy, self.seq_lens
+        if self.pre:
+            if kind == KIND_ANCHOR0:
+                ops.dense_decode(ql, kl, vl, seq_len, out=out, lse=self.lse, seq_lens=sl, workspace=self.ws)
+            ops.select_decode_pre(ql, kl, seq_len, pol, pooled=self.pooled, workspace=self.pre_ws,
+                                  indices=self.indices, counts=self.counts, all_heads=self.all_heads, seq_lens=sl)
+            return
         if kind == KIND_ANCHOR0:
-            ops.dense_decode(ql, kl, vl, seq_len, out=self.out[l], lse=self.lse, scores=self.scores, seq_lens=sl,
+            ops.dense_decode(ql, kl, vl, seq_len, out=out, lse=self.lse, scores=self.scores, seq_lens=sl,
                              workspace=self.ws)
         else:
             ops.anchor_scores_decode(ql, kl, seq_len, self.scores, self.lse, seq_lens=sl, workspace=self.ws)
         ops.select_decode(self.scores, self.lse, seq_len, pol, self.Hkv, indices=self.indices,
                           counts=self.counts, pooled=self.pooled, all_heads=self.all_heads, seq_lens=sl)
-        if kind == KIND_ANCHOR:
-            ops.sparse_decode(ql, kl, vl, seq_len, self.indices, self.counts, self.shared_map, out=self.out[l],
-                              workspace=self.ws)
 
     def _dense_layer(self, l: int, q, k_caches, v_caches, seq_len: int) -> None:
         ops.dense_decode(q[l], k_caches[l], v_caches[l], seq_len, out=self.out[l], lse=self.lse,
@@ -230,8 +247,6 @@ class KascadePrefill:
                  validate: bool = True):
         if validate:   # sharded executors validate against the GLOBAL head count themselves
             validate_plan(plan, num_layers, num_kv_heads)
-        if plan.pooling != POOL_POST:
-            raise InvalidArgumentError("prefill engine implements post-softmax pooling (the paper's mode)")
         if plan.tile_size != ops.TILE:
             raise InvalidArgumentError(f"prefill engine tiles are {ops.TILE} rows (plan has {plan.tile_size})")
         self.plan = plan
@@ -250,7 +265,13 @@ class KascadePrefill:
                 self.head_maps[l] = torch.tensor(m, dtype=torch.int32, device=dev)
         self.shared_map = torch.zeros(num_kv_heads, dtype=torch.int32, device=dev) if self.all_heads else None
         self.lse = torch.empty(num_q_heads, seq_len, dtype=torch.float32, device=dev)
-        self.pooled = torch.empty(2, rows, T, (seq_len + 3) // 4 * 4, dtype=torch.float32, device=dev)
+        self.pre = plan.pooling == POOL_PRE     # pre-softmax pooling (runner.py:155-161): no pass A / pass B
+        if self.pre:
+            self.pooled, self.pre_ws, _, _ = ops.select_pre_buffers(1, num_kv_heads, seq_len, plan.k_policy, dev,
+                                                                    prefill=True, all_heads=self.all_heads,
+                                                                    num_q_heads=num_q_heads)
+        else:
+            self.pooled = torch.empty(2, rows, T, (seq_len + 3) // 4 * 4, dtype=torch.float32, device=dev)
         self.indices = torch.empty(rows, T, kc, dtype=torch.int32, device=dev)
         self.counts = torch.zeros(rows, T, dtype=torch.int32, device=dev)
         self.out = torch.empty(num_layers, num_q_heads, seq_len, 128, dtype=torch.bfloat16, device=dev)
@@ -260,7 +281,6 @@ class KascadePrefill:
         """qs/ks/vs: per-layer [Hq][N][128] / [Hkv][N][128] bf16.  Returns the
         bf16 outputs [L][Hq][N][128].  ``stop_after`` ends the loop after that
         layer (the index lists then hold that layer's latest anchor sets)."""
-        pol = self.plan.k_policy
         for l, kind in enumerate(self.kinds):
             if stop_after is not None and l > stop_after:
                 break
@@ -268,15 +288,26 @@ class KascadePrefill:
             if kind == KIND_REUSE:
                 ops.sparse_prefill(q, k, v, self.indices, self.counts, self.head_maps[l], out=self.out[l])
                 continue
-            if kind == KIND_ANCHOR0:
-                ops.dense_prefill(q, k, v, out=self.out[l], lse=self.lse)
-            else:
-                ops.anchor_lse_prefill(q, k, lse=self.lse)
-            ops.select_prefill(q, k, self.lse, pol, indices=self.indices, counts=self.counts, pooled=self.pooled,
-                               all_heads=self.all_heads)
+            self._anchor_select(kind, q, k, v, self.out[l])
             if kind == KIND_ANCHOR:
                 ops.sparse_prefill(q, k, v, self.indices, self.counts, self.shared_map, out=self.out[l])
         return self.out
+
+    def _anchor_select(self, kind: str, q, k, v, out) -> None:
+        """Layer 0's dense output and the anchor's per-(kv head, tile) sets
+        (runner.py:250-266): pass A (LSE) + pass B pooled Top-k, or the
+        pre-softmax q_bar selection (no attention pass)."""
+        pol = self.plan.k_policy
+        if kind == KIND_ANCHOR0:
+            ops.dense_prefill(q, k, v, out=out, lse=self.lse)
+        if self.pre:
+            ops.select_prefill_pre(q, k, pol, pooled=self.pooled, workspace=self.pre_ws, indices=self.indices,
+                                   counts=self.counts, all_heads=self.all_heads)
+            return
+        if kind != KIND_ANCHOR0:
+            ops.anchor_lse_prefill(q, k, lse=self.lse)
+        ops.select_prefill(q, k, self.lse, pol, indices=self.indices, counts=self.counts, pooled=self.pooled,
+                           all_heads=self.all_heads)
 
     def dense_forward(self, qs, ks, vs) -> torch.Tensor:
         for l in range(self.L):

@@ -467,3 +467,94 @@ def anchor_prefill(q, k, v, policy: KBudgetPolicy, *, layer0: bool = False, out=
 def reuse_prefill(q, k, v, indices, counts, head_map=None, *, out=None):
     """One reuse layer of a prefill (runner.py:267-275)."""
     return sparse_prefill(q, k, v, indices, counts, head_map, out=out)[0]
+
+
+# ------------------------------------------------- pre-softmax selection
+def _pre_params(q, k, seq_len, policy, *, prefill, pooled, workspace, indices, counts, all_heads, seq_lens, scale):
+    if prefill:
+        Hq, Hkv, N = _check_prefill_qkv(q, k, None)
+        B, q_sh, kv_sb, kv_sh = 1, q.stride(0), 0, k.stride(0)
+    else:
+        B, Hq = _check_q(q)
+        Hkv, n_cap, kv_sb, kv_sh = _check_kv(k, None, B)
+        if not (1 <= seq_len <= n_cap):
+            raise InvalidArgumentError(f"seq_len {seq_len} outside [1, {n_cap}]")
+        if Hq % Hkv:
+            raise InvalidArgumentError(f"num_query_heads ({Hq}) must be divisible by num_kv_heads ({Hkv})")
+        q_sh = 0
+        _check_seq_lens(seq_lens, B, seq_len)
+    return _lib.SelectPreParams(
+        batch=B, num_q_heads=Hq, num_kv_heads=Hkv, head_dim=HEAD_DIM, seq_len=int(seq_len),
+        tile_size=TILE if prefill else 0, q=q.data_ptr(), q_stride_head=q_sh, k=k.data_ptr(),
+        kv_stride_batch=kv_sb, kv_stride_head=kv_sh, softmax_scale=float(scale or 0.0),
+        topk_fraction=float(policy.fraction), k_min=int(policy.k_min), all_heads=1 if all_heads else 0,
+        seq_lens=_ptr(seq_lens) if not prefill else None)
+
+
+def select_pre_buffers(B: int, Hkv: int, n: int, policy: KBudgetPolicy, device, *, prefill: bool,
+                       all_heads: bool = False, num_q_heads: Optional[int] = None):
+    """(pooled, workspace, indices, counts) for select_*_pre: pooled rows are
+    the per-(kv head, tile) probabilities plus, in all-heads mode, one mean
+    row per tile / sequence."""
+    T = (n + TILE - 1) // TILE if prefill else 1
+    rows = Hkv * T if prefill else B * Hkv
+    out_rows = (T if prefill else B) if all_heads else rows
+    pooled = torch.empty(rows + (out_rows if all_heads else 0), (n + 3) // 4 * 4, dtype=torch.float32, device=device)
+    p = _lib.SelectPreParams(batch=1 if prefill else B, num_q_heads=num_q_heads or Hkv, num_kv_heads=Hkv,
+                             head_dim=HEAD_DIM, seq_len=n, tile_size=TILE if prefill else 0)
+    nbytes = _lib.c_sz(0)
+    _lib.check(_lib.load().kscd_select_pre_workspace_size(ctypes.byref(p), ctypes.byref(nbytes)))
+    ws = torch.empty(nbytes.value, dtype=torch.uint8, device=device)
+    kc = k_budget(policy, n)
+    idx = torch.empty(out_rows, kc, dtype=torch.int32, device=device)
+    cnt = torch.empty(out_rows, dtype=torch.int32, device=device)
+    return pooled, ws, idx, cnt
+
+
+def _run_pre(p, pooled, workspace, indices, counts):
+    p.pooled, p.pooled_stride = pooled.data_ptr(), pooled.stride(0)
+    p.workspace, p.workspace_bytes = workspace.data_ptr(), workspace.numel()
+    p.indices, p.counts, p.k_cap = indices.data_ptr(), counts.data_ptr(), indices.shape[-1]
+    _lib.call("kscd_select_pre", p, _stream())
+
+
+def select_decode_pre(q, k_cache, seq_len, policy: KBudgetPolicy, *, pooled=None, workspace=None, indices=None,
+                      counts=None, all_heads: bool = False, seq_lens=None, scale=None):
+    """Pre-softmax pooled selection of one decode step (runner.py:155-161
+    for the decode tile): q_bar = mean of the group's query heads, softmax
+    of K q_bar / sqrt(d), exact Top-k.  No attention pass is needed.
+    Returns (indices [B][Hsrc][k_cap], counts [B][Hsrc])."""
+    B, Hkv = q.shape[0], k_cache.shape[1]
+    if pooled is None or workspace is None or indices is None or counts is None:
+        pb, wb, ib, cb = select_pre_buffers(B, Hkv, seq_len, policy, q.device, prefill=False, all_heads=all_heads,
+                                            num_q_heads=q.shape[1])
+        pooled = pb if pooled is None else pooled
+        workspace = wb if workspace is None else workspace
+        Hs = 1 if all_heads else Hkv
+        indices = ib.view(B, Hs, -1) if indices is None else indices
+        counts = cb.view(B, Hs) if counts is None else counts
+    p = _pre_params(q, k_cache, seq_len, policy, prefill=False, pooled=pooled, workspace=workspace,
+                    indices=indices, counts=counts, all_heads=all_heads, seq_lens=seq_lens, scale=scale)
+    _run_pre(p, pooled, workspace, indices, counts)
+    return indices, counts
+
+
+def select_prefill_pre(q, k, policy: KBudgetPolicy, *, pooled=None, workspace=None, indices=None, counts=None,
+                       all_heads: bool = False, scale=None):
+    """Pre-softmax pooled selection of every (kv head, 128-row tile) of a
+    prefill layer (runner.py:155-161,199-206).  Returns (indices
+    [Hsrc][T][k_cap], counts [Hsrc][T])."""
+    Hq, Hkv, N = _check_prefill_qkv(q, k, None)
+    T = (N + TILE - 1) // TILE
+    if pooled is None or workspace is None or indices is None or counts is None:
+        pb, wb, ib, cb = select_pre_buffers(1, Hkv, N, policy, q.device, prefill=True, all_heads=all_heads,
+                                            num_q_heads=Hq)
+        pooled = pb if pooled is None else pooled
+        workspace = wb if workspace is None else workspace
+        Hs = 1 if all_heads else Hkv
+        indices = ib.view(Hs, T, -1) if indices is None else indices
+        counts = cb.view(Hs, T) if counts is None else counts
+    p = _pre_params(q, k, N, policy, prefill=True, pooled=pooled, workspace=workspace, indices=indices,
+                    counts=counts, all_heads=all_heads, seq_lens=None, scale=scale)
+    _run_pre(p, pooled, workspace, indices, counts)
+    return indices, counts

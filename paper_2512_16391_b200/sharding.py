@@ -228,9 +228,9 @@ class ShardedKascadeDecoder:
         """One decode step on this rank's heads; ``seq_lens`` (device int32
         [B]) runs a ragged batch as in KascadeDecoder.step."""
         from . import ops
-        from .host_types import KIND_ANCHOR, KIND_ANCHOR0, KIND_REUSE
+        from .host_types import KIND_ANCHOR, KIND_REUSE
         loc = self.local
-        pol = loc.plan.k_policy
+        loc.seq_lens = seq_lens
         ws = loc.ws
         for l, kind in enumerate(self.kinds):
             ql, kl, vl = q[l], k_caches[l], v_caches[l]
@@ -238,13 +238,7 @@ class ShardedKascadeDecoder:
                 ops.sparse_decode(ql, kl, vl, seq_len, self.full_idx, self.full_cnt, self.maps[l], out=loc.out[l],
                                   workspace=ws)
                 continue
-            if kind == KIND_ANCHOR0:
-                ops.dense_decode(ql, kl, vl, seq_len, out=loc.out[l], lse=loc.lse, scores=loc.scores,
-                                 seq_lens=seq_lens, workspace=ws)
-            else:
-                ops.anchor_scores_decode(ql, kl, seq_len, loc.scores, loc.lse, seq_lens=seq_lens, workspace=ws)
-            ops.select_decode(loc.scores, loc.lse, seq_len, pol, self.Hloc, indices=loc.indices, counts=loc.counts,
-                              pooled=loc.pooled, seq_lens=seq_lens)
+            loc._anchor_select(l, kind, ql, kl, vl, seq_len, loc.out[l])
             # the exchange overlaps the anchor's own sparse pass, which only
             # needs this rank's lists
             self.exchange.start()
@@ -308,19 +302,14 @@ class ShardedKascadePrefill:
         """qs/ks/vs: this rank's head slices per layer ([Hq_loc][N][128] and
         [Hloc][N][128]).  Returns the local outputs [L][Hq_loc][N][128]."""
         from . import ops
-        from .host_types import KIND_ANCHOR, KIND_ANCHOR0, KIND_REUSE
+        from .host_types import KIND_ANCHOR, KIND_REUSE
         loc = self.local
-        pol = loc.plan.k_policy
         for l, kind in enumerate(self.kinds):
             q, k, v = qs[l], ks[l], vs[l]
             if kind == KIND_REUSE:
                 ops.sparse_prefill(q, k, v, self.full_idx, self.full_cnt, self.maps[l], out=loc.out[l])
                 continue
-            if kind == KIND_ANCHOR0:
-                ops.dense_prefill(q, k, v, out=loc.out[l], lse=loc.lse)
-            else:
-                ops.anchor_lse_prefill(q, k, lse=loc.lse)
-            ops.select_prefill(q, k, loc.lse, pol, indices=loc.indices, counts=loc.counts, pooled=loc.pooled)
+            loc._anchor_select(kind, q, k, v, loc.out[l])
             self.exchange.start()
             if kind == KIND_ANCHOR:           # overlaps the exchange: own lists only
                 ops.sparse_prefill(q, k, v, loc.indices, loc.counts, None, out=loc.out[l])

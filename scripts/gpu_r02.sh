@@ -36,11 +36,22 @@ for s in "$@"; do
       echo "topk ncu rc=$?" ;;
     shard_ncu)
       timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-        -k 'regex:decode_attn_kernel<1' -s 1 -c 1 -o $O/shard_sparse_$TAG -f python scripts/prof_kernels.py decode_shard \
+        -k 'regex:decode_attn_kernel<\(int\)1' -s 1 -c 1 -o $O/shard_sparse_$TAG -f python scripts/prof_kernels.py decode_shard \
         > $O/shard_ncu_$TAG.out 2>&1
       echo "shard ncu rc=$?"
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/shard_launches_$TAG.csv \
         python scripts/prof_kernels.py decode_shard > /dev/null 2>&1
       echo "shard launches rc=$?" ;;
+  esac
+done
+for s in "$@"; do
+  case $s in
+    newtests)
+      timeout 1500 python -m pytest tests/test_pre_pooling_gpu.py tests/test_exporter_traces_gpu.py tests/test_decode_gpu.py \
+        tests/test_compat_gpu.py tests/test_acceptance_gpu.py tests/test_shapes_gpu.py -q -s -rf > $O/newtests_$TAG.log 2>&1
+      echo "newtests rc=$?"; grep -E "passed|failed|Error|swaps|rel-L2 engine" $O/newtests_$TAG.log | tail -30 ;;
+    configs)
+      timeout 1500 python bench.py --no-prefill --no-cpu-baseline --no-parity-sample > $O/configs_$TAG.json 2> $O/configs_$TAG.err
+      echo "configs rc=$?"; tail -c 1500 $O/configs_$TAG.json ;;
   esac
 done
