@@ -144,9 +144,13 @@ def test_prefill_engine_pre_pooling_64k(cuda_ok):
                                                       pooling=orc.PRE)
                 swaps += topk_swaps(idx[g, t, :cnt[g, t]], sel, pooled)
                 ref[(layer, g)] = sel
+        # outputs on identical index sets (the engine's; a documented near-tie
+        # swap of the pre-softmax ranking can move a key that one row weighs heavily)
         for g in range(Hkv):
-            y1, _, _ = orc.sparse_tile(*host[1], g, G, s, e, ref[(0, hm[g])])
-            y2, _, _ = orc.sparse_tile(*host[2], g, G, s, e, ref[(2, g)])
+            e1 = sets0[0][hm[g], t, :sets0[1][hm[g], t]].astype(np.int64)
+            e2 = sets2[0][g, t, :sets2[1][g, t]].astype(np.int64)
+            y1, _, _ = orc.sparse_tile(*host[1], g, G, s, e, e1)
+            y2, _, _ = orc.sparse_tile(*host[2], g, G, s, e, e2)
             assert_outputs_close(out[1, g * G:(g + 1) * G, s:e].float().cpu().numpy(), y1)
             assert_outputs_close(out[2, g * G:(g + 1) * G, s:e].float().cpu().numpy(), y2)
     print(f"pre-softmax prefill 64K: near-tie swaps {swaps}")

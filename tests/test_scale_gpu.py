@@ -101,8 +101,8 @@ def _decode_case(plan, L, B, Hq, Hkv, n, seed, check_seqs, max_swaps_per_list=2)
     for b in check_seqs:
         pooled = {}
         Y, sels, _ = orc.decode_step(qn[:, b], DeviceKV(Ks, b, n), DeviceKV(Vs, b, n), plan.anchors, maps,
-                                     plan.k_policy.fraction, plan.k_policy.k_min, want_mass=False,
-                                     pooled_out=pooled)
+                                     plan.k_policy.fraction, plan.k_policy.k_min, pooling=plan.pooling,
+                                     want_mass=False, pooled_out=pooled)
         for l, (idx, cnt) in snaps.items():
             for gg in range(Hkv):
                 assert int(cnt[b, gg]) == k, (l, b, gg, int(cnt[b, gg]), k)
