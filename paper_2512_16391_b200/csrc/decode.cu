@@ -139,11 +139,23 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
 #pragma unroll
   for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
 
+  // prologue: the positions of every prologue tile are loaded together (one
+  // L2 round trip instead of one per stage before the first gather issues)
+  {
+    int pos_pro[Cfg::kStages - 1][8];
 #pragma unroll
-  for (int s = 0; s < Cfg::kStages - 1; ++s) {
-    load_positions(s);
-    if (s < my_tiles) issue_tile(s, s);
-    cp_async_commit();
+    for (int s = 0; s < Cfg::kStages - 1; ++s) {
+      load_positions(s);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) pos_pro[s][i] = pos_next[i];
+    }
+#pragma unroll
+    for (int s = 0; s < Cfg::kStages - 1; ++s) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) pos_next[i] = pos_pro[s][i];
+      if (s < my_tiles) issue_tile(s, s);
+      cp_async_commit();
+    }
   }
   load_positions(Cfg::kStages - 1);
 

@@ -485,7 +485,9 @@ cudaError_t launch_topk(const TopkArgs& a, cudaStream_t st) {
   // 16 rows: 4: 64, 8: 54; 8 rows: 4: 62, 8: 44.  Warp-aggregated
   // (match_any) histogram atomics and a sample-bracketed single-CTA select
   // were measured slower and removed.
-  const int cl = a.len < 8192 ? 1 : (a.rows * 8 <= 148 ? 8 : (a.rows <= 148 ? 4 : 1));
+  // 16-CTA (non-portable) clusters when even 8 per row leave half the SMs idle
+  const int cl = a.len < 8192 ? 1 : (a.rows * 16 <= 148 ? 16 : (a.rows * 8 <= 148 ? 8 : (a.rows <= 148 ? 4 : 1)));
+  if (cl == 16) return launch_topk_cl<16>(a, st);
   if (cl == 8) return launch_topk_cl<8>(a, st);
   if (cl == 4) return launch_topk_cl<4>(a, st);
   return launch_topk_cl<1>(a, st);

@@ -42,6 +42,8 @@ def main():
     ref = torch.sort(torch.topk(pooled, k, dim=1).indices, dim=1).values.to(torch.int32)
     assert torch.equal(idx[:, :k], ref), "decode top-k differs from torch.topk"
     res["decode_64x128K"] = timed(lambda: ops.topk(pooled, k))
+    p8 = pooled[:8].contiguous()
+    res["shard_8x128K"] = timed(lambda: ops.topk(p8, k))
     p32 = pooled[:, :32768].contiguous()
     res["decode_64x32K"] = timed(lambda: ops.topk(p32, 32768 // 40))
     # prefill: 8 kv heads x T tiles, row t has 128 (t + 1) keys, k = 10 % (k_min 128)
