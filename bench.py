@@ -34,6 +34,8 @@ sys.path.insert(0, REPO)
 LLAMA_ANCHORS = [0, 2, 8, 13, 14]
 CFG = dict(model="Llama-3.1-8B attention", layers=32, Hq=32, Hkv=8, d=128)
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+SPEC_HBM_GBS = 8000.0          # north_star's "roughly 8 TB/s" (B200 DGX HBM3e)
+MUFU_EX2_PER_CLK_SM = 16       # MUFU ex2 throughput per SM per clock (B200; the guides' figure)
 
 
 def parse():
@@ -390,6 +392,23 @@ def cpu_prefill_sample(N, fraction, k_min, tiles=(0.25, 0.5, 0.75, 1.0)):
     return kascade, layer
 
 
+def _mufu_roofline(Hq, N, t_lse_ms, t_sel_ms, peaks):
+    """The anchor passes are exp-bound: pass A (LSE) and pass B (pooling)
+    each take one exponential per causal score, Hq*N(N+1)/2 per pass.  The
+    peak is the MUFU ex2 rate at the maximum SM clock (16 / clk / SM x 148
+    SMs); the 128K launches run under sw_power_cap below that clock, and
+    1/8 of the exponentials go to an FMA-pipe polynomial."""
+    exps = Hq * N * (N + 1) / 2
+    clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    peak = MUFU_EX2_PER_CLK_SM * 148 * clk
+    out = {"bound": "mufu_ex2", "exps_per_pass": exps, "unit": "exp/s", "peak": peak,
+           "peak_kind": f"16 ex2/clk/SM x 148 SMs at {clk / 1e6:.0f} MHz (max clock)"}
+    for name, t in (("pass_a_lse", t_lse_ms), ("pass_b_select", t_sel_ms)):
+        ach = exps / (t * 1e-3)
+        out[name] = {"ms": round(t, 3), "achieved": round(ach, 1), "frac": round(ach / peak, 4)}
+    return out
+
+
 def bench_prefill(args, dev, world, dist):
     """Llama-3.1-8B prefill at 128K (batch 1 per GPU): the full 32-layer
     Kascade forward and the dense (Top-k = 100%) forward of the same engine,
@@ -521,6 +540,7 @@ def bench_prefill(args, dev, world, dist):
                                 "unit": "GB/s", "peak_kind": "measured (scripts/micro/gather_bench.cu)",
                                 "frac": round(gather_bytes / (t_reuse * 1e-3) / 1e9 / gather_peak, 4)
                                 if gather_peak else None}},
+        "mufu": _mufu_roofline(Hq, N, t_lse, t_sel, peaks),
         "gpu_launches_per_step": 1 * 3 + n_anchor * 4 + n_reuse,
         "parity_sample": parity,
         "cpu_baseline": cpu_prefill,
@@ -1025,6 +1045,9 @@ def main():
         "roofline": {"kernel": "kscd sparse_decode (reuse layer)", "bound": "hbm",
                      "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": load_traffic(f"sparse_decode_{n // 1024}k_b{B}"),
+                     "frac_of_spec": round(achieved / SPEC_HBM_GBS, 4),
+                     "spec_note": f"frac_of_spec: against the ~{SPEC_HBM_GBS / 1000:g} TB/s north_star names (DGX B200; "
+                                  "7.7 TB/s HGX); frac: against the measured copy peak",
                      "peak_kind": peaks_kind,
                      "bytes_per_launch": reuse_bytes, "launch_ms": round(reuse_ms, 4),
                      "dense_decode_frac": round(dense_bytes / (dense_ms_launch * 1e-3) / 1e9 / hbm, 4),
@@ -1032,6 +1055,7 @@ def main():
                      "chained": {"launch_ms": round(chain_ms, 4),
                                  "achieved": round(reuse_bytes / (chain_ms * 1e-3) / 1e9, 1),
                                  "frac": round(reuse_bytes / (chain_ms * 1e-3) / 1e9 / hbm, 4),
+                                 "frac_of_spec": round(reuse_bytes / (chain_ms * 1e-3) / 1e9 / SPEC_HBM_GBS, 4),
                                  "note": "the 27 reuse launches back to back as in the step (PDL overlaps each "
                                          "launch's ramp with the previous tail), events around the chain only; "
                                          "achieved/frac above are per isolated launch"}},

@@ -149,9 +149,12 @@ typedef struct kscd_select_prefill_params {
   int64_t q_stride_head, kv_stride_head;
   float softmax_scale;
   const float* lse;        /* fp32 [Hq][N] from kscd_dense_prefill / kscd_anchor_lse_prefill */
-  float* pooled;           /* scratch fp32 [2][Hkv][T][pooled_stride] (all-heads: [2][1][T][...]):
-                              two partial-sum planes, the pooled row is plane0 + plane1 */
+  float* pooled;           /* fp32 scratch, kscd_select_prefill_scratch_size bytes: when one pass covers
+                              the kv group (G <= 4, not all-heads) two row planes per SM slot, each CTA
+                              selecting in its own tail (the fused anchor selection); otherwise
+                              [2][Hkv or 1][T][pooled_stride] partial-sum planes for a separate Top-k */
   int64_t pooled_stride;   /* >= N, multiple of 4 */
+  size_t pooled_bytes;     /* size of pooled (checked) */
   double topk_fraction;
   int32_t k_min;
   int32_t all_heads;       /* 1: all-heads-pooled mode, one shared set per tile (runner.py:180-197) */
@@ -290,6 +293,9 @@ int kscd_dense_probs(const kscd_probs_params* p, void* stream);
 int kscd_pool_tiles(const kscd_pool_tiles_params* p, void* stream);
 
 int kscd_append_kv(const kscd_append_kv_params* p, void* stream);
+
+/* Bytes of `pooled` scratch kscd_select_prefill needs for these shapes. */
+int kscd_select_prefill_scratch_size(const kscd_select_prefill_params* p, size_t* bytes);
 
 /* Pre-softmax pooled selection (see kscd_select_pre_params): q_bar, the
  * scores against K, the row softmax and the exact Top-k, stream-ordered. */

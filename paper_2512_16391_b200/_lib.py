@@ -74,7 +74,7 @@ class SelectPrefillParams(ctypes.Structure):
         ("num_q_heads", c_i32), ("num_kv_heads", c_i32), ("head_dim", c_i32), ("seq_len", c_i32),
         ("q", c_vp), ("k", c_vp), ("q_stride_head", c_i64), ("kv_stride_head", c_i64),
         ("softmax_scale", c_f32), ("lse", c_vp),
-        ("pooled", c_vp), ("pooled_stride", c_i64),
+        ("pooled", c_vp), ("pooled_stride", c_i64), ("pooled_bytes", c_sz),
         ("topk_fraction", c_f64), ("k_min", c_i32), ("all_heads", c_i32),
         ("indices", c_vp), ("counts", c_vp), ("k_cap", c_i32), ("tile_size", c_i32),
     ]
@@ -178,6 +178,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.kscd_k_budget.argtypes = [c_f64, c_i32, c_i32]
         lib.kscd_decode_workspace_size.restype = ctypes.c_int
         lib.kscd_decode_workspace_size.argtypes = [ctypes.POINTER(DecodeParams), ctypes.POINTER(c_sz)]
+        lib.kscd_select_prefill_scratch_size.restype = ctypes.c_int
+        lib.kscd_select_prefill_scratch_size.argtypes = [ctypes.POINTER(SelectPrefillParams), ctypes.POINTER(c_sz)]
         lib.kscd_select_pre_workspace_size.restype = ctypes.c_int
         lib.kscd_select_pre_workspace_size.argtypes = [ctypes.POINTER(SelectPreParams), ctypes.POINTER(c_sz)]
         _lib = lib

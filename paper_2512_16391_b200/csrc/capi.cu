@@ -398,6 +398,28 @@ extern "C" int kscd_pool_tiles(const kscd_pool_tiles_params* p, void* stream) {
   return cuda_status(kscd::launch_pool_rows(a, (cudaStream_t)stream), "kscd_pool_tiles");
 }
 
+namespace {
+// One pass-B launch covers every head of a kv group (G <= 4) in post mode:
+// the Top-k then runs in the tail of each pass-B CTA on its SM's scratch slot.
+bool select_prefill_fused(const kscd_select_prefill_params* p) {
+  return !p->all_heads && p->num_q_heads / p->num_kv_heads <= 4;
+}
+size_t select_prefill_scratch_bytes(const kscd_select_prefill_params* p) {
+  const size_t T = (size_t)(p->seq_len + 127) / 128;
+  const size_t rows = select_prefill_fused(p) ? (size_t)kscd::sm_slots() : (p->all_heads ? 1 : p->num_kv_heads) * T;
+  return 2 * rows * (size_t)p->pooled_stride * sizeof(float);
+}
+}  // namespace
+
+extern "C" int kscd_select_prefill_scratch_size(const kscd_select_prefill_params* p, size_t* bytes) {
+  if (!p || !bytes) return fail(KSCD_INVALID_ARGUMENT, "NULL argument");
+  if (p->num_q_heads < 1 || p->num_kv_heads < 1 || p->num_q_heads % p->num_kv_heads || p->seq_len < 1)
+    return fail(KSCD_INVALID_ARGUMENT, "bad shape");
+  if (p->pooled_stride < p->seq_len) return fail(KSCD_INVALID_ARGUMENT, "pooled_stride < seq_len");
+  *bytes = select_prefill_scratch_bytes(p);
+  return KSCD_OK;
+}
+
 extern "C" int kscd_select_prefill(const kscd_select_prefill_params* p, void* stream) {
   if (!p) return fail(KSCD_INVALID_ARGUMENT, "params is NULL");
   if (bad_head_dim(p->head_dim)) return fail(KSCD_UNSUPPORTED, KSCD_HEAD_DIM_MSG, p->head_dim);
@@ -410,7 +432,11 @@ extern "C" int kscd_select_prefill(const kscd_select_prefill_params* p, void* st
   if (p->k_min < 1) return fail(KSCD_INVALID_ARGUMENT, "k_min must be >= 1, got %d", p->k_min);
   if (!p->q || !p->k || !p->lse || !p->pooled || !p->indices || !p->counts)
     return fail(KSCD_INVALID_ARGUMENT, "NULL buffer");
-  if (p->pooled_stride < p->seq_len) return fail(KSCD_INVALID_ARGUMENT, "pooled_stride < seq_len");
+  if (p->pooled_stride < p->seq_len || (p->pooled_stride & 3) || ((uintptr_t)p->pooled & 15))
+    return fail(KSCD_INVALID_ARGUMENT, "pooled_stride must be >= seq_len and a multiple of 4, pooled 16-byte aligned");
+  if (p->pooled_bytes < select_prefill_scratch_bytes(p))
+    return fail(KSCD_INVALID_ARGUMENT, "pooled scratch too small (%zu < %zu bytes, kscd_select_prefill_scratch_size)",
+                p->pooled_bytes, select_prefill_scratch_bytes(p));
   const int kmax = kscd_k_budget(p->topk_fraction, p->k_min, p->seq_len);
   if (p->k_cap < kmax) return fail(KSCD_INVALID_ARGUMENT, "k_cap %d < k_budget %d", p->k_cap, kmax);
   const int G = p->num_q_heads / p->num_kv_heads;
@@ -430,6 +456,19 @@ extern "C" int kscd_select_prefill(const kscd_select_prefill_params* p, void* st
   pa.lse = p->lse;
   pa.pooled = p->pooled;
   pa.pool_stride = p->pooled_stride;
+  if (select_prefill_fused(p)) {
+    pa.head_begin = 0;
+    pa.nheads = G;
+    pa.g_fixed = -1;
+    pa.accumulate = 0;
+    pa.fuse = 1;
+    pa.idx = p->indices;
+    pa.counts = p->counts;
+    pa.k_cap = p->k_cap;
+    pa.fraction = p->topk_fraction;
+    pa.k_min = p->k_min;
+    return cuda_status(kscd::launch_pool_prefill(pa, st), "pool_prefill (fused Top-k)");
+  }
   const int gcount = p->all_heads ? p->num_kv_heads : 1;
   int launches = 0;
   for (int gi = 0; gi < gcount; ++gi) {

@@ -187,4 +187,12 @@ KSCD_DEV T warp_sum(T v) {
   return v;
 }
 
+// k_budget (tiles.py:81-89) on the device: floor of the fp64 product,
+// clamped below by k_min and above by n (the host's kscd_k_budget).
+KSCD_DEV int k_budget_dev(double fraction, int k_min, int n) {
+  long long kk = (long long)floor(fraction * (double)n);
+  kk = kk < k_min ? k_min : kk;
+  return (int)(kk > n ? n : kk);
+}
+
 }  // namespace kscd

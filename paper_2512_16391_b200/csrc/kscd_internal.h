@@ -115,10 +115,21 @@ struct PoolPrefillArgs {
   const __nv_bfloat16* k;
   int64_t q_sh, kv_sh;
   const float* lse;                       // [Hq][N] natural
-  float* pooled;                          // [Hkv or 1][T][pool_stride]
+  float* pooled;                          // [Hkv or 1][T][pool_stride]; fused: [slots][2][pool_stride]
   int64_t pool_stride;
+  // fused anchor selection (one launch covers the whole group, post mode):
+  // each CTA writes its pooled row into the slot of its SM and runs the exact
+  // Top-k of that row in its tail -- no [Hkv][T][N] scratch held for the layer
+  int fuse;
+  int* idx;                               // [Hkv][T][k_cap]
+  int* counts;                            // [Hkv][T]
+  int k_cap;
+  double fraction;
+  int k_min;
 };
 cudaError_t launch_pool_prefill(const PoolPrefillArgs& a, cudaStream_t st);
+constexpr int kSmSlots = 160;            // >= %smid + 1 on B200 (148 SMs): scratch slots of the fused pass B
+int sm_slots();
 
 // ------------------------------------------------------- calibration (calib.cu)
 struct MaskedMassArgs {

@@ -24,6 +24,7 @@
 // partial-sum plane that the Top-k reads as plane0 + plane1.
 #include "sm100.cuh"
 #include "kscd_internal.h"
+#include "topk_select.cuh"
 
 namespace kscd {
 using namespace sm100;
@@ -175,8 +176,10 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
     const int key_in_blk = q * 32 + lane;          // TMEM lane = key
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
     const int64_t plane = (int64_t)(a.g_fixed >= 0 ? 1 : a.Hkv) * T * a.pool_stride;
-    // all-heads-pooled mode writes one row per tile (runner.py:180-197)
-    float* out_row = a.pooled + x * plane + ((int64_t)(a.g_fixed >= 0 ? 0 : g) * T + ti) * a.pool_stride;
+    // all-heads-pooled mode writes one row per tile (runner.py:180-197);
+    // fused: the two planes of this SM's slot (one CTA per SM at a time)
+    float* out_row = a.fuse ? a.pooled + ((int64_t)smid_u32() * 2 + x) * a.pool_stride
+                            : a.pooled + x * plane + ((int64_t)(a.g_fixed >= 0 ? 0 : g) * T + ti) * a.pool_stride;
     const float2 sc2 = make_float2(a.scale_log2, a.scale_log2);
     for (int j = 0; j < nb; ++j) {
       const int key = j * kBlock + key_in_blk;
@@ -204,6 +207,23 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
       }
     }
   }
+  if (a.fuse && threadIdx.x == 0 && smid_u32() >= (uint32_t)kSmSlots) __trap();   // scratch slot bound
+  if (a.fuse) {
+    // ---- fused selection: the exact Top-k of this (kv head, tile) row with
+    // k = k_budget(t1) (runner.py:199-206), by all 384 threads.  Registers
+    // are rebalanced to an even split first; the pooled row was written by
+    // this CTA (visible after the barrier) and Q/K shared memory is free.
+    __syncwarp();
+    if (warp < 4) asm volatile("setmaxnreg.inc.sync.aligned.u32 168;\n");
+    else asm volatile("setmaxnreg.dec.sync.aligned.u32 168;\n");
+    __syncthreads();
+    TopkShared& tsh = *reinterpret_cast<TopkShared*>(smem + kOffQ);
+    const float* row0 = a.pooled + (int64_t)smid_u32() * 2 * a.pool_stride;
+    const int k = k_budget_dev(a.fraction, a.k_min, t1);
+    const int64_t r = (int64_t)g * T + ti;
+    topk_select<1, kThreads>(row0, row0 + a.pool_stride, t1, min(k, t1), a.idx + r * a.k_cap, a.k_cap,
+                             a.counts + r, tsh);
+  }
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
@@ -212,6 +232,7 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
 }
 
 // ------------------------------------------------------------------- host
+int sm_slots() { return kSmSlots; }
 bool make_prefill_map(CUtensorMap* m, const void* base, int heads, int rows, int64_t head_stride);
 
 cudaError_t launch_pool_prefill(const PoolPrefillArgs& a, cudaStream_t st) {

@@ -8,6 +8,12 @@ namespace kscd {
 namespace sm100 {
 
 // ------------------------------------------------------------- mbarrier
+KSCD_DEV uint32_t smid_u32() {
+  uint32_t v;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(v));
+  return v;
+}
+
 KSCD_DEV void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
 }

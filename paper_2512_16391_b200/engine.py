@@ -271,7 +271,7 @@ class KascadePrefill:
                                                                     prefill=True, all_heads=self.all_heads,
                                                                     num_q_heads=num_q_heads)
         else:
-            self.pooled = torch.empty(2, rows, T, (seq_len + 3) // 4 * 4, dtype=torch.float32, device=dev)
+            self.pooled = ops.select_prefill_scratch(num_q_heads, num_kv_heads, seq_len, dev, self.all_heads)
         self.indices = torch.empty(rows, T, kc, dtype=torch.int32, device=dev)
         self.counts = torch.zeros(rows, T, dtype=torch.int32, device=dev)
         self.out = torch.empty(num_layers, num_q_heads, seq_len, 128, dtype=torch.bfloat16, device=dev)

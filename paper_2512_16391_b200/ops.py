@@ -397,21 +397,36 @@ def prefill_k_cap(policy: KBudgetPolicy, N: int) -> int:
     return k_budget(policy, N)
 
 
+def select_prefill_scratch(num_q_heads: int, num_kv_heads: int, N: int, device, all_heads: bool = False
+                           ) -> torch.Tensor:
+    """The pooled scratch select_prefill needs (flat fp32; rows of stride
+    (N + 3) // 4 * 4): one row pair per SM when the pass B launch covers the
+    kv group and selects in its own tail (G <= 4, post mode -- ~150 MB at
+    128K), else the two [Hkv][T][N] partial planes of a separate Top-k."""
+    p = _lib.SelectPrefillParams(num_q_heads=num_q_heads, num_kv_heads=num_kv_heads, head_dim=HEAD_DIM,
+                                 seq_len=N, pooled_stride=(N + 3) // 4 * 4, all_heads=1 if all_heads else 0,
+                                 tile_size=TILE)
+    nbytes = _lib.c_sz(0)
+    _lib.check(_lib.load().kscd_select_prefill_scratch_size(ctypes.byref(p), ctypes.byref(nbytes)))
+    return torch.empty(nbytes.value // 4, dtype=torch.float32, device=device)
+
+
 def select_prefill(q, k, lse, policy: KBudgetPolicy, *, indices=None, counts=None, pooled=None,
                    all_heads: bool = False, scale=None):
     """Anchor selection of every (kv head, tile): pooled post-softmax weights
     (pass B, runner.py:148-152) and the exact Top-k with k = k_budget(causal
-    bound) (runner.py:199-206).  all_heads -> one shared set per tile."""
+    bound) (runner.py:199-206), fused into one launch when pass B covers the
+    kv group.  all_heads -> one shared set per tile.  ``pooled``: a flat fp32
+    scratch from select_prefill_scratch."""
     Hq, Hkv, N = _check_prefill_qkv(q, k, None)
     T = (N + TILE - 1) // TILE
     rows = 1 if all_heads else Hkv
     kc = prefill_k_cap(policy, N)
     dev = q.device
     if pooled is None:
-        # two partial-sum planes (one per column-sum warpgroup), row = sum
-        pooled = torch.empty(2, rows, T, (N + 3) // 4 * 4, dtype=torch.float32, device=dev)
-    if pooled.dim() != 4 or pooled.shape[:3] != (2, rows, T) or pooled.shape[3] < N or not pooled.is_contiguous():
-        raise InvalidArgumentError(f"pooled scratch must be fp32 [2][{rows}][{T}][>=N] contiguous")
+        pooled = select_prefill_scratch(Hq, Hkv, N, dev, all_heads)
+    if pooled.dtype != torch.float32 or not pooled.is_contiguous() or not pooled.is_cuda:
+        raise InvalidArgumentError("pooled scratch must be a contiguous CUDA fp32 tensor (select_prefill_scratch)")
     if indices is None:
         indices = torch.empty(rows, T, kc, dtype=torch.int32, device=dev)
     if counts is None:
@@ -419,7 +434,8 @@ def select_prefill(q, k, lse, policy: KBudgetPolicy, *, indices=None, counts=Non
     p = _lib.SelectPrefillParams(
         num_q_heads=Hq, num_kv_heads=Hkv, head_dim=HEAD_DIM, seq_len=N, q=q.data_ptr(), k=k.data_ptr(),
         q_stride_head=q.stride(0), kv_stride_head=k.stride(0), softmax_scale=float(scale or 0.0),
-        lse=lse.data_ptr(), pooled=pooled.data_ptr(), pooled_stride=pooled.stride(2),
+        lse=lse.data_ptr(), pooled=pooled.data_ptr(), pooled_stride=(N + 3) // 4 * 4,
+        pooled_bytes=pooled.numel() * 4,
         topk_fraction=float(policy.fraction), k_min=int(policy.k_min), all_heads=1 if all_heads else 0,
         indices=indices.data_ptr(), counts=counts.data_ptr(), k_cap=indices.shape[-1], tile_size=TILE)
     _lib.call("kscd_select_prefill", p, _stream())

@@ -49,7 +49,7 @@ def main():
         print(json.dumps({k_: (round(v_, 3) if isinstance(v_, float) else v_) for k_, v_ in res.items()}))
         return
     T = (N + 127) // 128
-    pooled = torch.empty(2, Hkv, T, (N + 3) // 4 * 4, dtype=torch.float32, device=dev)
+    pooled = ops.select_prefill_scratch(Hq, Hkv, N, dev)
     idx = torch.empty(Hkv, T, ops.prefill_k_cap(pol, N), dtype=torch.int32, device=dev)
     cnt = torch.empty(Hkv, T, dtype=torch.int32, device=dev)
     t = timeit(lambda: ops.select_prefill(q, k, lse, pol, indices=idx, counts=cnt, pooled=pooled))

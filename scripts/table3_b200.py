@@ -82,7 +82,7 @@ def prefill_rows():
         t_lse = ev(lambda i: ops.anchor_lse_prefill(qs[i % 2], ks[i % 2], lse=lse), reps)
         ops.dense_prefill(qs[0], ks[0], vs[0], out=out, lse=lse)
         T = (N + 127) // 128
-        pooled = torch.empty(2, Hkv, T, (N + 3) // 4 * 4, dtype=torch.float32, device="cuda")
+        pooled = ops.select_prefill_scratch(32, Hkv, N, "cuda")
         for pct in PCTS:
             pol = KBudgetPolicy(pct / 100.0, 128)
             idx = torch.empty(Hkv, T, ops.prefill_k_cap(pol, N), dtype=torch.int32, device="cuda")
