@@ -86,6 +86,24 @@ typedef struct kscd_decode_params {
   const int32_t* seq_lens;
 } kscd_decode_params;
 
+/* Several independent decode layers in ONE launch (e.g. every reuse layer
+ * between two anchors: they share the anchor's index lists and differ in
+ * queries, caches and head maps).  `p` describes layer 0 (shapes, strides,
+ * lists, q/out of layer 0); layer l reads q + l*q_stride_layer and caches
+ * k_caches[l] / v_caches[l] (same shape and strides as layer 0), routes
+ * through head_maps[l*Hkv ...] and writes out + l*out_stride_layer.  The
+ * workspace holds kscd_decode_layers_workspace_size bytes.  No scores or lse
+ * outputs.  A launch of L layers has L x the CTAs of one, so small layers
+ * (few (sequence, kv head) rows, short lists) stop paying a grid ramp each. */
+typedef struct kscd_decode_layers {
+  int32_t num_layers;
+  const void* const* k_caches;  /* device array of L pointers, bf16 [B][Hkv][n_cap][128] */
+  const void* const* v_caches;
+  int64_t q_stride_layer;       /* elements between consecutive layers' q */
+  int64_t out_stride_layer;     /* elements between consecutive layers' out */
+  const int32_t* head_maps;     /* device int32 [L][Hkv], or NULL = identity */
+} kscd_decode_layers;
+
 /* Selection of one decode step: pooled post-softmax weights of the G heads
  * of each kv head (runner.py:148-152), k = k_budget(n) (tiles.py:81-89) and
  * the exact Top-k (attention.py:147-174). */
@@ -244,6 +262,12 @@ const char* kscd_last_error(void);
 
 /* Bytes of workspace the decode entry points need for these shapes. */
 int kscd_decode_workspace_size(const kscd_decode_params* p, size_t* bytes);
+/* ... and a multi-layer launch of num_layers layers. */
+int kscd_decode_layers_workspace_size(const kscd_decode_params* p, int32_t num_layers, size_t* bytes);
+/* Reuse / sparse layers (as kscd_sparse_decode) and dense layers (as
+ * kscd_dense_decode without scores or lse), several per launch. */
+int kscd_sparse_decode_layers(const kscd_decode_params* p, const kscd_decode_layers* layers, void* stream);
+int kscd_dense_decode_layers(const kscd_decode_params* p, const kscd_decode_layers* layers, void* stream);
 
 /* Dense attention of the step's query over keys 0..n-1: out, lse, and --
  * when p->scores != NULL -- the scores the anchor-0 selection pools.

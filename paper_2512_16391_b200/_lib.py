@@ -117,6 +117,13 @@ class SelectPreParams(ctypes.Structure):
     ]
 
 
+class DecodeLayers(ctypes.Structure):
+    _fields_ = [
+        ("num_layers", c_i32), ("k_caches", c_vp), ("v_caches", c_vp),
+        ("q_stride_layer", c_i64), ("out_stride_layer", c_i64), ("head_maps", c_vp),
+    ]
+
+
 # entry point name -> params struct (None for non-struct signatures)
 class MaskedMassParams(ctypes.Structure):
     _fields_ = [
@@ -178,6 +185,12 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.kscd_k_budget.argtypes = [c_f64, c_i32, c_i32]
         lib.kscd_decode_workspace_size.restype = ctypes.c_int
         lib.kscd_decode_workspace_size.argtypes = [ctypes.POINTER(DecodeParams), ctypes.POINTER(c_sz)]
+        for name in ("kscd_sparse_decode_layers", "kscd_dense_decode_layers"):
+            fn = getattr(lib, name)
+            fn.argtypes = [ctypes.POINTER(DecodeParams), ctypes.POINTER(DecodeLayers), c_vp]
+            fn.restype = ctypes.c_int
+        lib.kscd_decode_layers_workspace_size.restype = ctypes.c_int
+        lib.kscd_decode_layers_workspace_size.argtypes = [ctypes.POINTER(DecodeParams), c_i32, ctypes.POINTER(c_sz)]
         lib.kscd_select_prefill_scratch_size.restype = ctypes.c_int
         lib.kscd_select_prefill_scratch_size.argtypes = [ctypes.POINTER(SelectPrefillParams), ctypes.POINTER(c_sz)]
         lib.kscd_select_pre_workspace_size.restype = ctypes.c_int
@@ -198,6 +211,9 @@ def check(rc: int) -> None:
     raise KascadeError(msg)
 
 
-def call(name: str, params, stream_ptr: int) -> None:
+def call(name: str, params, stream_ptr: int, extra=None) -> None:
     fn = getattr(load(), name)
-    check(fn(ctypes.byref(params), c_vp(stream_ptr)))
+    if extra is None:
+        check(fn(ctypes.byref(params), c_vp(stream_ptr)))
+    else:
+        check(fn(ctypes.byref(params), ctypes.byref(extra), c_vp(stream_ptr)))

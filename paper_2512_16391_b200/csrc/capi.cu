@@ -203,6 +203,52 @@ int kscd_sparse_decode(const kscd_decode_params* p, void* stream) {
   return cuda_status(kscd::launch_decode_attn(kscd::MODE_SPARSE, a, (cudaStream_t)stream), "kscd_sparse_decode");
 }
 
+// ---- several independent layers in one launch -------------------------
+size_t decode_layer_ws_bytes(const kscd_decode_params* p) { return (decode_ws_bytes(p) + 255) & ~(size_t)255; }
+
+int kscd_decode_layers_workspace_size(const kscd_decode_params* p, int32_t num_layers, size_t* bytes) {
+  if (!p || !bytes || num_layers < 1) return fail(KSCD_INVALID_ARGUMENT, "NULL argument or num_layers < 1");
+  *bytes = decode_layer_ws_bytes(p) * (size_t)num_layers;
+  return KSCD_OK;
+}
+
+static int decode_layers(int mode, const kscd_decode_params* p, const kscd_decode_layers* t, void* stream,
+                         const char* what) {
+  if (!t) return fail(KSCD_INVALID_ARGUMENT, "layers is NULL");
+  if (t->num_layers < 1) return fail(KSCD_INVALID_ARGUMENT, "num_layers must be >= 1");
+  if (!t->k_caches || !t->v_caches) return fail(KSCD_INVALID_ARGUMENT, "k_caches/v_caches must be non-NULL");
+  if (p && (p->scores || p->lse)) return fail(KSCD_INVALID_ARGUMENT, "multi-layer launches take no scores/lse outputs");
+  if (p && (t->q_stride_layer < (int64_t)p->batch * p->num_q_heads * 128 ||
+            t->out_stride_layer < (int64_t)p->batch * p->num_q_heads * 128))
+    return fail(KSCD_INVALID_ARGUMENT, "layer strides of q/out overlap");
+  int rc = check_decode(p, true, mode == kscd::MODE_SPARSE);
+  if (rc) return rc;
+  const size_t per = decode_layer_ws_bytes(p);
+  if (p->workspace_bytes < per * (size_t)t->num_layers)
+    return fail(KSCD_INVALID_ARGUMENT, "workspace too small for %d layers (%zu < %zu bytes)", t->num_layers,
+                p->workspace_bytes, per * (size_t)t->num_layers);
+  kscd::DecodeArgs a = make_args(p, mode == kscd::MODE_SPARSE ? p->k_cap : p->seq_len);
+  a.scores = nullptr;
+  a.lse = nullptr;
+  a.nl = t->num_layers;
+  a.k_tab = (const __nv_bfloat16* const*)t->k_caches;
+  a.v_tab = (const __nv_bfloat16* const*)t->v_caches;
+  a.q_ls = t->q_stride_layer;
+  a.out_ls = t->out_stride_layer;
+  a.head_map = t->head_maps;
+  a.hm_ls = p->num_kv_heads;
+  a.ws_ls = (int64_t)per;
+  return cuda_status(kscd::launch_decode_attn(mode, a, (cudaStream_t)stream), what);
+}
+
+int kscd_sparse_decode_layers(const kscd_decode_params* p, const kscd_decode_layers* t, void* stream) {
+  return decode_layers(kscd::MODE_SPARSE, p, t, stream, "kscd_sparse_decode_layers");
+}
+
+int kscd_dense_decode_layers(const kscd_decode_params* p, const kscd_decode_layers* t, void* stream) {
+  return decode_layers(kscd::MODE_DENSE, p, t, stream, "kscd_dense_decode_layers");
+}
+
 int kscd_select_decode(const kscd_select_decode_params* p, void* stream) {
   if (!p) return fail(KSCD_INVALID_ARGUMENT, "params is NULL");
   if (p->batch < 1 || p->num_q_heads < 1 || p->num_kv_heads < 1 || p->num_q_heads % p->num_kv_heads)

@@ -50,14 +50,25 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
     decode_attn_kernel(const DecodeArgs a) {
   using Cfg = DecodeCfg<MODE, STG>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;   // g: (virtual) head group
+  const int split = blockIdx.x, g = blockIdx.y;                     // g: (virtual) head group
+  const int lyr = blockIdx.z / a.B, b = blockIdx.z - lyr * a.B;        // layer of a multi-layer launch
   const int gk = g / a.kv_rep;                                        // its kv head
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int G = a.G;
+  // this layer's tensors (a multi-layer launch runs consecutive independent
+  // layers -- e.g. all reuse layers between two anchors -- as one grid)
+  const __nv_bfloat16* q_l = a.q + (int64_t)lyr * a.q_ls;
+  const __nv_bfloat16* k_l = a.k_tab ? a.k_tab[lyr] : a.k;
+  const __nv_bfloat16* v_l = a.v_tab ? a.v_tab[lyr] : a.v;
+  float* out_l = a.out ? a.out + (int64_t)lyr * a.out_ls : nullptr;
+  const int* hm_l = a.head_map ? a.head_map + (int64_t)lyr * a.hm_ls : nullptr;
+  float* part_l = reinterpret_cast<float*>(reinterpret_cast<char*>(a.part) + (int64_t)lyr * a.ws_ls);
+  float* part_ml_l = reinterpret_cast<float*>(reinterpret_cast<char*>(a.part_ml) + (int64_t)lyr * a.ws_ls);
+  int* counters_l = reinterpret_cast<int*>(reinterpret_cast<char*>(a.counters) + (int64_t)lyr * a.ws_ls);
 
-  const __nv_bfloat16* kbase = a.k + (int64_t)b * a.kv_sb + (int64_t)gk * a.kv_sh;
-  const __nv_bfloat16* vbase = a.v + (int64_t)b * a.kv_sb + (int64_t)gk * a.kv_sh;
+  const __nv_bfloat16* kbase = k_l + (int64_t)b * a.kv_sb + (int64_t)gk * a.kv_sh;
+  const __nv_bfloat16* vbase = v_l + (int64_t)b * a.kv_sb + (int64_t)gk * a.kv_sh;
   const int* sel = nullptr;
   // Programmatic dependent launch (consecutive decode layers): let the next
   // layer's kernel start filling SMs as ours retire.  Our inputs are all
@@ -70,7 +81,7 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   int count = a.lens ? min(__ldg(a.lens + b), a.n) : a.n;
   if (MODE == MODE_SPARSE) {
-    const int src = a.head_map ? __ldg(a.head_map + gk) : gk;
+    const int src = hm_l ? __ldg(hm_l + gk) : gk;
     sel = a.idx + (int64_t)b * a.idx_sb + (int64_t)src * a.idx_sh;
     count = min(__ldg(a.cnt + (int64_t)b * a.cnt_sb + src), a.k_cap);
   }
@@ -83,7 +94,7 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
   // ---- Q fragments (A operand: rows = query heads of the group) --------
   uint32_t qa0[8], qa2[8], qa1[8], qa3[8];
   {
-    const __nv_bfloat16* qg = a.q + ((int64_t)b * a.Hq + (int64_t)g * G) * kHeadDim;
+    const __nv_bfloat16* qg = q_l + ((int64_t)b * a.Hq + (int64_t)g * G) * kHeadDim;
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
       const int c = ks * 16 + 2 * tig;
@@ -306,13 +317,13 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
     if (a.splits == 1) {
       const float inv = L > 0.f ? 1.f / L : 0.f;
       if (Cfg::kHasV)
-        *reinterpret_cast<float4*>(a.out + (bh0 + h) * kHeadDim + lane * 4) =
+        *reinterpret_cast<float4*>(out_l + (bh0 + h) * kHeadDim + lane * 4) =
             make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
       if (lane == 0 && a.lse) a.lse[bh0 + h] = (M + __log2f(L)) * kLn2;
     } else {
       const int64_t pi = (bh0 + h) * a.splits + split;
-      if (Cfg::kHasV) *reinterpret_cast<float4*>(a.part + pi * kHeadDim + lane * 4) = acc;
-      if (lane == 0) *reinterpret_cast<float2*>(a.part_ml + pi * 2) = make_float2(M, L);
+      if (Cfg::kHasV) *reinterpret_cast<float4*>(part_l + pi * kHeadDim + lane * 4) = acc;
+      if (lane == 0) *reinterpret_cast<float2*>(part_ml_l + pi * 2) = make_float2(M, L);
     }
   }
   if (a.splits == 1) return;
@@ -322,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
   __threadfence();
   __syncthreads();
   if (tid == 0) {
-    int* ctr = a.counters + (int64_t)b * a.Hkv + g;
+    int* ctr = counters_l + (int64_t)b * a.Hkv + g;
     const int prev = atomicAdd(ctr, 1);
     is_last = prev == a.splits - 1;
     if (is_last) *ctr = 0;  // re-arm for the next launch / graph replay
@@ -341,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
 #pragma unroll
     for (int i = 0; i < kMaxSplitsDev / 32; ++i) {
       const int sp = lane + 32 * i;
-      ml[i] = sp < a.splits ? __ldcg(reinterpret_cast<const float2*>(a.part_ml + (p0 + sp) * 2))
+      ml[i] = sp < a.splits ? __ldcg(reinterpret_cast<const float2*>(part_ml_l + (p0 + sp) * 2))
                             : make_float2(-INFINITY, 0.f);
     }
     float M = -INFINITY;
@@ -365,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
         float4 v[kB];
 #pragma unroll
         for (int u = 0; u < kB; ++u)
-          v[u] = sp0 + u < a.splits ? __ldcg(reinterpret_cast<const float4*>(a.part + (p0 + sp0 + u) * kHeadDim + lane * 4))
+          v[u] = sp0 + u < a.splits ? __ldcg(reinterpret_cast<const float4*>(part_l + (p0 + sp0 + u) * kHeadDim + lane * 4))
                                     : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int u = 0; u < kB; ++u) {
@@ -374,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
         }
       }
       const float inv = L > 0.f ? 1.f / L : 0.f;
-      *reinterpret_cast<float4*>(a.out + (bh0 + h) * kHeadDim + lane * 4) =
+      *reinterpret_cast<float4*>(out_l + (bh0 + h) * kHeadDim + lane * 4) =
           make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
     }
     if (lane == 0 && a.lse) a.lse[bh0 + h] = (M + __log2f(L)) * kLn2;
@@ -385,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
 template <int MODE, int STG = 0>
 static cudaError_t launch_mode(const DecodeArgs& a, cudaStream_t st) {
   using Cfg = DecodeCfg<MODE, STG>;
-  dim3 grid(a.splits, a.Hkv, a.B);
+  dim3 grid(a.splits, a.Hkv, a.B * (a.nl > 0 ? a.nl : 1));
   const int smem = Cfg::kSmemBytes;
   // one-time opt-in to >48 KB dynamic shared memory per instantiation
   static const cudaError_t attr_hi = cudaFuncSetAttribute(

@@ -37,6 +37,13 @@ struct DecodeArgs {
   // virtual ones, and virtual head gv reads kv head gv / kv_rep
   int kv_rep;
   const int* lens;                        // [B] per-sequence key counts (nullable => n)
+  // several layers in one launch (blockIdx.z = layer * B + b): layer l reads
+  // q + l*q_ls, caches k_tab[l] / v_tab[l] (nullable => k / v), head_map +
+  // l*hm_ls, writes out + l*out_ls, and uses the workspace at + l*ws_ls bytes
+  int nl;
+  const __nv_bfloat16* const* k_tab;
+  const __nv_bfloat16* const* v_tab;
+  int64_t q_ls, out_ls, hm_ls, ws_ls;
 };
 
 cudaError_t launch_decode_attn(int mode, const DecodeArgs& a, cudaStream_t st);

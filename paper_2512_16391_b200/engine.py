@@ -79,6 +79,25 @@ class KascadeDecoder:
         # the executor's own split-K workspace: its layers run stream-ordered,
         # so they share it; no other executor, stream or graph touches it
         self.ws = ops.new_decode_workspace(dev, batch, num_q_heads, num_kv_heads)
+        # consecutive reuse layers run as ONE multi-layer launch (they only
+        # share the anchor's lists); run_end[l] = end of l's reuse run
+        self.run_end: Dict[int, int] = {}
+        l = 0
+        while l < num_layers:
+            if self.kinds[l] != KIND_REUSE:
+                l += 1
+                continue
+            e = l
+            while e < num_layers and self.kinds[e] == KIND_REUSE:
+                e += 1
+            for i in range(l, e):
+                self.run_end[i] = e
+            l = e
+        self.map_table = torch.stack([self.head_maps[l] if self.kinds[l] == KIND_REUSE else
+                                      torch.zeros(num_kv_heads, dtype=torch.int32, device=dev)
+                                      for l in range(num_layers)]).contiguous()
+        self.ws_layers = ops.new_decode_layers_workspace(dev, batch, num_q_heads, num_kv_heads, num_layers)
+        self._tables = {}
         self._graphs = {}
         self.seq_lens: Optional[torch.Tensor] = None     # ragged batch (step / dense_step)
 
@@ -94,9 +113,42 @@ class KascadeDecoder:
         if seq_len > self.n_max:
             raise InvalidArgumentError(f"seq_len {seq_len} exceeds max_seq_len {self.n_max}")
         self.seq_lens = seq_lens
-        for l in range(self.L):
-            self._layer(l, q, k_caches, v_caches, seq_len)
+        self._run_range(0, self.L, q, k_caches, v_caches, seq_len)
         return self.out
+
+    def _layer_tables(self, k_caches, v_caches, l0: int, l1: int):
+        """Device pointer tables of layers [l0, l1)'s caches (cached: built
+        on the eager warm-up before any graph capture)."""
+        key = (l0, l1) + tuple(t.data_ptr() for t in k_caches[l0:l1]) + tuple(t.data_ptr() for t in v_caches[l0:l1])
+        tab = self._tables.get(key)
+        if tab is None:
+            if torch.cuda.is_current_stream_capturing():
+                raise InvalidArgumentError("new cache buffers inside a CUDA graph capture: run the step eagerly first")
+            kp = torch.tensor([t.data_ptr() for t in k_caches[l0:l1]], dtype=torch.int64, device=self.device)
+            vp = torch.tensor([t.data_ptr() for t in v_caches[l0:l1]], dtype=torch.int64, device=self.device)
+            tab = self._tables[key] = (kp, vp)
+        return tab
+
+    def _run_range(self, l0: int, l1: int, q, k_caches, v_caches, seq_len: int, dense: bool = False) -> None:
+        """Layers [l0, l1): every run of consecutive reuse layers (every
+        layer in dense mode) is one multi-layer launch; anchors run alone."""
+        l = l0
+        while l < l1:
+            end = l1 if dense else (min(self.run_end[l], l1) if self.kinds[l] == KIND_REUSE else l + 1)
+            # one launch needs one cache layout; dense layers of a ragged batch
+            # run per layer (the multi-layer launch has no per-sequence lengths)
+            fuse = end - l >= 2 and not (dense and self.seq_lens is not None) and all(
+                t.shape == k_caches[l].shape and t.stride() == k_caches[l].stride()
+                for t in list(k_caches[l:end]) + list(v_caches[l:end]))
+            if fuse:
+                ops.decode_layers(q[l:end], k_caches[l:end], v_caches[l:end], seq_len, out=self.out[l:end],
+                                  workspace=self.ws_layers, tables=self._layer_tables(k_caches, v_caches, l, end),
+                                  indices=None if dense else self.indices, counts=None if dense else self.counts,
+                                  head_maps=None if dense else self.map_table[l:end])
+            else:
+                for i in range(l, end):
+                    (self._dense_layer if dense else self._layer)(i, q, k_caches, v_caches, seq_len)
+            l = end
 
     def _layer(self, l: int, q, k_caches, v_caches, seq_len: int) -> None:
         """The kernels of layer l (runner.py:250-275 for one decode token)."""
@@ -137,10 +189,11 @@ class KascadeDecoder:
 
     def dense_step(self, q, k_caches, v_caches, seq_len: int, seq_lens: Optional[torch.Tensor] = None
                    ) -> torch.Tensor:
-        """Top-k = 100% baseline: dense attention on every layer."""
+        """Top-k = 100% baseline: dense attention on every layer (one launch
+        for all layers, like the Kascade step's reuse runs; per layer with a
+        ragged batch)."""
         self.seq_lens = seq_lens
-        for l in range(self.L):
-            self._dense_layer(l, q, k_caches, v_caches, seq_len)
+        self._run_range(0, self.L, q, k_caches, v_caches, seq_len, dense=True)
         return self.out
 
     # -------------------------------------------------------------- graphs
@@ -180,7 +233,6 @@ class KascadeDecoder:
                                        f"cache capacity {n_cap})]")
         kv_dev = torch.empty(kv_host.shape, dtype=torch.bfloat16, device=self.device)
         tables0, tables_rest = (kp[:1], vp[:1], sb, sh, n_cap), (kp[1:], vp[1:], sb, sh, n_cap)
-        layer = self._dense_layer if dense else self._layer
         # The copies are pipelined against the layer loop on two side streams
         # (graph branches): layer 0's new K/V rows and queries arrive first
         # and layer 0 starts behind their append; the other layers' rows and
@@ -208,19 +260,22 @@ class KascadeDecoder:
                 ev_rest.record(h2d)
             main.wait_event(ev_first)
             ops.append_kv(kv_dev[:1], seq_len - 1, tables0, seq_lens)
+            # segments: layer 0 alone (its rows and queries arrive first), then
+            # the layers between the output-copy boundaries
+            bounds = sorted({0, 1, self.L} | set(ends))
             start = 0
-            for l in range(self.L):
-                if l == 1:
+            for a_, b_ in zip(bounds[:-1], bounds[1:]):
+                if a_ == 1:
                     main.wait_event(ev_rest)
                     ops.append_kv(kv_dev[1:], seq_len - 1, tables_rest, seq_lens)
-                layer(l, q, k_caches, v_caches, seq_len)
-                if l + 1 in ends:
-                    c = ends.index(l + 1)
+                self._run_range(a_, b_, q, k_caches, v_caches, seq_len, dense=dense)
+                if b_ in ends:
+                    c = ends.index(b_)
                     ev_done[c].record(main)
                     with torch.cuda.stream(d2h):
                         d2h.wait_event(ev_done[c])
-                        out_host[start:l + 1].copy_(self.out[start:l + 1], non_blocking=True)
-                    start = l + 1
+                        out_host[start:b_].copy_(self.out[start:b_], non_blocking=True)
+                    start = b_
             main.wait_stream(h2d)
             main.wait_stream(d2h)
 

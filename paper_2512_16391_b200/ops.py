@@ -116,6 +116,15 @@ def decode_workspace(device: torch.device, B: int, Hq: int, Hkv: int) -> torch.T
     return ws
 
 
+def new_decode_layers_workspace(device, B: int, Hq: int, Hkv: int, num_layers: int) -> torch.Tensor:
+    """Zero-filled workspace of a multi-layer decode launch (one split-K
+    block per layer, each self re-arming like new_decode_workspace's)."""
+    p = _lib.DecodeParams(batch=B, num_q_heads=Hq, num_kv_heads=Hkv, head_dim=HEAD_DIM, seq_len=1)
+    nbytes = _lib.c_sz(0)
+    _lib.check(_lib.load().kscd_decode_layers_workspace_size(ctypes.byref(p), int(num_layers), ctypes.byref(nbytes)))
+    return torch.zeros(nbytes.value, dtype=torch.uint8, device=device)
+
+
 def _check_seq_lens(seq_lens: Optional[torch.Tensor], B: int, n: int) -> None:
     """Ragged batch: device int32 [B], every entry in [1, seq_len] (checked
     on the device side by the kernels' min(); values are the caller's)."""
@@ -294,6 +303,38 @@ def anchor_decode(q, k_cache, v_cache, seq_len, policy: KBudgetPolicy, *, layer0
         hm = torch.zeros(Hkv, dtype=torch.int32, device=q.device)
     out = sparse_decode(q, k_cache, v_cache, seq_len, indices, counts, hm, out=out)
     return out, lse, indices, counts
+
+
+def decode_layers(q, k_caches, v_caches, seq_len, *, out, workspace, tables, indices=None, counts=None,
+                  head_maps=None, scale=None, num_splits=0):
+    """Several independent decode layers in ONE launch: sparse (reuse) layers
+    when ``indices`` is given -- layer l attends indices[b][head_maps[l][g]]
+    (runner.py:210-225) -- else dense layers.  q / out: [nl][B][Hq][128]
+    (layer-strided views, e.g. slices of the executor's buffers); k_caches /
+    v_caches: nl caches of one shape and stride layout; ``tables``: their
+    device pointer arrays (cache_pointer_tables); head_maps: device int32
+    [nl][Hkv] or None (identity)."""
+    nl = len(k_caches)
+    if q.dim() != 4 or out.dim() != 4 or q.shape[0] != nl or out.shape[0] != nl or q.shape[1:] != out.shape[1:] \
+            or not q[0].is_contiguous() or not out[0].is_contiguous():
+        raise InvalidArgumentError("q / out must be [nl][B][Hq][128] with contiguous layers")
+    sparse = indices is not None
+    p = _decode_params(q[0], k_caches[0], v_caches[0], seq_len, out[0], None, None, scale, num_splits,
+                       workspace=workspace)
+    if sparse:
+        if indices.dtype != torch.int32 or counts.dtype != torch.int32 or indices.dim() != 3 \
+                or not indices.is_contiguous() or not counts.is_contiguous() or counts.shape != indices.shape[:2]:
+            raise InvalidArgumentError("indices must be int32 [B][Hsrc][k_cap], counts int32 [B][Hsrc]")
+        p.indices, p.counts = indices.data_ptr(), counts.data_ptr()
+        p.k_cap, p.num_src_heads = indices.shape[2], indices.shape[1]
+    if head_maps is not None and (head_maps.dtype != torch.int32 or tuple(head_maps.shape) != (nl, p.num_kv_heads)
+                                  or not head_maps.is_contiguous()):
+        raise InvalidArgumentError("head_maps must be a contiguous CUDA int32 [nl][Hkv] tensor")
+    kp, vp = tables[0], tables[1]
+    t = _lib.DecodeLayers(num_layers=nl, k_caches=kp.data_ptr(), v_caches=vp.data_ptr(),
+                          q_stride_layer=q.stride(0), out_stride_layer=out.stride(0), head_maps=_ptr(head_maps))
+    _lib.call("kscd_sparse_decode_layers" if sparse else "kscd_dense_decode_layers", p, _stream(), t)
+    return out
 
 
 def reuse_decode(q, k_cache, v_cache, seq_len, indices, counts, head_map=None, *, out=None):

@@ -77,7 +77,8 @@ STRUCTS = {"kscd_decode_params": "DecodeParams", "kscd_select_decode_params": "S
            "kscd_topk_params": "TopkParams", "kscd_prefill_params": "PrefillParams",
            "kscd_select_prefill_params": "SelectPrefillParams", "kscd_probs_params": "ProbsParams",
            "kscd_pool_tiles_params": "PoolTilesParams", "kscd_append_kv_params": "AppendKvParams",
-           "kscd_masked_mass_params": "MaskedMassParams", "kscd_select_pre_params": "SelectPreParams"}
+           "kscd_masked_mass_params": "MaskedMassParams", "kscd_select_pre_params": "SelectPreParams",
+           "kscd_decode_layers": "DecodeLayers"}
 
 
 def _header_fields():
