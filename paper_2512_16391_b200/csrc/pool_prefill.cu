@@ -207,21 +207,21 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
       }
     }
   }
-  if (a.fuse && threadIdx.x == 0 && smid_u32() >= (uint32_t)kSmSlots) __trap();   // scratch slot bound
-  if (a.fuse) {
+  if (a.fuse && warp >= 4) {
     // ---- fused selection: the exact Top-k of this (kv head, tile) row with
-    // k = k_budget(t1) (runner.py:199-206), by all 384 threads.  Registers
-    // are rebalanced to an even split first; the pooled row was written by
-    // this CTA (visible after the barrier) and Q/K shared memory is free.
-    __syncwarp();
-    if (warp < 4) asm volatile("setmaxnreg.inc.sync.aligned.u32 168;\n");
-    else asm volatile("setmaxnreg.dec.sync.aligned.u32 168;\n");
-    __syncthreads();
+    // k = k_budget(t1) (runner.py:199-206), run by the two column-sum
+    // warpgroups (256 threads, named barrier 1) right after they wrote the
+    // row; the producer / MMA warps keep their reduced register budget and
+    // wait at the final barrier.  The row's global writes are visible to the
+    // group after the barrier, and Q shared memory is free (every MMA retired
+    // before the last column sums were read).
+    asm volatile("bar.sync 1, 256;\n" ::: "memory");
+    if (threadIdx.x == 128 && smid_u32() >= (uint32_t)kSmSlots) __trap();   // scratch slot bound
     TopkShared& tsh = *reinterpret_cast<TopkShared*>(smem + kOffQ);
     const float* row0 = a.pooled + (int64_t)smid_u32() * 2 * a.pool_stride;
     const int k = k_budget_dev(a.fraction, a.k_min, t1);
     const int64_t r = (int64_t)g * T + ti;
-    topk_select<1, kThreads>(row0, row0 + a.pool_stride, t1, min(k, t1), a.idx + r * a.k_cap, a.k_cap,
+    topk_select<1, 256, 128>(row0, row0 + a.pool_stride, t1, min(k, t1), a.idx + r * a.k_cap, a.k_cap,
                              a.counts + r, tsh);
   }
   __syncthreads();

@@ -29,11 +29,20 @@ KSCD_DEV uint32_t order_key(float f) {
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-// Exclusive prefix sum over the NT threads of the block (thread order).
-template <int NT = kTopkThreads>
+// Barrier of the NT threads taking part: the whole CTA (TID0 = 0), or the
+// warps from thread TID0 on through named barrier 1 (the fused prefill
+// selection runs on the pass-B column-sum warpgroups only).
+template <int NT, int TID0>
+KSCD_DEV void tk_sync() {
+  if (TID0 == 0) __syncthreads();
+  else asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory");
+}
+
+// Exclusive prefix sum over the NT threads (thread order).
+template <int NT = kTopkThreads, int TID0 = 0>
 KSCD_DEV uint32_t block_excl_scan(uint32_t v, uint32_t* warp_tot, uint32_t& total) {
   constexpr int kTopkWarps = NT / 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = (threadIdx.x - TID0) >> 5;
   uint32_t x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -41,7 +50,7 @@ KSCD_DEV uint32_t block_excl_scan(uint32_t v, uint32_t* warp_tot, uint32_t& tota
     if (lane >= o) x += y;
   }
   if (lane == 31) warp_tot[warp] = x;
-  __syncthreads();
+  tk_sync<NT, TID0>();
   if (warp == 0) {
     const uint32_t w = lane < kTopkWarps ? warp_tot[lane] : 0u;
     uint32_t wx = w;
@@ -53,10 +62,10 @@ KSCD_DEV uint32_t block_excl_scan(uint32_t v, uint32_t* warp_tot, uint32_t& tota
     if (lane < kTopkWarps) warp_tot[lane] = wx - w;  // exclusive warp offsets
     if (lane == 31) warp_tot[32] = wx;
   }
-  __syncthreads();
+  tk_sync<NT, TID0>();
   const uint32_t res = warp_tot[warp] + x - v;
   total = warp_tot[32];
-  __syncthreads();
+  tk_sync<NT, TID0>();
   return res;
 }
 
@@ -116,12 +125,13 @@ struct TopkShared {
 // counts_out (written by CTA 0 of the cluster) = take.  NT threads of the CTA
 // take part; CL CTAs of a cluster split the row.  Used by topk_kernel and by
 // the fused anchor-selection tail of pool_prefill_kernel (NT = 384, CL = 1).
-template <int CL, int NT>
+template <int CL, int NT, int TID0 = 0>
 KSCD_DEV void topk_select(const float* vals, const float* vals2, int n, int take, int* out, int k_cap,
                           int* counts_out, TopkShared& sh) {
+  static_assert(CL == 1 || TID0 == 0, "a cluster-split row runs on whole CTAs");
   cg::cluster_group cluster = cg::this_cluster();
   const int c = CL > 1 ? (int)cluster.block_rank() : 0;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x - TID0, lane = threadIdx.x & 31;
   constexpr int kTopkThreads = NT;
   // segment of this CTA (multiple of 8 elements so float4 loads stay aligned)
   const int seg_len = ((n + CL - 1) / CL + 7) & ~7;
@@ -154,7 +164,7 @@ KSCD_DEV void topk_select(const float* vals, const float* vals2, int n, int take
     const int shift = pass == 0 ? 20 : (pass == 1 ? 8 : 0);
     const int nb = pass == 2 ? 256 : 4096;
     for (int i = tid; i < nb; i += kTopkThreads) sh.hist[i] = 0;
-    __syncthreads();
+    tk_sync<NT, TID0>();
     if (cand_mode) {
       const int nc = (int)sh.ncand;
       for (int i = tid; i < nc; i += kTopkThreads) {
@@ -181,7 +191,7 @@ KSCD_DEV void topk_select(const float* vals, const float* vals2, int n, int take
         }
       }
     }
-    if (CL > 1) cluster.sync(); else __syncthreads();
+    if (CL > 1) cluster.sync(); else tk_sync<NT, TID0>();
     // CTA c owns bins [c*per, (c+1)*per): sum them over the cluster
     const int per = nb / CL;
     const int b0 = c * per;
@@ -197,13 +207,13 @@ KSCD_DEV void topk_select(const float* vals, const float* vals2, int n, int take
     }
     // range total -> CTA 0
     uint32_t tot_unused;
-    const uint32_t pre = block_excl_scan<NT>(mine, sh.scan_buf, tot_unused);
+    const uint32_t pre = block_excl_scan<NT, TID0>(mine, sh.scan_buf, tot_unused);
     (void)pre;
     if (tid == 0) {
       uint32_t* dst = CL > 1 ? cluster.map_shared_rank(sh.range_tot, 0) : sh.range_tot;
       dst[c] = tot_unused;
     }
-    if (CL > 1) cluster.sync(); else __syncthreads();
+    if (CL > 1) cluster.sync(); else tk_sync<NT, TID0>();
     uint32_t above_range = 0;
     {
       const uint32_t* rt = CL > 1 ? cluster.map_shared_rank(sh.range_tot, 0) : sh.range_tot;
@@ -232,7 +242,7 @@ KSCD_DEV void topk_select(const float* vals, const float* vals2, int n, int take
           local += s;
         }
         uint32_t tot2;
-        uint32_t above = above_range + block_excl_scan<NT>(local, sh.scan_buf, tot2);
+        uint32_t above = above_range + block_excl_scan<NT, TID0>(local, sh.scan_buf, tot2);
 #pragma unroll
         for (int i = 0; i < kMaxBpt; ++i) {
           const int bin = top - i;
@@ -250,11 +260,11 @@ KSCD_DEV void topk_select(const float* vals, const float* vals2, int n, int take
         }
       }
     }
-    if (CL > 1) cluster.sync(); else __syncthreads();
+    if (CL > 1) cluster.sync(); else tk_sync<NT, TID0>();
     prefix |= sh.sel_bin << shift;
     pmask |= (uint32_t)(nb - 1) << shift;
     remaining -= sh.sel_above;
-    if (CL > 1) cluster.sync(); else __syncthreads();   // hist / sel reuse in the next pass
+    if (CL > 1) cluster.sync(); else tk_sync<NT, TID0>();   // hist / sel reuse in the next pass
     // only when the bin's cluster-wide count says the copy will (very
     // likely) fit: long prefill rows of near-uniform attention put most of a
     // row in one bin, and a wasted copy pass costs more than it saves
@@ -288,14 +298,14 @@ KSCD_DEV void topk_select(const float* vals, const float* vals2, int n, int take
         }
       }
       uint32_t ab_tot;
-      block_excl_scan<NT>(ab, sh.scan_buf, ab_tot);    // (its barriers also publish ncand)
+      block_excl_scan<NT, TID0>(ab, sh.scan_buf, ab_tot);    // (its barriers also publish ncand)
       above_bin = ab_tot;
       const uint32_t my_ovf = sh.ncand > (uint32_t)kRadixCandCap;
       if (tid < CL) {
         uint32_t* dst = CL > 1 ? cluster.map_shared_rank(sh.ovf, tid) : sh.ovf;
         dst[c] = my_ovf;
       }
-      if (CL > 1) cluster.sync(); else __syncthreads();
+      if (CL > 1) cluster.sync(); else tk_sync<NT, TID0>();
       uint32_t any = 0;
 #pragma unroll
       for (int q = 0; q < CL; ++q) any |= sh.ovf[q];
@@ -333,14 +343,14 @@ KSCD_DEV void topk_select(const float* vals, const float* vals2, int n, int take
     }
   }
   uint32_t tg, te;
-  block_excl_scan<NT>(gt_seg, sh.scan_buf, tg);
-  block_excl_scan<NT>(eq_seg, sh.scan_buf, te);
+  block_excl_scan<NT, TID0>(gt_seg, sh.scan_buf, tg);
+  block_excl_scan<NT, TID0>(eq_seg, sh.scan_buf, te);
   if (tid == 0) {
     uint32_t* dst = CL > 1 ? &cluster.map_shared_rank(&sh, 0)->seg_cnt[c][0] : &sh.seg_cnt[c][0];
     dst[0] = tg;
     dst[1] = te;
   }
-  if (CL > 1) cluster.sync(); else __syncthreads();
+  if (CL > 1) cluster.sync(); else tk_sync<NT, TID0>();
   uint32_t gt_carry = 0, eq_carry = 0;
   {
     const TopkShared* s0 = CL > 1 ? cluster.map_shared_rank(&sh, 0) : &sh;
@@ -368,7 +378,7 @@ KSCD_DEV void topk_select(const float* vals, const float* vals2, int n, int take
       eq += (ok && keys[i] == T);
     }
     uint32_t tot;
-    const uint32_t pre = block_excl_scan<NT>((eq << 16) | gt, sh.scan_buf, tot);
+    const uint32_t pre = block_excl_scan<NT, TID0>((eq << 16) | gt, sh.scan_buf, tot);
     uint32_t g_before = gt_carry + (pre & 0xffffu);
     uint32_t e_before = eq_carry + (pre >> 16);
 #pragma unroll

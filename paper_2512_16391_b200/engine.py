@@ -93,8 +93,10 @@ class KascadeDecoder:
             for i in range(l, e):
                 self.run_end[i] = e
             l = e
-        self.map_table = torch.stack([self.head_maps[l] if self.kinds[l] == KIND_REUSE else
-                                      torch.zeros(num_kv_heads, dtype=torch.int32, device=dev)
+        # (a sharded executor's local decoder holds GLOBAL maps and runs its own loop)
+        zeros = torch.zeros(num_kv_heads, dtype=torch.int32, device=dev)
+        self.map_table = torch.stack([self.head_maps[l] if self.kinds[l] == KIND_REUSE and
+                                      self.head_maps[l].numel() == num_kv_heads else zeros
                                       for l in range(num_layers)]).contiguous()
         self.ws_layers = ops.new_decode_layers_workspace(dev, batch, num_q_heads, num_kv_heads, num_layers)
         self._tables = {}
