@@ -74,6 +74,17 @@ KSCD_DEV float2 pool_colsum(const uint32_t (&r)[128], uint32_t l4, float2 sc2, i
   return acc2;
 }
 
+// Top-k of the pooled row this CTA just wrote into its SM's scratch slot
+// (two planes), by threads 128..383.
+__device__ __noinline__ void fused_select_tail(const PoolPrefillArgs& a, uint8_t* sh_mem, int t1, int64_t r) {
+  if (threadIdx.x == 128 && smid_u32() >= (uint32_t)kSmSlots) __trap();   // scratch slot bound
+  TopkShared& tsh = *reinterpret_cast<TopkShared*>(sh_mem);
+  const float* row0 = a.pooled + (int64_t)smid_u32() * 2 * a.pool_stride;
+  const int k = k_budget_dev(a.fraction, a.k_min, t1);
+  topk_select<1, 256, 128>(row0, row0 + a.pool_stride, t1, min(k, t1), a.idx + r * a.k_cap, a.k_cap,
+                           a.counts + r, tsh);
+}
+
 // bars: 0 q_full | 1-2 k_full[s] | 3-4 k_empty[s] | 5-6 s_full[x] | 7-8 buf_free[x]
 __global__ void __launch_bounds__(pp::kThreads, 1)
     pool_prefill_kernel(const __grid_constant__ PoolTmaps tm, const PoolPrefillArgs a) {
@@ -214,15 +225,10 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
     // row; the producer / MMA warps keep their reduced register budget and
     // wait at the final barrier.  The row's global writes are visible to the
     // group after the barrier, and Q shared memory is free (every MMA retired
-    // before the last column sums were read).
+    // before the last column sums were read).  Out of line, so the select's
+    // registers never compete with the column-sum loop's.
     asm volatile("bar.sync 1, 256;\n" ::: "memory");
-    if (threadIdx.x == 128 && smid_u32() >= (uint32_t)kSmSlots) __trap();   // scratch slot bound
-    TopkShared& tsh = *reinterpret_cast<TopkShared*>(smem + kOffQ);
-    const float* row0 = a.pooled + (int64_t)smid_u32() * 2 * a.pool_stride;
-    const int k = k_budget_dev(a.fraction, a.k_min, t1);
-    const int64_t r = (int64_t)g * T + ti;
-    topk_select<1, 256, 128>(row0, row0 + a.pool_stride, t1, min(k, t1), a.idx + r * a.k_cap, a.k_cap,
-                             a.counts + r, tsh);
+    fused_select_tail(a, smem + kOffQ, t1, (int64_t)g * T + ti);
   }
   __syncthreads();
   if (warp == 0) {
