@@ -92,9 +92,9 @@ typedef struct kscd_decode_params {
  * lists, q/out of layer 0); layer l reads q + l*q_stride_layer and caches
  * k_caches[l] / v_caches[l] (same shape and strides as layer 0), routes
  * through head_maps[l*Hkv ...] and writes out + l*out_stride_layer.  The
- * workspace holds kscd_decode_layers_workspace_size bytes.  No scores or lse
- * outputs.  A launch of L layers has L x the CTAs of one, so small layers
- * (few (sequence, kv head) rows, short lists) stop paying a grid ramp each. */
+ * workspace holds kscd_decode_layers_workspace_size bytes.  A launch of L
+ * layers has L x the CTAs of one, so small layers (few (sequence, kv head)
+ * rows, short lists) stop paying a grid ramp each. */
 typedef struct kscd_decode_layers {
   int32_t num_layers;
   const void* const* k_caches;  /* device array of L pointers, bf16 [B][Hkv][n_cap][128] */
@@ -102,6 +102,12 @@ typedef struct kscd_decode_layers {
   int64_t q_stride_layer;       /* elements between consecutive layers' q */
   int64_t out_stride_layer;     /* elements between consecutive layers' out */
   const int32_t* head_maps;     /* device int32 [L][Hkv], or NULL = identity */
+  /* per-layer lists (p->indices / counts of layer 0, e.g. a group of
+   * consecutive anchors each attending its own fresh sets) and per-layer score
+   * / lse outputs (the anchors' pass 1); element strides, may be negative;
+   * 0 = one list shared by every layer (reuse runs) */
+  int64_t index_stride_layer, count_stride_layer;
+  int64_t scores_stride_layer, lse_stride_layer;
 } kscd_decode_layers;
 
 /* Selection of one decode step: pooled post-softmax weights of the G heads
@@ -268,6 +274,9 @@ int kscd_decode_layers_workspace_size(const kscd_decode_params* p, int32_t num_l
  * kscd_dense_decode without scores or lse), several per launch. */
 int kscd_sparse_decode_layers(const kscd_decode_params* p, const kscd_decode_layers* layers, void* stream);
 int kscd_dense_decode_layers(const kscd_decode_params* p, const kscd_decode_layers* layers, void* stream);
+/* Anchor pass 1 (as kscd_anchor_scores_decode: scores + lse, no V) of
+ * several anchor layers in one launch. */
+int kscd_anchor_scores_decode_layers(const kscd_decode_params* p, const kscd_decode_layers* layers, void* stream);
 
 /* Dense attention of the step's query over keys 0..n-1: out, lse, and --
  * when p->scores != NULL -- the scores the anchor-0 selection pools.

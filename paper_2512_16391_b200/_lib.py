@@ -121,6 +121,8 @@ class DecodeLayers(ctypes.Structure):
     _fields_ = [
         ("num_layers", c_i32), ("k_caches", c_vp), ("v_caches", c_vp),
         ("q_stride_layer", c_i64), ("out_stride_layer", c_i64), ("head_maps", c_vp),
+        ("index_stride_layer", c_i64), ("count_stride_layer", c_i64),
+        ("scores_stride_layer", c_i64), ("lse_stride_layer", c_i64),
     ]
 
 
@@ -185,7 +187,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         lib.kscd_k_budget.argtypes = [c_f64, c_i32, c_i32]
         lib.kscd_decode_workspace_size.restype = ctypes.c_int
         lib.kscd_decode_workspace_size.argtypes = [ctypes.POINTER(DecodeParams), ctypes.POINTER(c_sz)]
-        for name in ("kscd_sparse_decode_layers", "kscd_dense_decode_layers"):
+        for name in ("kscd_sparse_decode_layers", "kscd_dense_decode_layers", "kscd_anchor_scores_decode_layers"):
             fn = getattr(lib, name)
             fn.argtypes = [ctypes.POINTER(DecodeParams), ctypes.POINTER(DecodeLayers), c_vp]
             fn.restype = ctypes.c_int

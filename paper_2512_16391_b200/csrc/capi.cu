@@ -216,23 +216,29 @@ static int decode_layers(int mode, const kscd_decode_params* p, const kscd_decod
                          const char* what) {
   if (!t) return fail(KSCD_INVALID_ARGUMENT, "layers is NULL");
   if (t->num_layers < 1) return fail(KSCD_INVALID_ARGUMENT, "num_layers must be >= 1");
-  if (!t->k_caches || !t->v_caches) return fail(KSCD_INVALID_ARGUMENT, "k_caches/v_caches must be non-NULL");
-  if (p && (p->scores || p->lse)) return fail(KSCD_INVALID_ARGUMENT, "multi-layer launches take no scores/lse outputs");
+  if (!t->k_caches || (mode != kscd::MODE_SCORES && !t->v_caches))
+    return fail(KSCD_INVALID_ARGUMENT, "k_caches/v_caches must be non-NULL");
+  if (p && mode == kscd::MODE_SCORES && (!p->scores || !p->lse))
+    return fail(KSCD_INVALID_ARGUMENT, "scores and lse must be non-NULL");
+  if (p && mode != kscd::MODE_SCORES && p->scores)
+    return fail(KSCD_INVALID_ARGUMENT, "only the score pass writes scores");
   if (p && (t->q_stride_layer < (int64_t)p->batch * p->num_q_heads * 128 ||
             t->out_stride_layer < (int64_t)p->batch * p->num_q_heads * 128))
     return fail(KSCD_INVALID_ARGUMENT, "layer strides of q/out overlap");
-  int rc = check_decode(p, true, mode == kscd::MODE_SPARSE);
+  int rc = check_decode(p, mode != kscd::MODE_SCORES, mode == kscd::MODE_SPARSE);
   if (rc) return rc;
   const size_t per = decode_layer_ws_bytes(p);
   if (p->workspace_bytes < per * (size_t)t->num_layers)
     return fail(KSCD_INVALID_ARGUMENT, "workspace too small for %d layers (%zu < %zu bytes)", t->num_layers,
                 p->workspace_bytes, per * (size_t)t->num_layers);
   kscd::DecodeArgs a = make_args(p, mode == kscd::MODE_SPARSE ? p->k_cap : p->seq_len);
-  a.scores = nullptr;
-  a.lse = nullptr;
   a.nl = t->num_layers;
   a.k_tab = (const __nv_bfloat16* const*)t->k_caches;
-  a.v_tab = (const __nv_bfloat16* const*)t->v_caches;
+  a.v_tab = (const __nv_bfloat16* const*)(t->v_caches ? t->v_caches : t->k_caches);
+  a.idx_ls = t->index_stride_layer;
+  a.cnt_ls = t->count_stride_layer;
+  a.scores_ls = t->scores_stride_layer;
+  a.lse_ls = t->lse_stride_layer;
   a.q_ls = t->q_stride_layer;
   a.out_ls = t->out_stride_layer;
   a.head_map = t->head_maps;
@@ -247,6 +253,10 @@ int kscd_sparse_decode_layers(const kscd_decode_params* p, const kscd_decode_lay
 
 int kscd_dense_decode_layers(const kscd_decode_params* p, const kscd_decode_layers* t, void* stream) {
   return decode_layers(kscd::MODE_DENSE, p, t, stream, "kscd_dense_decode_layers");
+}
+
+int kscd_anchor_scores_decode_layers(const kscd_decode_params* p, const kscd_decode_layers* t, void* stream) {
+  return decode_layers(kscd::MODE_SCORES, p, t, stream, "kscd_anchor_scores_decode_layers");
 }
 
 int kscd_select_decode(const kscd_select_decode_params* p, void* stream) {

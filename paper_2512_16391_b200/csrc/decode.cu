@@ -66,6 +66,8 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
   float* part_l = reinterpret_cast<float*>(reinterpret_cast<char*>(a.part) + (int64_t)lyr * a.ws_ls);
   float* part_ml_l = reinterpret_cast<float*>(reinterpret_cast<char*>(a.part_ml) + (int64_t)lyr * a.ws_ls);
   int* counters_l = reinterpret_cast<int*>(reinterpret_cast<char*>(a.counters) + (int64_t)lyr * a.ws_ls);
+  float* scores_l = a.scores ? a.scores + (int64_t)lyr * a.scores_ls : nullptr;
+  float* lse_l = a.lse ? a.lse + (int64_t)lyr * a.lse_ls : nullptr;
 
   const __nv_bfloat16* kbase = k_l + (int64_t)b * a.kv_sb + (int64_t)gk * a.kv_sh;
   const __nv_bfloat16* vbase = v_l + (int64_t)b * a.kv_sb + (int64_t)gk * a.kv_sh;
@@ -82,8 +84,8 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
   int count = a.lens ? min(__ldg(a.lens + b), a.n) : a.n;
   if (MODE == MODE_SPARSE) {
     const int src = hm_l ? __ldg(hm_l + gk) : gk;
-    sel = a.idx + (int64_t)b * a.idx_sb + (int64_t)src * a.idx_sh;
-    count = min(__ldg(a.cnt + (int64_t)b * a.cnt_sb + src), a.k_cap);
+    sel = a.idx + (int64_t)lyr * a.idx_ls + (int64_t)b * a.idx_sb + (int64_t)src * a.idx_sh;
+    count = min(__ldg(a.cnt + (int64_t)lyr * a.cnt_ls + (int64_t)b * a.cnt_sb + src), a.k_cap);
   }
   const int ntiles = (count + kTileKeys - 1) / kTileKeys;
   const int tps = (ntiles + a.splits - 1) / a.splits;
@@ -206,15 +208,15 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
         const int kk = key_w + nt * 8 + 2 * tig + (c & 1);
         s[nt][c] = kk < count ? s[nt][c] * a.scale_log2 : -INFINITY;
       }
-      if (MODE != MODE_SPARSE && a.scores != nullptr) {
+      if (MODE != MODE_SPARSE && scores_l != nullptr) {
         const int kk = key_w + nt * 8 + 2 * tig;
         if (gid < G && kk < count) {
-          float* dst = a.scores + ((int64_t)b * a.Hq + g * G + gid) * a.score_stride + kk;
+          float* dst = scores_l + ((int64_t)b * a.Hq + g * G + gid) * a.score_stride + kk;
           if (kk + 1 < count) *reinterpret_cast<float2*>(dst) = make_float2(s[nt][0], s[nt][1]);
           else dst[0] = s[nt][0];
         }
         if (G16 && gid + 8 < G && kk < count) {
-          float* dst = a.scores + ((int64_t)b * a.Hq + g * G + gid + 8) * a.score_stride + kk;
+          float* dst = scores_l + ((int64_t)b * a.Hq + g * G + gid + 8) * a.score_stride + kk;
           if (kk + 1 < count) *reinterpret_cast<float2*>(dst) = make_float2(s[nt][2], s[nt][3]);
           else dst[0] = s[nt][2];
         }
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
       if (Cfg::kHasV)
         *reinterpret_cast<float4*>(out_l + (bh0 + h) * kHeadDim + lane * 4) =
             make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-      if (lane == 0 && a.lse) a.lse[bh0 + h] = (M + __log2f(L)) * kLn2;
+      if (lane == 0 && lse_l) lse_l[bh0 + h] = (M + __log2f(L)) * kLn2;
     } else {
       const int64_t pi = (bh0 + h) * a.splits + split;
       if (Cfg::kHasV) *reinterpret_cast<float4*>(part_l + pi * kHeadDim + lane * 4) = acc;
@@ -388,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
       *reinterpret_cast<float4*>(out_l + (bh0 + h) * kHeadDim + lane * 4) =
           make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
     }
-    if (lane == 0 && a.lse) a.lse[bh0 + h] = (M + __log2f(L)) * kLn2;
+    if (lane == 0 && lse_l) lse_l[bh0 + h] = (M + __log2f(L)) * kLn2;
     __syncwarp();
   }
 }

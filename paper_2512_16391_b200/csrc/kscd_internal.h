@@ -44,6 +44,9 @@ struct DecodeArgs {
   const __nv_bfloat16* const* k_tab;
   const __nv_bfloat16* const* v_tab;
   int64_t q_ls, out_ls, hm_ls, ws_ls;
+  // per-layer index lists / counts / scores / lse (element strides, may be
+  // negative; 0 = shared by every layer of the launch)
+  int64_t idx_ls, cnt_ls, scores_ls, lse_ls;
 };
 
 cudaError_t launch_decode_attn(int mode, const DecodeArgs& a, cudaStream_t st);

@@ -64,17 +64,39 @@ class KascadeDecoder:
         self.shared_map = torch.zeros(num_kv_heads, dtype=torch.int32, device=dev) if self.all_heads else None
         k_cap = k_budget(plan.k_policy, max_seq_len)
         n_pad = (max_seq_len + 3) // 4 * 4
+        # groups of consecutive anchor layers (other than layer 0): they are
+        # independent of each other, so a group runs its score passes, its
+        # selections and its sparse passes as one launch each; every group
+        # member has its own slot of scores / pooled / lists, the LAST anchor
+        # in slot 0 (= self.indices, what the following reuse layers read)
+        self.group_end: Dict[int, int] = {}
+        l = 1
+        while l < num_layers:
+            e = l
+            while e < num_layers and self.kinds[e] == KIND_ANCHOR:
+                e += 1
+            for i in range(l, e):
+                self.group_end[i] = e
+            l = max(e, l + 1)
+        gmax = 1 if self.pre else max([e - l for l, e in self.group_end.items()] + [1])
         if self.pre:   # q_bar scores -> softmax -> Top-k: no score pass, no per-head score scratch
-            self.scores = None
+            self.scores_g = None
             self.pooled, self.pre_ws, _, _ = ops.select_pre_buffers(batch, num_kv_heads, max_seq_len, plan.k_policy,
                                                                     dev, prefill=False, all_heads=self.all_heads,
                                                                     num_q_heads=num_q_heads)
+            self.scores = None
         else:
-            self.scores = torch.empty(batch, num_q_heads, n_pad, dtype=torch.float32, device=dev)
-            self.pooled = torch.empty(batch * Hsrc, n_pad, dtype=torch.float32, device=dev)
-        self.lse = torch.empty(batch, num_q_heads, dtype=torch.float32, device=dev)
-        self.indices = torch.empty(batch, Hsrc, k_cap, dtype=torch.int32, device=dev)
-        self.counts = torch.zeros(batch, Hsrc, dtype=torch.int32, device=dev)
+            self.scores_g = torch.empty(gmax * batch, num_q_heads, n_pad, dtype=torch.float32, device=dev)
+            self.pooled_g = torch.empty(gmax * batch * Hsrc, n_pad, dtype=torch.float32, device=dev)
+            self.scores = self.scores_g[:batch]
+            self.pooled = self.pooled_g[:batch * Hsrc]
+        self.lse_g = torch.empty(gmax * batch, num_q_heads, dtype=torch.float32, device=dev)
+        self.idx_g = torch.empty(gmax, batch, Hsrc, k_cap, dtype=torch.int32, device=dev)
+        self.cnt_g = torch.zeros(gmax, batch, Hsrc, dtype=torch.int32, device=dev)
+        self.lse = self.lse_g[:batch]
+        self.indices = self.idx_g[0]
+        self.counts = self.cnt_g[0]
+        self.zero_maps = torch.zeros(gmax, num_kv_heads, dtype=torch.int32, device=dev)
         self.out = torch.empty(num_layers, batch, num_q_heads, 128, dtype=torch.float32, device=dev)
         # the executor's own split-K workspace: its layers run stream-ordered,
         # so they share it; no other executor, stream or graph touches it
@@ -136,6 +158,12 @@ class KascadeDecoder:
         layer in dense mode) is one multi-layer launch; anchors run alone."""
         l = l0
         while l < l1:
+            if not dense and self.kinds[l] == KIND_ANCHOR and not self.pre and self.seq_lens is None:
+                e = min(self.group_end[l], l1)
+                if e - l >= 2:
+                    self._anchor_group(l, e, q, k_caches, v_caches, seq_len)
+                    l = e
+                    continue
             end = l1 if dense else (min(self.run_end[l], l1) if self.kinds[l] == KIND_REUSE else l + 1)
             # one launch needs one cache layout; dense layers of a ragged batch
             # run per layer (the multi-layer launch has no per-sequence lengths)
@@ -151,6 +179,27 @@ class KascadeDecoder:
                 for i in range(l, end):
                     (self._dense_layer if dense else self._layer)(i, q, k_caches, v_caches, seq_len)
             l = end
+
+    def _anchor_group(self, l0: int, l1: int, q, k_caches, v_caches, seq_len: int) -> None:
+        """Consecutive anchor layers [l0, l1) as three launches: their score
+        passes, one select over all their (sequence, kv head) rows, and their
+        sparse passes over their own fresh sets (runner.py:263-266).  Layer
+        l0 + i uses slot m - 1 - i, so the last anchor's lists land in slot 0."""
+        m = l1 - l0
+        B, Hq = self.B, self.Hq
+        Hs = self.indices.shape[1]
+        tabs = self._layer_tables(k_caches, v_caches, l0, l1)
+        sc_ls = self.scores_g.stride(0) * B
+        ops.decode_layers(q[l0:l1], k_caches[l0:l1], v_caches[l0:l1], seq_len, workspace=self.ws_layers, tables=tabs,
+                          scores=self.scores_g[(m - 1) * B:m * B], scores_layer_stride=-sc_ls,
+                          lse=self.lse_g[(m - 1) * B:m * B], lse_layer_stride=-B * Hq)
+        ops.select_decode(self.scores_g[:m * B], self.lse_g[:m * B], seq_len, self.plan.k_policy, self.Hkv,
+                          indices=self.idx_g[:m].view(m * B, Hs, -1), counts=self.cnt_g[:m].view(m * B, Hs),
+                          pooled=self.pooled_g[:m * B * Hs], all_heads=self.all_heads)
+        ops.decode_layers(q[l0:l1], k_caches[l0:l1], v_caches[l0:l1], seq_len, out=self.out[l0:l1],
+                          workspace=self.ws_layers, tables=tabs, indices=self.idx_g[m - 1], counts=self.cnt_g[m - 1],
+                          index_layer_stride=-self.idx_g.stride(0), count_layer_stride=-self.cnt_g.stride(0),
+                          head_maps=self.zero_maps[:m] if self.all_heads else None)
 
     def _layer(self, l: int, q, k_caches, v_caches, seq_len: int) -> None:
         """The kernels of layer l (runner.py:250-275 for one decode token)."""

@@ -305,22 +305,35 @@ def anchor_decode(q, k_cache, v_cache, seq_len, policy: KBudgetPolicy, *, layer0
     return out, lse, indices, counts
 
 
-def decode_layers(q, k_caches, v_caches, seq_len, *, out, workspace, tables, indices=None, counts=None,
-                  head_maps=None, scale=None, num_splits=0):
-    """Several independent decode layers in ONE launch: sparse (reuse) layers
-    when ``indices`` is given -- layer l attends indices[b][head_maps[l][g]]
-    (runner.py:210-225) -- else dense layers.  q / out: [nl][B][Hq][128]
-    (layer-strided views, e.g. slices of the executor's buffers); k_caches /
-    v_caches: nl caches of one shape and stride layout; ``tables``: their
-    device pointer arrays (cache_pointer_tables); head_maps: device int32
+def decode_layers(q, k_caches, v_caches, seq_len, *, workspace, tables, out=None, indices=None, counts=None,
+                  head_maps=None, index_layer_stride: int = 0, count_layer_stride: int = 0, scores=None,
+                  lse=None, scores_layer_stride: int = 0, lse_layer_stride: int = 0, scale=None, num_splits=0):
+    """Several independent decode layers in ONE launch:
+
+    * sparse layers when ``indices`` is given -- layer l attends
+      indices[b][head_maps[l][g]] (runner.py:210-225), the lists shared by
+      every layer (a reuse run) or, with ``index_layer_stride`` /
+      ``count_layer_stride`` (elements, may be negative), its own (a group of
+      anchors over their fresh sets);
+    * the anchor score pass (scores + lse, no V) when ``scores`` is given,
+      each layer into scores + l * scores_layer_stride / lse + l * lse_layer_stride;
+    * dense layers otherwise.
+
+    q / out: [nl][B][Hq][128] layer-strided views; k_caches / v_caches: nl
+    caches of one shape and stride layout with their device pointer arrays in
+    ``tables`` (cache_pointer_tables-style); head_maps: device int32
     [nl][Hkv] or None (identity)."""
     nl = len(k_caches)
-    if q.dim() != 4 or out.dim() != 4 or q.shape[0] != nl or out.shape[0] != nl or q.shape[1:] != out.shape[1:] \
-            or not q[0].is_contiguous() or not out[0].is_contiguous():
-        raise InvalidArgumentError("q / out must be [nl][B][Hq][128] with contiguous layers")
-    sparse = indices is not None
-    p = _decode_params(q[0], k_caches[0], v_caches[0], seq_len, out[0], None, None, scale, num_splits,
-                       workspace=workspace)
+    if q.dim() != 4 or q.shape[0] != nl or not q[0].is_contiguous():
+        raise InvalidArgumentError("q must be [nl][B][Hq][128] with contiguous layers")
+    if out is not None and (out.dim() != 4 or out.shape != q.shape or not out[0].is_contiguous()):
+        raise InvalidArgumentError("out must be [nl][B][Hq][128] with contiguous layers")
+    sparse, score_pass = indices is not None, scores is not None
+    if score_pass:
+        B, Hq = q.shape[1], q.shape[2]
+        _check_scores(scores, B, Hq, seq_len)
+    p = _decode_params(q[0], k_caches[0], None if score_pass else v_caches[0], seq_len,
+                       None if out is None else out[0], lse, scores, scale, num_splits, workspace=workspace)
     if sparse:
         if indices.dtype != torch.int32 or counts.dtype != torch.int32 or indices.dim() != 3 \
                 or not indices.is_contiguous() or not counts.is_contiguous() or counts.shape != indices.shape[:2]:
@@ -332,8 +345,13 @@ def decode_layers(q, k_caches, v_caches, seq_len, *, out, workspace, tables, ind
         raise InvalidArgumentError("head_maps must be a contiguous CUDA int32 [nl][Hkv] tensor")
     kp, vp = tables[0], tables[1]
     t = _lib.DecodeLayers(num_layers=nl, k_caches=kp.data_ptr(), v_caches=vp.data_ptr(),
-                          q_stride_layer=q.stride(0), out_stride_layer=out.stride(0), head_maps=_ptr(head_maps))
-    _lib.call("kscd_sparse_decode_layers" if sparse else "kscd_dense_decode_layers", p, _stream(), t)
+                          q_stride_layer=q.stride(0), out_stride_layer=out.stride(0) if out is not None else q.stride(0),
+                          head_maps=_ptr(head_maps), index_stride_layer=int(index_layer_stride),
+                          count_stride_layer=int(count_layer_stride), scores_stride_layer=int(scores_layer_stride),
+                          lse_stride_layer=int(lse_layer_stride))
+    name = ("kscd_anchor_scores_decode_layers" if score_pass else
+            "kscd_sparse_decode_layers" if sparse else "kscd_dense_decode_layers")
+    _lib.call(name, p, _stream(), t)
     return out
 
 

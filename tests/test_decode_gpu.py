@@ -299,25 +299,29 @@ def test_host_step_graph_appends_and_matches_step(cuda_ok, splits):
 
 
 def test_multi_layer_launches_equal_per_layer(cuda_ok):
-    """Consecutive reuse layers run as ONE multi-layer launch in step() and
-    every dense layer as one launch in dense_step(); each layer's result is
-    bit-identical to launching it alone (same split plan, own workspace)."""
+    """Consecutive reuse layers run as ONE multi-layer launch in step(), a
+    group of consecutive anchors as one score launch + one select + one
+    sparse launch over per-layer lists, and every dense layer as one launch
+    in dense_step(); each layer's result (and the lists the reuse layers
+    read) is bit-identical to launching it alone."""
     from paper_2512_16391_b200 import engine
     from paper_2512_16391_b200.host_types import AnchorPlan, AnchorPlanCore, HeadMap, KBudgetPolicy
-    L, B, Hq, Hkv, n = 7, 3, 16, 4, 5000
-    maps = {1: HeadMap(1, 0, [3, 2, 1, 0]), 3: HeadMap(3, 2, [1, 0, 3, 2]), 4: HeadMap(4, 2, [0, 0, 1, 1]),
-            5: HeadMap(5, 2, [2, 3, 0, 1]), 6: HeadMap(6, 2, [3, 3, 3, 0])}
-    plan = AnchorPlan(AnchorPlanCore([0, 2], 2, 0.0), head_maps=maps, k_policy=KBudgetPolicy(0.1, 64))
+    L, B, Hq, Hkv, n = 8, 3, 16, 4, 5000
+    maps = {1: HeadMap(1, 0, [3, 2, 1, 0]), 5: HeadMap(5, 4, [1, 0, 3, 2]), 6: HeadMap(6, 4, [0, 0, 1, 1]),
+            7: HeadMap(7, 4, [2, 3, 0, 1])}
+    plan = AnchorPlan(AnchorPlanCore([0, 2, 3, 4], 4, 0.0), head_maps=maps, k_policy=KBudgetPolicy(0.1, 64))
     g = torch.Generator(device="cuda").manual_seed(3)
     Ks = [torch.randn(B, Hkv, n, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(L)]
     Vs = [torch.randn(B, Hkv, n, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(L)]
     q = (torch.randn(L, B, Hq, 128, device="cuda", generator=g) * 2).to(torch.bfloat16)
     dec = engine.KascadeDecoder(plan, L, B, Hq, Hkv, n)
-    assert dec.run_end[3] == 7 and dec.run_end[1] == 2
+    assert dec.run_end[5] == 8 and dec.run_end[1] == 2 and dec.group_end[2] == 5
     fused = dec.step(q, Ks, Vs, n).clone()
+    lists = (dec.indices.clone(), dec.counts.clone())
     for l in range(L):
         dec._layer(l, q, Ks, Vs, n)
     assert torch.equal(dec.out, fused)
+    assert torch.equal(dec.indices, lists[0]) and torch.equal(dec.counts, lists[1])
     dfused = dec.dense_step(q, Ks, Vs, n).clone()
     for l in range(L):
         dec._dense_layer(l, q, Ks, Vs, n)
