@@ -458,6 +458,9 @@ namespace {
 // One pass-B launch covers every head of a kv group (G <= 4) in post mode:
 // the Top-k then runs in the tail of each pass-B CTA on its SM's scratch slot.
 bool select_prefill_fused(const kscd_select_prefill_params* p) {
+#ifdef KSCD_NO_FUSED_SELECT      // experiment builds only (A/B of the fused selection)
+  return false;
+#endif
   return !p->all_heads && p->num_q_heads / p->num_kv_heads <= 4;
 }
 size_t select_prefill_scratch_bytes(const kscd_select_prefill_params* p) {

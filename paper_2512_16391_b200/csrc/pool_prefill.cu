@@ -26,6 +26,10 @@
 #include "kscd_internal.h"
 #include "topk_select.cuh"
 
+#ifndef KSCD_FUSED_NB
+#define KSCD_FUSED_NB 2
+#endif
+
 namespace kscd {
 using namespace sm100;
 
@@ -81,8 +85,10 @@ __device__ __noinline__ void fused_select_tail(const PoolPrefillArgs& a, uint8_t
   TopkShared& tsh = *reinterpret_cast<TopkShared*>(sh_mem);
   const float* row0 = a.pooled + (int64_t)smid_u32() * 2 * a.pool_stride;
   const int k = k_budget_dev(a.fraction, a.k_min, t1);
-  topk_select<1, 256, 128>(row0, row0 + a.pool_stride, t1, min(k, t1), a.idx + r * a.k_cap, a.k_cap,
-                           a.counts + r, tsh);
+  // 2 float4 loads in flight per thread (x2 planes); 4 and 8 spill and run slower (A/B at 128K: 82.4 / 84.0 / 89.8 ms per select, unfused 81.2)
+  // (x2 planes) keep the row passes from going L2-latency bound
+  topk_select<1, 256, 128, KSCD_FUSED_NB>(row0, row0 + a.pool_stride, t1, min(k, t1), a.idx + r * a.k_cap, a.k_cap,
+                              a.counts + r, tsh);
 }
 
 // bars: 0 q_full | 1-2 k_full[s] | 3-4 k_empty[s] | 5-6 s_full[x] | 7-8 buf_free[x]

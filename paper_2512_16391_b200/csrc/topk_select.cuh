@@ -18,7 +18,7 @@ constexpr int kTopkThreads = 512;
 // B200 (scripts/perf_topk.py, same box): 1 -> 2 cuts the decode select
 // 65.5 -> 62.2 us (64 rows x 128K) and the 128K prefill select 2658 -> 2426
 // us; 4 is equal on decode and slower on prefill; 8 drops occupancy.
-constexpr int kTopkBatch = KSCD_TOPK_BATCH;
+constexpr int kTopkBatchDefault = KSCD_TOPK_BATCH;
 #ifndef KSCD_TOPK_ITEMS
 #define KSCD_TOPK_ITEMS 8
 #endif
@@ -125,7 +125,7 @@ struct TopkShared {
 // counts_out (written by CTA 0 of the cluster) = take.  NT threads of the CTA
 // take part; CL CTAs of a cluster split the row.  Used by topk_kernel and by
 // the fused anchor-selection tail of pool_prefill_kernel (NT = 384, CL = 1).
-template <int CL, int NT, int TID0 = 0>
+template <int CL, int NT, int TID0 = 0, int kTopkBatch = kTopkBatchDefault>
 KSCD_DEV void topk_select(const float* vals, const float* vals2, int n, int take, int* out, int k_cap,
                           int* counts_out, TopkShared& sh) {
   static_assert(CL == 1 || TID0 == 0, "a cluster-split row runs on whole CTAs");
