@@ -180,6 +180,23 @@ class KascadeDecoder:
                     (self._dense_layer if dense else self._layer)(i, q, k_caches, v_caches, seq_len)
             l = end
 
+    def launches_per_step(self, dense: bool = False) -> int:
+        """Kernel launches of one step() (post-softmax pooling, uniform batch):
+        anchor 0 = dense + pool + Top-k; an anchor or a group of consecutive
+        anchors = scores + pool + Top-k + sparse; a reuse run = one launch."""
+        if dense:
+            return 1
+        n, l = 0, 0
+        while l < self.L:
+            kind = self.kinds[l]
+            if kind == KIND_ANCHOR0:
+                n, l = n + 3, l + 1
+            elif kind == KIND_ANCHOR:
+                n, l = n + 4, self.group_end[l]
+            else:
+                n, l = n + 1, self.run_end[l]
+        return n
+
     def _anchor_group(self, l0: int, l1: int, q, k_caches, v_caches, seq_len: int) -> None:
         """Consecutive anchor layers [l0, l1) as three launches: their score
         passes, one select over all their (sequence, kv head) rows, and their

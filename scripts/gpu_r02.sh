@@ -55,3 +55,20 @@ for s in "$@"; do
       echo "configs rc=$?"; tail -c 1500 $O/configs_$TAG.json ;;
   esac
 done
+for s in "$@"; do
+  case $s in
+    fullcap)
+      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+        -k 'regex:decode_attn_kernel<\(int\)1' -s 6 -c 1 -o $O/step_reuse_run_$TAG -f python scripts/prof_step.py \
+        > $O/fullcap_step_$TAG.out 2>&1
+      echo "step reuse-run capture rc=$?"
+      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+        -k 'regex:pool_prefill' -s 1 -c 1 -o $O/pool_prefill_fused_$TAG -f python scripts/prof_kernels.py prefill 32768 \
+        > $O/fullcap_pool_$TAG.out 2>&1
+      echo "fused pass-B capture rc=$?"
+      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+        -k 'regex:prefill_attn_kernel<\(int\)1' -s 1 -c 1 -o $O/sparse_prefill_$TAG -f python scripts/prof_kernels.py prefill 131072 \
+        > $O/fullcap_sp_$TAG.out 2>&1
+      echo "sparse prefill capture rc=$?" ;;
+  esac
+done
