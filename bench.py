@@ -891,79 +891,74 @@ def main():
     clk = clocks.stop()
     ms_kas = min(ms_kas, ms_kas2) if args.best_of else ms_kas
 
-    # ---- dominant kernel: reuse-layer sparse decode, per-launch CUDA events
+    # ---- dominant kernel: reuse-layer sparse decode, per-launch CUDA events.
+    # Every timed launch is replayed from its own CUDA graph, so the event
+    # interval holds the kernel and not the host's Python submission of it
+    # (the launches are shorter than an eager ops call's host overhead).
     reuse_layers = [l for l in range(L) if l not in LLAMA_ANCHORS]
     dec.step(q, Ks, Vs, n)  # fresh index lists from the last anchor
-    evs = []
     torch.cuda.synchronize()
-    for rep in range(max(1, args.steps // 2)):
-        for l in reuse_layers:
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            ops.sparse_decode(q[l], Ks[l], Vs[l], n, dec.indices, dec.counts, dec.head_maps[l], out=dec.out[l])
-            e.record()
-            evs.append((s, e))
-    torch.cuda.synchronize()
-    reuse_ms = float(np.mean([s.elapsed_time(e) for s, e in evs]))
-    # the same launches back to back, as inside the step (programmatic
-    # dependent launch overlaps each launch's ramp with the previous tail):
-    # events only around the whole chain
-    chain = []
-    for rep in range(max(1, args.steps // 2)):
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        for l in reuse_layers:
-            ops.sparse_decode(q[l], Ks[l], Vs[l], n, dec.indices, dec.counts, dec.head_maps[l], out=dec.out[l])
-        e.record()
-        chain.append((s, e))
-    torch.cuda.synchronize()
-    chain_ms = float(np.mean([s.elapsed_time(e) for s, e in chain])) / len(reuse_layers)
+
+    def graph_of(fn):
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        return g
+
+    def per_replay_ms(graphs, reps, divide=1):
+        evs = []
+        for _ in range(reps):
+            for g in graphs:
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                g.replay()
+                e.record()
+                evs.append((s, e))
+        torch.cuda.synchronize()
+        return float(np.mean([s.elapsed_time(e) for s, e in evs])) / divide
+
+    reps = max(1, args.steps // 2)
+    iso = [graph_of(lambda l=l: ops.sparse_decode(q[l], Ks[l], Vs[l], n, dec.indices, dec.counts, dec.head_maps[l],
+                                                   out=dec.out[l], workspace=dec.ws)) for l in reuse_layers]
+    reuse_ms = per_replay_ms(iso, reps)
+    # the same single-layer launches back to back, as one graph (PDL overlaps
+    # each launch's ramp with the previous tail): events around the chain only
+    chain_g = graph_of(lambda: [ops.sparse_decode(q[l], Ks[l], Vs[l], n, dec.indices, dec.counts, dec.head_maps[l],
+                                                  out=dec.out[l], workspace=dec.ws) for l in reuse_layers])
+    chain_ms = per_replay_ms([chain_g], reps, divide=len(reuse_layers))
     # the step itself runs every run of consecutive reuse layers as ONE
     # multi-layer launch: the longest run (layers 15-31) timed as it runs
     r0 = max(dec.run_end, key=lambda l: (dec.run_end[l] - l, -l))
     r1 = dec.run_end[r0]
     tabs = dec._layer_tables(Ks, Vs, r0, r1)
-    multi = []
-    for rep in range(max(1, args.steps // 2)):
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        ops.decode_layers(q[r0:r1], Ks[r0:r1], Vs[r0:r1], n, out=dec.out[r0:r1], workspace=dec.ws_layers,
-                          tables=tabs, indices=dec.indices, counts=dec.counts, head_maps=dec.map_table[r0:r1])
-        e.record()
-        multi.append((s, e))
-    torch.cuda.synchronize()
-    multi_ms = float(np.mean([s.elapsed_time(e) for s, e in multi]))
+    multi_g = graph_of(lambda: ops.decode_layers(q[r0:r1], Ks[r0:r1], Vs[r0:r1], n, out=dec.out[r0:r1],
+                                                 workspace=dec.ws_layers, tables=tabs, indices=dec.indices,
+                                                 counts=dec.counts, head_maps=dec.map_table[r0:r1]))
+    multi_ms = per_replay_ms([multi_g], reps)
+    del iso, chain_g, multi_g
     counts = dec.counts.cpu().numpy()
     reuse_bytes = int(counts.sum()) * (2 * 128 * 2 + 4)   # K+V rows + index per selected key
     peaks, peaks_kind = load_peaks()
     hbm = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
     achieved = reuse_bytes / (reuse_ms * 1e-3) / 1e9
+    multi_bytes = reuse_bytes * (r1 - r0)
 
     # dense kernel (baseline) per-launch duration for context
-    evs = []
-    for l in range(min(L, 8)):
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        ops.dense_decode(q[l], Ks[l], Vs[l], n, out=dec.out[l], lse=dec.lse)
-        e.record()
-        evs.append((s, e))
-    torch.cuda.synchronize()
-    dense_ms_launch = float(np.mean([s.elapsed_time(e) for s, e in evs]))
+    dg = [graph_of(lambda l=l: ops.dense_decode(q[l], Ks[l], Vs[l], n, out=dec.out[l], lse=dec.lse, workspace=dec.ws))
+          for l in range(min(L, 8))]
+    dense_ms_launch = per_replay_ms(dg, 1)
+    del dg
     dense_bytes = B * Hkv * n * 512
 
     # ---- per-layer-kind times (Table-3 layout) and the reference cost
     # model's weighted pipeline time from them (SURVEY 8(d) cross-check)
     per_kind = {}
     for kind, l in (("anchor0", 0), ("reuse", reuse_layers[0]), ("anchor", LLAMA_ANCHORS[1])):
-        evs = []
-        for rep in range(3):
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            dec._layer(l, q, Ks, Vs, n)
-            e.record()
-            evs.append((s, e))
-        torch.cuda.synchronize()
-        per_kind[kind] = float(np.median([s.elapsed_time(e) for s, e in evs]))
+        gk = graph_of(lambda l=l: dec._layer(l, q, Ks, Vs, n))
+        per_kind[kind] = per_replay_ms([gk], 3)
+        del gk
     dec.step(q, Ks, Vs, n)   # restore the step's final state
     from paper_2512_16391_b200 import costmodel
     cm = costmodel.weighted_pipeline_time(
@@ -1059,31 +1054,31 @@ def main():
                                  "(costmodel.weighted_pipeline_time) composes them to the 32-layer step"},
         "speedup_vs_dense": round(ms_den / ms_kas, 3),
         "paper_h100_us_per_token": 1415,
-        "roofline": {"kernel": "kscd sparse_decode (reuse layer)", "bound": "hbm",
-                     "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                     "frac": round(achieved / hbm, 4), "traffic": load_traffic(f"sparse_decode_{n // 1024}k_b{B}"),
-                     "frac_of_spec": round(achieved / SPEC_HBM_GBS, 4),
+        "roofline": {"kernel": "kscd sparse_decode_layers (the step's longest reuse run, layers %d-%d, one launch)"
+                               % (r0, r1 - 1), "bound": "hbm",
+                     "achieved": round(multi_bytes / (multi_ms * 1e-3) / 1e9, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(multi_bytes / (multi_ms * 1e-3) / 1e9 / hbm, 4),
+                     "traffic": load_traffic(f"sparse_decode_run_{n // 1024}k_b{B}"),
+                     "frac_of_spec": round(multi_bytes / (multi_ms * 1e-3) / 1e9 / SPEC_HBM_GBS, 4),
                      "spec_note": f"frac_of_spec: against the ~{SPEC_HBM_GBS / 1000:g} TB/s north_star names (DGX B200; "
                                   "7.7 TB/s HGX); frac: against the measured copy peak",
                      "peak_kind": peaks_kind,
-                     "bytes_per_launch": reuse_bytes, "launch_ms": round(reuse_ms, 4),
+                     "bytes_per_launch": multi_bytes, "launch_ms": round(multi_ms, 4),
+                     "units": f"{r1 - r0} layers x {int(counts.sum())} selected keys x 516 B (K+V rows + index)",
                      "dense_decode_frac": round(dense_bytes / (dense_ms_launch * 1e-3) / 1e9 / hbm, 4),
-                     "gather": _decode_gather_ceiling(achieved),
+                     "single_layer": {"launch_ms": round(reuse_ms, 4), "bytes_per_launch": reuse_bytes,
+                                      "achieved": round(achieved, 1), "frac": round(achieved / hbm, 4),
+                                      "frac_of_spec": round(achieved / SPEC_HBM_GBS, 4),
+                                      "traffic": load_traffic(f"sparse_decode_{n // 1024}k_b{B}"),
+                                      "gather": _decode_gather_ceiling(achieved),
+                                      "note": "one reuse layer per launch (kscd_sparse_decode), each replayed "
+                                              "alone from a CUDA graph"},
                      "chained": {"launch_ms": round(chain_ms, 4),
                                  "achieved": round(reuse_bytes / (chain_ms * 1e-3) / 1e9, 1),
                                  "frac": round(reuse_bytes / (chain_ms * 1e-3) / 1e9 / hbm, 4),
                                  "frac_of_spec": round(reuse_bytes / (chain_ms * 1e-3) / 1e9 / SPEC_HBM_GBS, 4),
-                                 "note": "the 27 reuse layers as single-layer launches back to back (PDL overlaps "
-                                         "each launch's ramp with the previous tail), events around the chain only; "
-                                         "achieved/frac above are per isolated launch"},
-                     "multi_layer": {"layers": [r0, r1 - 1], "launch_ms": round(multi_ms, 4),
-                                     "bytes_per_launch": reuse_bytes * (r1 - r0),
-                                     "achieved": round(reuse_bytes * (r1 - r0) / (multi_ms * 1e-3) / 1e9, 1),
-                                     "frac": round(reuse_bytes * (r1 - r0) / (multi_ms * 1e-3) / 1e9 / hbm, 4),
-                                     "frac_of_spec": round(reuse_bytes * (r1 - r0) / (multi_ms * 1e-3) / 1e9 /
-                                                           SPEC_HBM_GBS, 4),
-                                     "note": "the step's longest reuse run as the ONE multi-layer launch the step "
-                                             "issues (kscd_sparse_decode_layers), isolated, CUDA events"}},
+                                 "note": "the 27 reuse layers as single-layer launches back to back in one graph "
+                                         "(PDL overlaps each launch's ramp with the previous tail), per layer"}},
         "clocks": clk,
         "parity_sample": parity,
         "gpu_launches": launches_per_step * args.steps,
