@@ -96,7 +96,9 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
     pool_prefill_kernel(const __grid_constant__ PoolTmaps tm, const PoolPrefillArgs a) {
   using namespace pp;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned by pointer arithmetic on the shared array (an integer round
+  // trip would hide the address space and turn shared loads into generic LD)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmem);
   float* lse2 = reinterpret_cast<float*>(smem + kOffLse);
