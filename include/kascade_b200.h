@@ -108,6 +108,11 @@ typedef struct kscd_decode_layers {
    * 0 = one list shared by every layer (reuse runs) */
   int64_t index_stride_layer, count_stride_layer;
   int64_t scores_stride_layer, lse_stride_layer;
+  /* HOST arrays of the same L cache pointers: the dense and score passes
+   * stream K / V through TMA tensor maps encoded on the host per layer
+   * (required by kscd_dense_decode_layers / kscd_anchor_scores_decode_layers) */
+  const void* const* k_caches_host;
+  const void* const* v_caches_host;
 } kscd_decode_layers;
 
 /* Selection of one decode step: pooled post-softmax weights of the G heads

@@ -123,6 +123,7 @@ class DecodeLayers(ctypes.Structure):
         ("q_stride_layer", c_i64), ("out_stride_layer", c_i64), ("head_maps", c_vp),
         ("index_stride_layer", c_i64), ("count_stride_layer", c_i64),
         ("scores_stride_layer", c_i64), ("lse_stride_layer", c_i64),
+        ("k_caches_host", c_vp), ("v_caches_host", c_vp),
     ]
 
 

@@ -423,11 +423,9 @@ static cudaError_t launch_mode(const DecodeArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_decode_attn(int mode, const DecodeArgs& a, cudaStream_t st) {
-  switch (mode) {
-    case MODE_DENSE: return launch_mode<MODE_DENSE>(a, st);
-    case MODE_SPARSE: return launch_mode<MODE_SPARSE>(a, st);
-    default: return launch_mode<MODE_SCORES>(a, st);
-  }
+  // the dense and score passes run on the tcgen05 / TMA kernel (decode_tc.cu)
+  if (mode != MODE_SPARSE) return cudaErrorInvalidValue;
+  return launch_mode<MODE_SPARSE>(a, st);
 }
 
 int decode_tile_keys() { return kTileKeys; }

@@ -1,5 +1,6 @@
 // Internal launch structs shared by the kernels and the C-ABI layer.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -51,6 +52,20 @@ struct DecodeArgs {
 
 cudaError_t launch_decode_attn(int mode, const DecodeArgs& a, cudaStream_t st);
 int decode_tile_keys();
+
+// tcgen05 / TMA decode (decode_tc.cu) for the dense and score passes: K / V
+// blocks reach shared memory through per-layer TMA tensor maps, so a launch
+// carries up to kMaxMapLayers layers' maps (more layers: several launches)
+constexpr int kMaxMapLayers = 16;
+struct DecodeTmaps {
+  CUtensorMap k[kMaxMapLayers];
+  CUtensorMap v[kMaxMapLayers];
+};
+// k_ptrs / v_ptrs: HOST arrays of the layers' cache base pointers (v_ptrs
+// nullable for the score pass); rows past a.n read as zeros through TMA
+cudaError_t launch_decode_tc(int mode, const DecodeArgs& a, const void* const* k_ptrs, const void* const* v_ptrs,
+                             cudaStream_t st);
+int decode_tc_block_keys();
 
 // Pooled post-softmax weights for decode tiles: pooled[b][g][j] =
 // sum over the G heads of exp(s[b][h][j] - lse[b][h]).

@@ -344,7 +344,13 @@ def decode_layers(q, k_caches, v_caches, seq_len, *, workspace, tables, out=None
                                   or not head_maps.is_contiguous()):
         raise InvalidArgumentError("head_maps must be a contiguous CUDA int32 [nl][Hkv] tensor")
     kp, vp = tables[0], tables[1]
+    # host copies of the pointers: the dense / score passes encode one TMA
+    # tensor map per layer on the host (read during the call only)
+    kh = (ctypes.c_void_p * nl)(*[t_.data_ptr() for t_ in k_caches])
+    vh = (ctypes.c_void_p * nl)(*[t_.data_ptr() for t_ in v_caches])
     t = _lib.DecodeLayers(num_layers=nl, k_caches=kp.data_ptr(), v_caches=vp.data_ptr(),
+                          k_caches_host=ctypes.cast(kh, ctypes.c_void_p).value,
+                          v_caches_host=ctypes.cast(vh, ctypes.c_void_p).value,
                           q_stride_layer=q.stride(0), out_stride_layer=out.stride(0) if out is not None else q.stride(0),
                           head_maps=_ptr(head_maps), index_stride_layer=int(index_layer_stride),
                           count_stride_layer=int(count_layer_stride), scores_stride_layer=int(scores_layer_stride),
