@@ -77,26 +77,10 @@ void set_splits(kscd::DecodeArgs& a, int splits) {
   a.part_ml = a.part + (size_t)a.B * a.Hq * splits * kscd::kHeadDimC;
 }
 
-// Split-K factor of the tcgen05 dense / score passes (decode_tc.cu): 128-key
-// blocks, one CTA per SM (~200 KB of shared memory for the TMA ring).
-int plan_splits_tc(int pairs, int keys, int requested) {
-  const int blk = kscd::decode_tc_block_keys();
-  const int tiles = std::max(1, (keys + blk - 1) / blk);
-  const int cap = max_splits_for(pairs);
-  if (requested > 0) return std::max(1, std::min({requested, cap, tiles}));
-  const int slots = kSmCount;
-  const int want = std::max(1, (slots + pairs - 1) / pairs);
-  int best = 1;
-  double best_eff = -1.0;
-  for (int s = want; s <= cap && s <= tiles; ++s) {
-    const int tps = (tiles + s - 1) / s;
-    const int used = (tiles + tps - 1) / tps;
-    const double waves = (double)pairs * s / slots;
-    const double eff = (waves / ceil(waves)) * ((double)tiles / (tps * (double)used));
-    if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
-  }
-  return std::max(1, std::min(best, tiles));
-}
+// The tcgen05 dense / score passes (decode_tc.cu) split the keys stream-K
+// style over one CTA per SM; a (sequence, kv head) may span up to the
+// workspace's partial slots per head.
+int tc_partial_slots(int pairs) { return max_splits_for(pairs); }
 
 // Virtual kv heads per kv head for a query group of G heads: the smallest
 // divisor r of G with G / r <= 16 (the decode kernel's m16 tile).
@@ -210,7 +194,7 @@ int kscd_dense_decode(const kscd_decode_params* p, void* stream) {
   int rc = check_decode(p, true, false);
   if (rc) return rc;
   kscd::DecodeArgs a = make_args(p, p->seq_len);
-  set_splits(a, plan_splits_tc(a.B * a.Hkv, p->seq_len, p->num_splits));
+  set_splits(a, tc_partial_slots(a.B * a.Hkv));
   return cuda_status(kscd::launch_decode_tc(kscd::MODE_DENSE, a, &p->k_cache, &p->v_cache, (cudaStream_t)stream),
                      "kscd_dense_decode");
 }
@@ -220,7 +204,7 @@ int kscd_anchor_scores_decode(const kscd_decode_params* p, void* stream) {
   if (rc) return rc;
   if (!p->scores || !p->lse) return fail(KSCD_INVALID_ARGUMENT, "scores and lse must be non-NULL");
   kscd::DecodeArgs a = make_args(p, p->seq_len);
-  set_splits(a, plan_splits_tc(a.B * a.Hkv, p->seq_len, p->num_splits));
+  set_splits(a, tc_partial_slots(a.B * a.Hkv));
   return cuda_status(kscd::launch_decode_tc(kscd::MODE_SCORES, a, &p->k_cache, nullptr, (cudaStream_t)stream),
                      "kscd_anchor_scores_decode");
 }
@@ -278,7 +262,7 @@ static int decode_layers(int mode, const kscd_decode_params* p, const kscd_decod
   // dense / score passes: tcgen05 + TMA, tensor maps encoded from the host pointers
   if (!t->k_caches_host || (mode == kscd::MODE_DENSE && !t->v_caches_host))
     return fail(KSCD_INVALID_ARGUMENT, "k_caches_host / v_caches_host must be non-NULL for dense / score passes");
-  set_splits(a, plan_splits_tc(a.B * a.Hkv, p->seq_len, p->num_splits));
+  set_splits(a, tc_partial_slots(a.B * a.Hkv));
   return cuda_status(kscd::launch_decode_tc(mode, a, t->k_caches_host,
                                             mode == kscd::MODE_DENSE ? t->v_caches_host : nullptr,
                                             (cudaStream_t)stream), what);

@@ -39,10 +39,12 @@ using namespace sm100;
 namespace dtc {
 constexpr int kBlk = 128;                 // keys per block = UMMA M
 constexpr int kN = 16;                    // UMMA N: the group's heads, padded
-constexpr int kThreads = 192;
+constexpr int kThreads = 224;          // 7 warps: K/Q TMA, MMA, 4 softmax, V TMA
 constexpr int kTile = kBlk * 256;         // one K or V block, 32 KB
 constexpr int kHalf = kBlk * 128;         // one 64-column half of a block
+constexpr int kQBytes = 2 * kN * 128;     // Q of a group: [2 halves][16 rows][128 B]
 constexpr int kMaxSplits = 64;
+constexpr int kCtas = 148;                // one persistent CTA per SM
 constexpr uint32_t kIdescS = idesc_bf16(128, kN, false, false);   // A = K (K-major), B = Q (K-major)
 constexpr uint32_t kIdescO = idesc_bf16(128, kN, true, false);    // A = V^T (MN-major), B = P^T (K-major)
 constexpr float kRescale = 8.0f;          // log2 units
@@ -51,13 +53,33 @@ template <bool HAS_V>
 struct Cfg {
   static constexpr int kStages = HAS_V ? 3 : 6;
   static constexpr int kStageBytes = HAS_V ? 2 * kTile : kTile;
-  static constexpr int kOffQ = kStages * kStageBytes;      // [2 halves][16 rows][128 B]
-  static constexpr int kOffP = kOffQ + 4096;               // 2 x [2 halves][16 rows][128 B]
+  static constexpr int kOffQ = kStages * kStageBytes;      // 2 segment buffers of kQBytes
+  static constexpr int kOffP = kOffQ + 2 * kQBytes;        // 2 block buffers of P^T [2 halves][16][128 B]
   static constexpr int kOffRed = kOffP + 8192;             // float [2][4 warps][16] block max
-  static constexpr int kOffSum = kOffRed + 2 * 4 * 16 * 4; // float [4][16] l partials, [16] m
-  static constexpr int kOffBar = kOffSum + 4 * 16 * 4 + 16 * 4;
-  static constexpr int kOffTmem = kOffBar + 32 * 8;
+  static constexpr int kOffSum = kOffRed + 2 * 4 * 16 * 4; // float [4][16] l, [4][16] l (bf16 p), [16] m
+  static constexpr int kOffW = kOffSum + 144 * 4;          // float [4 warps][64] merge weights
+  static constexpr int kOffBar = kOffW + 4 * kMaxSplits * 4;
+  static constexpr int kNumBars = 4 * kStages + 16;
+  static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffTmem + 16 + 1024;
+};
+
+// The launch's work is a flat space of 128-key blocks,
+//   f = ((layer * B + b) * Hkv + g) * nblk + j,
+// cut into equal contiguous ranges, one per CTA ("stream-K"): a CTA streams
+// its range through ONE TMA ring without draining between (sequence, kv
+// head) pairs, and each pair it touches is a segment whose partial (m, l, O)
+// it writes; the last segment of a pair to finish merges them.  Blocks past
+// a ragged sequence's length are skipped.
+struct Walk {
+  int nblk, P, Hkv, n;
+  const int* lens;
+  KSCD_DEV int blocks_of(int pair) const {
+    if (!lens) return (n + kBlk - 1) / kBlk;
+    const int b = (pair % P) / Hkv;
+    const int cnt = max(0, min(__ldg(lens + b), n));
+    return (cnt + kBlk - 1) / kBlk;
+  }
 };
 }  // namespace dtc
 
@@ -84,21 +106,35 @@ KSCD_DEV void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int 
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+// named barrier with an OR vote over the participating threads
+KSCD_DEV bool bar_any(uint32_t id, uint32_t nthreads, bool pred) {
+  uint32_t r;
+  asm volatile(
+      "{\n .reg .pred p, q;\n setp.ne.u32 q, %1, 0;\n barrier.cta.red.or.pred p, %2, %3, q;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(r)
+      : "r"((uint32_t)pred), "r"(id), "r"(nthreads)
+      : "memory");
+  return r != 0;
+}
 
 // Byte offset of element (row, col) in a [2 halves of 64 cols][rows][128 B]
 // SWIZZLE_128B tile (16-byte chunks XOR-permuted by row % 8): the canonical
-// K-major layout UMMA reads for Q (rows = heads, cols = d) and P^T (rows =
-// heads, cols = keys).
+// K-major layout UMMA reads for P^T (rows = heads, cols = keys).
 KSCD_DEV uint32_t sw128_off(int row, int col, int rows) {
   const int half = col >> 6, c = col & 63;
   return half * rows * 128 + row * 128 + ((((c >> 3) ^ (row & 7)) & 7) << 4) + (c & 7) * 2;
 }
 
-// bars: 0..S-1 full[st] | S..2S-1 empty[st] | 2S+{0,1} s_full | +{2,3} s_free |
-//       +{4,5} p_full | +{6,7} pv_done | +8 o_done
-template <int MODE>
+// bars: full[S] / empty[S] (K slots), then pairs s_full, s_free, p_full,
+//       pv_done (by block parity), q_full, q_free, o_done, o_free (by segment
+//       parity), then vfull[S] / vempty[S] (V slots: a block's K slot frees
+//       when S^T retires, its V slot when PV retires)
+//
+// GM: the query heads per group rounded up to a power of two (<= 16); the
+// softmax threads only touch those S^T / O^T columns and P^T rows.
+template <int MODE, int GM>
 __global__ void __launch_bounds__(dtc::kThreads, 1)
-    decode_tc_kernel(const __grid_constant__ DecodeTmaps tm, const DecodeArgs a) {
+    decode_tc_kernel(const __grid_constant__ DecodeTmaps tm, const DecodeArgs a, const int per) {
   using namespace dtc;
   constexpr bool HAS_V = MODE == MODE_DENSE;
   using C = Cfg<HAS_V>;
@@ -112,113 +148,171 @@ __global__ void __launch_bounds__(dtc::kThreads, 1)
   uint64_t* s_free = s_full + 2;
   uint64_t* p_full = s_full + 4;
   uint64_t* pv_done = s_full + 6;
-  uint64_t* o_done = s_full + 8;
+  uint64_t* q_full = s_full + 8;
+  uint64_t* q_free = s_full + 10;
+  uint64_t* o_done = s_full + 12;
+  uint64_t* o_free = s_full + 14;
+  uint64_t* vfull = s_full + 16;
+  uint64_t* vempty = vfull + S;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffTmem);
+  int* flag = reinterpret_cast<int*>(smem + C::kOffTmem + 8);
   float* red = reinterpret_cast<float*>(smem + C::kOffRed);
   float* lred = reinterpret_cast<float*>(smem + C::kOffSum);
 
-  const int split = blockIdx.x, g = blockIdx.y;
-  const int lyr = blockIdx.z / a.B, b = blockIdx.z - lyr * a.B;
-  const int gk = g / a.kv_rep;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = a.G;
-  const __nv_bfloat16* q_l = a.q + (int64_t)lyr * a.q_ls;
-  float* out_l = a.out ? a.out + (int64_t)lyr * a.out_ls : nullptr;
-  float* part_l = reinterpret_cast<float*>(reinterpret_cast<char*>(a.part) + (int64_t)lyr * a.ws_ls);
-  float* part_ml_l = reinterpret_cast<float*>(reinterpret_cast<char*>(a.part_ml) + (int64_t)lyr * a.ws_ls);
-  int* counters_l = reinterpret_cast<int*>(reinterpret_cast<char*>(a.counters) + (int64_t)lyr * a.ws_ls);
-  float* scores_l = a.scores ? a.scores + (int64_t)lyr * a.scores_ls : nullptr;
-  float* lse_l = a.lse ? a.lse + (int64_t)lyr * a.lse_ls : nullptr;
-  const CUtensorMap* kmap = &tm.k[lyr];
-  const CUtensorMap* vmap = &tm.v[lyr];
+  const int P = a.B * a.Hkv;
+  const Walk w{(a.n + kBlk - 1) / kBlk, P, a.Hkv, a.n, a.lens};
+  const int nblk = w.nblk;
+  // Every layer's block space is cut identically into ranges of `per`
+  // blocks (a layer's result does not depend on how many layers share the
+  // launch); CTA c streams range c of each layer in turn, so the ring never
+  // drains between layers.  Its pairs (segments) are, per layer, the
+  // layer-local pairs [pl0, pl0 + npl), each over blocks [jb, je).
+  const int cta = blockIdx.x;
+  const int T1 = P * nblk;
+  const int g0 = cta * per, g1 = min(T1, g0 + per);
+  const int pl0 = g0 / nblk, npl = (g1 + nblk - 1) / nblk - pl0;
+  const int nv = a.nl * npl;
+  auto pair_of = [&](int v) {
+    const int lc = v / npl;
+    return lc * P + pl0 + (v - lc * npl);
+  };
+  auto seg_range = [&](int pair, int& jb, int& je) {
+    const int pl = pair % P;
+    jb = max(g0 - pl * nblk, 0);
+    je = min(g1 - pl * nblk, w.blocks_of(pair));
+  };
 
+  // PDL: our inputs (q, caches) are complete when we start (as decode.cu);
+  // only the workspace / output writes wait for the previous grid
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  const int count = a.lens ? min(__ldg(a.lens + b), a.n) : a.n;
-  const int nblk_all = (count + kBlk - 1) / kBlk;
-  const int bps = (nblk_all + a.splits - 1) / a.splits;
-  const int j0 = split * bps;
-  const int nb = max(0, min(nblk_all, j0 + bps) - j0);
-
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < C::kNumBars; ++s) {
+      const uint64_t* bp = &bars[s];
+      const bool by_threads = (bp >= s_free && bp < s_free + 2) || (bp >= p_full && bp < p_full + 2) ||
+                              (bp >= o_free && bp < o_free + 2);
+      mbar_init(&bars[s], by_threads ? 128 : 1);   // softmax-thread arrivals vs one arrive / commit
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 128);
-      mbar_init(&p_full[i], 128);
-      mbar_init(&pv_done[i], 1);
-    }
-    mbar_init(o_done, 1);
     fence_barrier_init();
   }
-  // Q of the group -> [2 halves][16 rows][128 B] SW128 (rows >= G zero)
-  for (int i = threadIdx.x; i < kN * 16; i += kThreads) {
-    const int row = i >> 4, ch = i & 15;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (row < G) v = *reinterpret_cast<const uint4*>(q_l + ((int64_t)b * a.Hq + g * G + row) * 128 + ch * 8);
-    *reinterpret_cast<uint4*>(smem + C::kOffQ + sw128_off(row, ch * 8, kN)) = v;
+  if (HAS_V && GM < kN) {
+    // P^T rows >= GM are never written: zero them once
+    for (int i = threadIdx.x; i < 2 * 4096 / 16; i += kThreads) {
+      const int row = (i >> 3) & 15;
+      if (row >= GM) reinterpret_cast<uint4*>(smem + C::kOffP)[i] = make_uint4(0, 0, 0, 0);
+    }
+    fence_proxy_async_smem();
   }
-  fence_proxy_async_smem();
   if (warp == 1) tmem_alloc<64>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;          // cols [0,16) S0 | [16,32) S1 | [32,48) O^T
+  const uint32_t tmem = *tmem_slot;          // cols [0,16) S0 | [16,32) S1 | [32,48) O^T 0 | [48,64) O^T 1
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0 && nb > 0) {
-      tma_prefetch(kmap);
-      if (HAS_V) tma_prefetch(vmap);
-      for (int j = 0; j < nb; ++j) {
-        const int st = j % S;
-        if (j >= S) mbar_wait(&empty[st], ((j / S) - 1) & 1);
-        mbar_expect_tx(&full[st], C::kStageBytes);
-        const int key0 = (j0 + j) * kBlk;
-        uint8_t* dst = smem + st * C::kStageBytes;
-        for (int hf = 0; hf < 2; ++hf) tma_load_4d(dst + hf * kHalf, kmap, &full[st], hf * 64, key0, gk, b);
-        if (HAS_V)
-          for (int hf = 0; hf < 2; ++hf) tma_load_4d(dst + kTile + hf * kHalf, vmap, &full[st], hf * 64, key0, gk, b);
+    if (lane == 0) {
+      tma_prefetch(&tm.q);
+      int i = 0, s = 0;
+      for (int v = 0; v < nv; ++v) {
+        const int pair = pair_of(v);
+        int jb, je;
+        seg_range(pair, jb, je);
+        if (jb >= je) continue;
+        const int lyr = pair / P, rem = pair - lyr * P, b = rem / a.Hkv, g = rem - b * a.Hkv;
+        const int gk = g / a.kv_rep;
+        const CUtensorMap* kmap = &tm.k[lyr];
+        const int qb = s & 1;                 // the segment's group Q rows
+        if (s >= 2) mbar_wait(&q_free[qb], ((s - 2) >> 1) & 1);
+        mbar_expect_tx(&q_full[qb], kQBytes);
+        for (int hf = 0; hf < 2; ++hf)
+          tma_load_3d(smem + C::kOffQ + qb * kQBytes + hf * 2048, &tm.q, &q_full[qb], hf * 64, b * a.Hq + g * G, lyr);
+        for (int j = jb; j < je; ++j, ++i) {
+          const int st = i % S;
+          if (i >= S) mbar_wait(&empty[st], ((i / S) - 1) & 1);
+          mbar_expect_tx(&full[st], kTile);
+          uint8_t* dst = smem + st * C::kStageBytes;
+          for (int hf = 0; hf < 2; ++hf) tma_load_4d(dst + hf * kHalf, kmap, &full[st], hf * 64, j * kBlk, gk, b);
+        }
+        ++s;
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------- MMA issuer
-    if (lane == 0 && nb > 0) {
-      const uint32_t qaddr = smem_u32(smem + C::kOffQ);
+    if (lane == 0) {
+      const uint32_t qaddr0 = smem_u32(smem + C::kOffQ);
       const uint32_t paddr = smem_u32(smem + C::kOffP);
-      auto issue_pv = [&](int jj) {            // O^T += V_jj^T P_jj^T
-        const int st = jj % S, pb = jj & 1;
-        mbar_wait(&p_full[pb], (jj >> 1) & 1);
+      // O^T_seg += V_ii^T P_ii^T
+      auto issue_pv = [&](int ii, int seg, bool first, bool last) {
+        const int pb = ii & 1, ob = seg & 1, st = ii % S;
+        if (first && seg >= 2) mbar_wait(&o_free[ob], ((seg - 2) >> 1) & 1);
+        mbar_wait(&vfull[st], (ii / S) & 1);
+        mbar_wait(&p_full[pb], (ii >> 1) & 1);
         tc_fence_after();
         const uint32_t vaddr = smem_u32(smem + st * C::kStageBytes + kTile);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
-          mma_ss(tmem + 32, sw128_desc(vaddr + ks * 2048, kHalf, 1024),
+          mma_ss(tmem + 32 + ob * 16, sw128_desc(vaddr + ks * 2048, kHalf, 1024),
                  sw128_desc(paddr + pb * 4096 + (ks >> 2) * 2048 + (ks & 3) * 32, 16, 1024), kIdescO,
-                 (jj > 0 || ks > 0) ? 1u : 0u);
+                 (!first || ks > 0) ? 1u : 0u);
         mma_commit(&pv_done[pb]);
-        mma_commit(&empty[st]);
+        mma_commit(&vempty[st]);
+        if (last) mma_commit(&o_done[ob]);
       };
-      for (int j = 0; j < nb; ++j) {
-        const int st = j % S, sb = j & 1;
-        mbar_wait(&full[st], (j / S) & 1);
-        if (j >= 2) mbar_wait(&s_free[sb], ((j - 2) >> 1) & 1);
-        tc_fence_after();
-        const uint32_t kaddr = smem_u32(smem + st * C::kStageBytes);
+      int i = 0, s = 0, pseg = 0;
+      bool pfirst = false, plast = false;
+      for (int v = 0; v < nv; ++v) {
+        const int pair = pair_of(v);
+        int jb, je;
+        seg_range(pair, jb, je);
+        if (jb >= je) continue;
+        mbar_wait(&q_full[s & 1], (s >> 1) & 1);
+        const uint32_t qaddr = qaddr0 + (s & 1) * kQBytes;
+        for (int j = jb; j < je; ++j, ++i) {
+          const int st = i % S, sb = i & 1;
+          mbar_wait(&full[st], (i / S) & 1);
+          if (i >= 2) mbar_wait(&s_free[sb], ((i - 2) >> 1) & 1);
+          tc_fence_after();
+          const uint32_t kaddr = smem_u32(smem + st * C::kStageBytes);
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-          const uint32_t off = (ks >> 2) * kHalf + (ks & 3) * 32;
-          mma_ss(tmem + sb * 16, sw128_desc(kaddr + off, 16, 1024),
-                 sw128_desc(qaddr + (ks >> 2) * 2048 + (ks & 3) * 32, 16, 1024), kIdescS, ks > 0);
+          for (int ks = 0; ks < 8; ++ks) {
+            const uint32_t off = (ks >> 2) * kHalf + (ks & 3) * 32;
+            mma_ss(tmem + sb * 16, sw128_desc(kaddr + off, 16, 1024),
+                   sw128_desc(qaddr + (ks >> 2) * 2048 + (ks & 3) * 32, 16, 1024), kIdescS, ks > 0);
+          }
+          mma_commit(&s_full[sb]);
+          if (j == je - 1) mma_commit(&q_free[s & 1]);
+          mma_commit(&empty[st]);                 // K consumed once S^T retires
+          if (HAS_V && i > 0) issue_pv(i - 1, pseg, pfirst, plast);
+          pseg = s;
+          pfirst = j == jb;
+          plast = j == je - 1;
         }
-        mma_commit(&s_full[sb]);
-        if (!HAS_V) mma_commit(&empty[st]);     // K consumed once S^T retires
-        if (HAS_V && j >= 1) issue_pv(j - 1);
+        ++s;
       }
-      if (HAS_V) issue_pv(nb - 1);
-      mma_commit(o_done);
+      if (HAS_V && i > 0) issue_pv(i - 1, pseg, pfirst, plast);
+    }
+  } else if (warp == 6) {
+    // ---------------------------------------------------------- V TMA producer
+    if (HAS_V && lane == 0) {
+      int i = 0;
+      for (int v = 0; v < nv; ++v) {
+        const int pair = pair_of(v);
+        int jb, je;
+        seg_range(pair, jb, je);
+        if (jb >= je) continue;
+        const int lyr = pair / P, rem = pair - lyr * P, b = rem / a.Hkv, g = rem - b * a.Hkv;
+        const int gk = g / a.kv_rep;
+        const CUtensorMap* vmap = &tm.v[lyr];
+        for (int j = jb; j < je; ++j, ++i) {
+          const int st = i % S;
+          if (i >= S) mbar_wait(&vempty[st], ((i / S) - 1) & 1);
+          mbar_expect_tx(&vfull[st], kTile);
+          uint8_t* dst = smem + st * C::kStageBytes + kTile;
+          for (int hf = 0; hf < 2; ++hf) tma_load_4d(dst + hf * kHalf, vmap, &vfull[st], hf * 64, j * kBlk, gk, b);
+        }
+      }
     }
   } else {
     // ------------------------------------------------------ softmax / epilogue
@@ -226,208 +320,305 @@ __global__ void __launch_bounds__(dtc::kThreads, 1)
     const int wi = warp - 2;                          // softmax warp 0..3
     const int kin = qw * 32 + lane;                   // key within the block / dim of O^T
     const uint32_t lane_base = tmem + ((uint32_t)(qw * 32) << 16);
-    float m_used[kN], lsum[kN];
-#pragma unroll
-    for (int h = 0; h < kN; ++h) {
-      m_used[h] = -INFINITY;
-      lsum[h] = 0.f;
-    }
-    for (int j = 0; j < nb; ++j) {
-      const int sb = j & 1;
-      mbar_wait(&s_full[sb], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t r[16];
-      tmem_ld16(lane_base + sb * 16, r);
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&s_free[sb]);
-      const int key = (j0 + j) * kBlk + kin;
-      const bool valid = key < count;
-      float s[kN];
-#pragma unroll
-      for (int h = 0; h < kN; ++h) s[h] = (valid && h < G) ? __uint_as_float(r[h]) * a.scale_log2 : -INFINITY;
-      if (scores_l && valid) {
-#pragma unroll
-        for (int h = 0; h < kN; ++h)
-          if (h < G) scores_l[((int64_t)b * a.Hq + g * G + h) * a.score_stride + key] = s[h];
-      }
-      // block max per head: warp shuffles, then the 4 warps through smem
-      float* rb = red + sb * 64;
-#pragma unroll
-      for (int h = 0; h < kN; ++h) {
-        if (h < G) {
-          const float mx = warp_max(s[h]);
-          if (lane == 0) rb[wi * 16 + h] = mx;
-        }
-      }
-      named_bar_sync(1, 128);
-      bool need_any = false;
-      float alpha[kN];
-#pragma unroll
-      for (int h = 0; h < kN; ++h) {
-        alpha[h] = 1.f;
-        if (h < G) {
-          const float mb = fmaxf(fmaxf(rb[h], rb[16 + h]), fmaxf(rb[32 + h], rb[48 + h]));
-          if (mb > m_used[h] + kRescale) {          // uniform across the CTA
-            alpha[h] = m_used[h] == -INFINITY ? 1.f : exp2f(m_used[h] - mb);
-            m_used[h] = mb;
-            need_any = true;
+    float* wsp = reinterpret_cast<float*>(smem + C::kOffW) + wi * kMaxSplits;
+    bool waited = false;
+    int i = 0, s = 0;
+    for (int v = 0; v < nv; ++v) {
+      const int pair = pair_of(v);
+      int jb, je;
+      seg_range(pair, jb, je);
+      const int lyr = pair / P, rem = pair - lyr * P, b = rem / a.Hkv, g = rem - b * a.Hkv;
+      const int64_t bh0 = (int64_t)b * a.Hq + (int64_t)g * G;
+      float* out_l = a.out ? a.out + (int64_t)lyr * a.out_ls : nullptr;
+      float* lse_l = a.lse ? a.lse + (int64_t)lyr * a.lse_ls : nullptr;
+      if (jb >= je) {
+        // a pair with no keys at all (ragged length 0) whose first block
+        // lies in this CTA's range: zero output, lse = -inf
+        if (w.blocks_of(pair) == 0 && (pair % P) * nblk >= g0) {
+          if (!waited) {
+            asm volatile("griddepcontrol.wait;\n" ::: "memory");
+            waited = true;
+          }
+          for (int h = 0; h < G; ++h) {
+            if (HAS_V && out_l) out_l[(bh0 + h) * 128 + kin] = 0.f;
+            if (kin == 0 && lse_l) lse_l[bh0 + h] = -INFINITY;
           }
         }
+        continue;
       }
-      const bool rescale = HAS_V && need_any && j > 0;
-      float p[kN];
+      const int count = a.lens ? min(__ldg(a.lens + b), a.n) : a.n;
+      float* sc_base = a.scores ? a.scores + (int64_t)lyr * a.scores_ls + bh0 * a.score_stride : nullptr;
+      float m_used[GM], lsum[GM], lbf[GM];
 #pragma unroll
-      for (int h = 0; h < kN; ++h) {
-        const float mu = m_used[h] == -INFINITY ? 0.f : m_used[h];
-        p[h] = (h < G && valid) ? exp2f(s[h] - mu) : 0.f;
-        lsum[h] = lsum[h] * alpha[h] + p[h];
+      for (int h = 0; h < GM; ++h) {
+        m_used[h] = -INFINITY;
+        lsum[h] = 0.f;
+        lbf[h] = 0.f;
       }
-      if (HAS_V) {
-        if (!valid) {
-          // a key past this sequence's length (ragged batch): its V row may
-          // hold anything (NaN * 0 would poison O); zero it before PV reads it
-          uint8_t* vrow = smem + ((j % S) * C::kStageBytes) + kTile + kin * 128;
-          *reinterpret_cast<uint4*>(vrow) = make_uint4(0, 0, 0, 0);
-#pragma unroll
-          for (int c = 1; c < 8; ++c) reinterpret_cast<uint4*>(vrow)[c] = make_uint4(0, 0, 0, 0);
-#pragma unroll
-          for (int c = 0; c < 8; ++c) reinterpret_cast<uint4*>(vrow + kHalf)[c] = make_uint4(0, 0, 0, 0);
-        }
-        if (rescale) {
-          // O^T holds blocks < j: wait for PV_{j-1}, scale each head's column
-          mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
-          tc_fence_after();
-          uint32_t o[16];
-          tmem_ld16(lane_base + 32, o);
-          tmem_ld_wait();
-#pragma unroll
-          for (int h = 0; h < kN; ++h) o[h] = __float_as_uint(__uint_as_float(o[h]) * alpha[h]);
-          tmem_st16(lane_base + 32, o);
-          tmem_st_wait();
-        }
-        if (j >= 2) mbar_wait(&pv_done[sb], ((j - 2) >> 1) & 1);   // P buffer read by PV_{j-2}
-        uint8_t* pbuf = smem + C::kOffP + sb * 4096;
-#pragma unroll
-        for (int h = 0; h < kN; ++h)
-          *reinterpret_cast<__nv_bfloat16*>(pbuf + sw128_off(h, kin, kN)) = __float2bfloat16_rn(p[h]);
-        fence_proxy_async_smem();
+      for (int j = jb; j < je; ++j, ++i) {
+        const int sb = i & 1;
+        mbar_wait(&s_full[sb], (i >> 1) & 1);
+        tc_fence_after();
+        uint32_t r[16];
+        tmem_ld16(lane_base + sb * 16, r);
+        tmem_ld_wait();
         tc_fence_before();
-        mbar_arrive(&p_full[sb]);
-      }
-    }
-    // ---- epilogue: l per head (4-warp reduce), this split's partial --------
+        mbar_arrive(&s_free[sb]);
+        const int key = j * kBlk + kin;
+        const bool valid = key < count;
+        float sv[GM];
 #pragma unroll
-    for (int h = 0; h < kN; ++h) {
-      if (h < G) {
+        for (int h = 0; h < GM; ++h) sv[h] = (valid && h < G) ? __uint_as_float(r[h]) * a.scale_log2 : -INFINITY;
+        if (sc_base && valid) {
+#pragma unroll
+          for (int h = 0; h < GM; ++h)
+            if (h < G) sc_base[h * a.score_stride + key] = sv[h];
+        }
+        if (!HAS_V) {
+          // score pass: no shared O accumulator, so each thread keeps its own
+          // lazy reference per head (merged in the epilogue) -- no barrier
+#pragma unroll
+          for (int h = 0; h < GM; ++h) {
+            if (sv[h] > m_used[h] + kRescale) {
+              lsum[h] *= m_used[h] == -INFINITY ? 1.f : fast_exp2(m_used[h] - sv[h]);
+              m_used[h] = sv[h];
+            }
+            lsum[h] += valid && h < G ? fast_exp2(sv[h] - m_used[h]) : 0.f;
+          }
+          continue;
+        }
+        // lazy max: the CTA-wide block max is only formed when some key
+        // exceeds the running reference by more than 2^8 (one OR vote)
+        bool need = false;
+#pragma unroll
+        for (int h = 0; h < GM; ++h) need |= sv[h] > m_used[h] + kRescale;
+        float alpha[GM];
+#pragma unroll
+        for (int h = 0; h < GM; ++h) alpha[h] = 1.f;
+        bool rescaled = false;
+        if (bar_any(1, 128, need)) {
+          float* rb = red + sb * 64;
+#pragma unroll
+          for (int h = 0; h < GM; ++h) {
+            const float mx = warp_max(sv[h]);
+            if (lane == 0) rb[wi * 16 + h] = mx;
+          }
+          named_bar_sync(1, 128);
+#pragma unroll
+          for (int h = 0; h < GM; ++h) {
+            const float mb = fmaxf(fmaxf(rb[h], rb[16 + h]), fmaxf(rb[32 + h], rb[48 + h]));
+            if (mb > m_used[h] + kRescale) {          // uniform across the CTA
+              alpha[h] = m_used[h] == -INFINITY ? 1.f : fast_exp2(m_used[h] - mb);
+              m_used[h] = mb;
+              rescaled = true;
+            }
+          }
+        }
+        float p[GM];
+#pragma unroll
+        for (int h = 0; h < GM; ++h) {
+          p[h] = valid && h < G ? fast_exp2(sv[h] - m_used[h]) : 0.f;
+          lsum[h] = lsum[h] * alpha[h] + p[h];
+        }
+        if (HAS_V) {
+          if (!valid) {
+            // a key past this sequence's length (ragged batch): its V row may
+            // hold anything (NaN * 0 would poison O); zero it before PV reads it
+            mbar_wait(&vfull[i % S], (i / S) & 1);
+            uint8_t* vrow = smem + (i % S) * C::kStageBytes + kTile + kin * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) reinterpret_cast<uint4*>(vrow)[c] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) reinterpret_cast<uint4*>(vrow + kHalf)[c] = make_uint4(0, 0, 0, 0);
+          }
+          if (rescaled && j > jb) {
+            // O^T holds this segment's blocks < j: wait for PV_{i-1}, scale each head's column
+            mbar_wait(&pv_done[(i - 1) & 1], ((i - 1) >> 1) & 1);
+            tc_fence_after();
+            uint32_t o[16];
+            tmem_ld16(lane_base + 32 + (s & 1) * 16, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int h = 0; h < GM; ++h) o[h] = __float_as_uint(__uint_as_float(o[h]) * alpha[h]);
+            tmem_st16(lane_base + 32 + (s & 1) * 16, o);
+            tmem_st_wait();
+          }
+          if (i >= 2) mbar_wait(&pv_done[sb], ((i - 2) >> 1) & 1);   // P buffer read by PV_{i-2}
+          uint8_t* pbuf = smem + C::kOffP + sb * 4096;
+#pragma unroll
+          for (int h = 0; h < GM; ++h) {
+            const __nv_bfloat16 pb = __float2bfloat16_rn(p[h]);
+            // O is normalised by the sum of the bf16 weights the MMA used
+            lbf[h] = lbf[h] * alpha[h] + __bfloat162float(pb);
+            *reinterpret_cast<__nv_bfloat16*>(pbuf + sw128_off(h, kin, kN)) = pb;
+          }
+          fence_proxy_async_smem();
+          tc_fence_before();
+          mbar_arrive(&p_full[sb]);
+        }
+      }
+
+      // ---- segment epilogue: l per head (4-warp reduce), partial or output --
+      if (!HAS_V) {
+        // per-thread (m, l) -> one reference per head: the CTA max of the m's
+#pragma unroll
+        for (int h = 0; h < GM; ++h) {
+          const float mw = warp_max(m_used[h]);
+          if (lane == 0) red[wi * 16 + h] = mw;
+        }
+        named_bar_sync(1, 128);
+#pragma unroll
+        for (int h = 0; h < GM; ++h) {
+          const float M = fmaxf(fmaxf(red[h], red[16 + h]), fmaxf(red[32 + h], red[48 + h]));
+          lsum[h] = m_used[h] == -INFINITY ? 0.f : lsum[h] * fast_exp2(m_used[h] - M);
+          m_used[h] = M;
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < GM; ++h) {
         const float t = warp_sum(lsum[h]);
-        if (lane == 0) lred[wi * 16 + h] = t;
+        const float tb = HAS_V ? warp_sum(lbf[h]) : t;
+        if (lane == 0) {
+          lred[wi * 16 + h] = t;
+          lred[64 + wi * 16 + h] = tb;
+        }
       }
-    }
-    if (wi == 0 && lane < kN) lred[64 + lane] = m_used[lane];
-    named_bar_sync(1, 128);
-    float o[kN];
-    if (HAS_V && nb > 0) {
-      mbar_wait(o_done, 0);
-      tc_fence_after();
-      uint32_t r[16];
-      tmem_ld16(lane_base + 32, r);
-      tmem_ld_wait();
+      if (wi == 0 && lane < GM) {
 #pragma unroll
-      for (int h = 0; h < kN; ++h) o[h] = __uint_as_float(r[h]);
-    } else {
+        for (int h = 0; h < GM; ++h)
+          if (lane == h) lred[128 + h] = m_used[h];
+      }
+      named_bar_sync(1, 128);
+      float o[GM];
+      if (HAS_V) {
+        mbar_wait(&o_done[s & 1], (s >> 1) & 1);
+        tc_fence_after();
+        uint32_t ro[16];
+        tmem_ld16(lane_base + 32 + (s & 1) * 16, ro);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&o_free[s & 1]);
 #pragma unroll
-      for (int h = 0; h < kN; ++h) o[h] = 0.f;
-    }
-    // the previous grid (PDL) may still use the shared workspace / outputs
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    const int64_t bh0 = (int64_t)b * a.Hq + (int64_t)g * G;
-    const int d = kin;                                // O^T lane = dimension
-#pragma unroll
-    for (int h = 0; h < kN; ++h) {
-      if (h >= G) continue;
-      const float L = lred[h] + lred[16 + h] + lred[32 + h] + lred[48 + h];
-      const float M = lred[64 + h];
-      if (a.splits == 1) {
-        if (HAS_V && out_l) out_l[(bh0 + h) * 128 + d] = L > 0.f ? o[h] / L : 0.f;
-        if (d == 0 && lse_l) lse_l[bh0 + h] = (M + __log2f(L)) * kLn2;
+        for (int h = 0; h < GM; ++h) o[h] = __uint_as_float(ro[h]);
       } else {
-        const int64_t pi = (bh0 + h) * a.splits + split;
-        if (HAS_V) part_l[pi * 128 + d] = o[h];
-        if (d == 0) *reinterpret_cast<float2*>(part_ml_l + pi * 2) = make_float2(M, L);
+#pragma unroll
+        for (int h = 0; h < GM; ++h) o[h] = 0.f;
+      }
+      ++s;
+      if (!waited) {
+        // the previous grid (PDL) may still use the workspace / outputs
+        asm volatile("griddepcontrol.wait;\n" ::: "memory");
+        waited = true;
+      }
+      const int pl = pair - lyr * P;                    // pair within the layer
+      const int c_first = (pl * nblk) / per;
+      const int nseg = (pl * nblk + w.blocks_of(pair) - 1) / per - c_first + 1;
+      const int seg = cta - c_first;
+      float* part_l = reinterpret_cast<float*>(reinterpret_cast<char*>(a.part) + (int64_t)lyr * a.ws_ls);
+      float* part_ml_l = reinterpret_cast<float*>(reinterpret_cast<char*>(a.part_ml) + (int64_t)lyr * a.ws_ls);
+      const int d = kin;                                // O^T lane = dimension
+#pragma unroll
+      for (int h = 0; h < GM; ++h) {
+        if (h >= G) continue;
+        const float L = lred[h] + lred[16 + h] + lred[32 + h] + lred[48 + h];
+        const float Lb = lred[64 + h] + lred[80 + h] + lred[96 + h] + lred[112 + h];
+        const float M = lred[128 + h];
+        const float on = Lb > 0.f ? o[h] / Lb : 0.f;
+        if (nseg == 1) {
+          if (HAS_V && out_l) out_l[(bh0 + h) * 128 + d] = on;
+          if (d == 0 && lse_l) lse_l[bh0 + h] = (M + __log2f(L)) * kLn2;
+        } else {
+          const int64_t pi = (bh0 + h) * a.splits + seg;
+          if (HAS_V) part_l[pi * 128 + d] = on;
+          if (d == 0) *reinterpret_cast<float2*>(part_ml_l + pi * 2) = make_float2(M, L);
+        }
+      }
+      if (nseg == 1) continue;
+      // the last segment of this (sequence, kv head) to finish merges
+      __threadfence();
+      named_bar_sync(1, 128);
+      if (threadIdx.x == 64) {
+        int* ctr = reinterpret_cast<int*>(reinterpret_cast<char*>(a.counters) + (int64_t)lyr * a.ws_ls) +
+                   (int64_t)b * a.Hkv + g;
+        const int prev_n = atomicAdd(ctr, 1);
+        *flag = prev_n == nseg - 1;
+        if (*flag) *ctr = 0;                          // re-arm for the next launch / graph replay
+      }
+      named_bar_sync(1, 128);
+      if (!*flag) continue;
+      __threadfence();
+      for (int h = wi; h < G; h += 4) {
+        const int64_t p0 = (bh0 + h) * a.splits;
+        float2 ml[kMaxSplits / 32];
+#pragma unroll
+        for (int u = 0; u < kMaxSplits / 32; ++u) {
+          const int sp = lane + 32 * u;
+          ml[u] = sp < nseg ? __ldcg(reinterpret_cast<const float2*>(part_ml_l + (p0 + sp) * 2))
+                            : make_float2(-INFINITY, 0.f);
+        }
+        float M = -INFINITY;
+#pragma unroll
+        for (int u = 0; u < kMaxSplits / 32; ++u) M = fmaxf(M, ml[u].x);
+        M = warp_max(M);
+        const float Mu = M == -INFINITY ? 0.f : M;
+        float L = 0.f;
+#pragma unroll
+        for (int u = 0; u < kMaxSplits / 32; ++u) {
+          const float wgt = ml[u].x == -INFINITY ? 0.f : fast_exp2(ml[u].x - Mu) * ml[u].y;
+          L += wgt;
+          wsp[lane + 32 * u] = wgt;
+        }
+        L = warp_sum(L);
+        __syncwarp();
+        if (HAS_V) {
+          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          constexpr int kB = 8;
+          for (int sp0 = 0; sp0 < nseg; sp0 += kB) {
+            float4 v[kB];
+#pragma unroll
+            for (int u = 0; u < kB; ++u)
+              v[u] = sp0 + u < nseg ? __ldcg(reinterpret_cast<const float4*>(part_l + (p0 + sp0 + u) * 128 + lane * 4))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < kB; ++u) {
+              const float sc = sp0 + u < nseg ? wsp[sp0 + u] : 0.f;
+              acc.x += sc * v[u].x; acc.y += sc * v[u].y; acc.z += sc * v[u].z; acc.w += sc * v[u].w;
+            }
+          }
+          const float inv = L > 0.f ? 1.f / L : 0.f;
+          if (out_l)
+            *reinterpret_cast<float4*>(out_l + (bh0 + h) * 128 + lane * 4) =
+                make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+        }
+        if (lane == 0 && lse_l) lse_l[bh0 + h] = (M + __log2f(L)) * kLn2;
+        __syncwarp();
       }
     }
   }
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   __syncthreads();
   if (warp == 1) {
+    __syncwarp();
     tc_fence_after();
     tmem_dealloc<64>(tmem);
   }
-  if (a.splits == 1) return;
+}
 
-  // ---- the last CTA of this (b, g) merges the splits (as decode.cu) -------
-  __shared__ int is_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int* ctr = counters_l + (int64_t)b * a.Hkv + g;
-    const int prev = atomicAdd(ctr, 1);
-    is_last = prev == a.splits - 1;
-    if (is_last) *ctr = 0;                     // re-arm for the next launch / graph replay
-  }
-  __syncthreads();
-  if (!is_last || warp < 2) return;
-  __threadfence();
-  const int wi = warp - 2;
-  float* wsp = reinterpret_cast<float*>(smem) + wi * kMaxSplits;      // reuses the ring
-  const int64_t bh0 = (int64_t)b * a.Hq + (int64_t)g * G;
-  for (int h = wi; h < G; h += 4) {
-    const int64_t p0 = (bh0 + h) * a.splits;
-    float2 ml[kMaxSplits / 32];
-#pragma unroll
-    for (int i = 0; i < kMaxSplits / 32; ++i) {
-      const int sp = lane + 32 * i;
-      ml[i] = sp < a.splits ? __ldcg(reinterpret_cast<const float2*>(part_ml_l + (p0 + sp) * 2))
-                            : make_float2(-INFINITY, 0.f);
-    }
-    float M = -INFINITY;
-#pragma unroll
-    for (int i = 0; i < kMaxSplits / 32; ++i) M = fmaxf(M, ml[i].x);
-    M = warp_max(M);
-    const float Mu = M == -INFINITY ? 0.f : M;
-    float L = 0.f;
-#pragma unroll
-    for (int i = 0; i < kMaxSplits / 32; ++i) {
-      const float sc = ml[i].x == -INFINITY ? 0.f : fast_exp2(ml[i].x - Mu);
-      L += sc * ml[i].y;
-      wsp[lane + 32 * i] = sc;
-    }
-    L = warp_sum(L);
-    __syncwarp();
-    if (HAS_V) {
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      constexpr int kB = 8;
-      for (int sp0 = 0; sp0 < a.splits; sp0 += kB) {
-        float4 v[kB];
-#pragma unroll
-        for (int u = 0; u < kB; ++u)
-          v[u] = sp0 + u < a.splits ? __ldcg(reinterpret_cast<const float4*>(part_l + (p0 + sp0 + u) * 128 + lane * 4))
-                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int u = 0; u < kB; ++u) {
-          const float sc = sp0 + u < a.splits ? wsp[sp0 + u] : 0.f;
-          acc.x += sc * v[u].x; acc.y += sc * v[u].y; acc.z += sc * v[u].z; acc.w += sc * v[u].w;
-        }
-      }
-      const float inv = L > 0.f ? 1.f / L : 0.f;
-      if (out_l)
-        *reinterpret_cast<float4*>(out_l + (bh0 + h) * 128 + lane * 4) =
-            make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-    }
-    if (lane == 0 && lse_l) lse_l[bh0 + h] = (M + __log2f(L)) * kLn2;
-    __syncwarp();
-  }
+template <int MODE, int GM>
+static cudaError_t launch_tc(const cudaLaunchConfig_t& cfg, const DecodeTmaps& tm, const DecodeArgs& c, int per) {
+  static const cudaError_t at = cudaFuncSetAttribute(decode_tc_kernel<MODE, GM>,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)cfg.dynamicSmemBytes);
+  if (at != cudaSuccess) return at;
+  return cudaLaunchKernelEx(&cfg, decode_tc_kernel<MODE, GM>, tm, c, per);
+}
+
+template <int MODE>
+static cudaError_t launch_tc_g(const cudaLaunchConfig_t& cfg, const DecodeTmaps& tm, const DecodeArgs& c, int per) {
+  if (c.G <= 1) return launch_tc<MODE, 1>(cfg, tm, c, per);
+  if (c.G <= 2) return launch_tc<MODE, 2>(cfg, tm, c, per);
+  if (c.G <= 4) return launch_tc<MODE, 4>(cfg, tm, c, per);
+  if (c.G <= 8) return launch_tc<MODE, 8>(cfg, tm, c, per);
+  return launch_tc<MODE, 16>(cfg, tm, c, per);
 }
 
 // ------------------------------------------------------------------- host
@@ -463,6 +654,23 @@ static bool make_cache_map(CUtensorMap* m, const void* base, int B, int Hkv, int
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Q of the launch's layers [layers][B*Hq][128] bf16 (layer stride q_ls
+// elements), box {64, 16 rows, 1}: a group's (padded) 16 query rows per
+// half; rows past B*Hq read as zeros.
+static bool make_q_map(CUtensorMap* m, const void* base, int rows, int layers, int64_t layer_stride) {
+  EncodeTiled4Fn fn = encode4_fn();
+  if (!fn) return false;
+  const int64_t ls = layers > 1 ? layer_stride : (int64_t)rows * 128;
+  if (ls <= 0 || (ls & 7)) return false;
+  cuuint64_t dims[3] = {128, (cuuint64_t)rows, (cuuint64_t)layers};
+  cuuint64_t strides[2] = {256, (cuuint64_t)ls * 2};
+  cuuint32_t box[3] = {64, (cuuint32_t)dtc::kN, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int decode_tc_block_keys() { return dtc::kBlk; }
 
 cudaError_t launch_decode_tc(int mode, const DecodeArgs& a_in, const void* const* k_ptrs, const void* const* v_ptrs,
@@ -483,6 +691,7 @@ cudaError_t launch_decode_tc(int mode, const DecodeArgs& a_in, const void* const
     DecodeArgs c = a;
     c.nl = m;
     c.q = a.q + (int64_t)l0 * a.q_ls;
+    if (!make_q_map(&tm.q, c.q, a.B * a.Hq, m, a.q_ls)) return cudaErrorInvalidValue;
     if (a.out) c.out = a.out + (int64_t)l0 * a.out_ls;
     if (a.scores) c.scores = a.scores + (int64_t)l0 * a.scores_ls;
     if (a.lse) c.lse = a.lse + (int64_t)l0 * a.lse_ls;
@@ -491,8 +700,17 @@ cudaError_t launch_decode_tc(int mode, const DecodeArgs& a_in, const void* const
     c.counters = reinterpret_cast<int*>(reinterpret_cast<char*>(a.counters) + (int64_t)l0 * a.ws_ls);
     const bool has_v = mode == MODE_DENSE;
     const int smem = has_v ? dtc::Cfg<true>::kSmem : dtc::Cfg<false>::kSmem;
+    // stream-K: equal contiguous ranges of the flat block space, one per SM;
+    // a (sequence, kv head) spans at most a.splits ranges (its partial slots)
+    const int64_t nblk = (a.n + dtc::kBlk - 1) / dtc::kBlk;
+    const int64_t T1 = (int64_t)a.B * a.Hkv * nblk;
+    if (T1 * m >= ((int64_t)1 << 31) || a.splits < 2) return cudaErrorInvalidValue;
+    int64_t per = (T1 + dtc::kCtas - 1) / dtc::kCtas;
+    per = std::max<int64_t>(per, (nblk - 1 + a.splits - 2) / (a.splits - 1));
+    per = std::max<int64_t>(per, 1);
+    const int nctas = (int)((T1 + per - 1) / per);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(c.splits, c.Hkv, c.B * m);
+    cfg.gridDim = dim3(nctas);
     cfg.blockDim = dim3(dtc::kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -501,18 +719,8 @@ cudaError_t launch_decode_tc(int mode, const DecodeArgs& a_in, const void* const
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e;
-    if (has_v) {
-      static const cudaError_t at = cudaFuncSetAttribute(decode_tc_kernel<MODE_DENSE>,
-                                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (at != cudaSuccess) return at;
-      e = cudaLaunchKernelEx(&cfg, decode_tc_kernel<MODE_DENSE>, tm, c);
-    } else {
-      static const cudaError_t at = cudaFuncSetAttribute(decode_tc_kernel<MODE_SCORES>,
-                                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (at != cudaSuccess) return at;
-      e = cudaLaunchKernelEx(&cfg, decode_tc_kernel<MODE_SCORES>, tm, c);
-    }
+    const cudaError_t e = has_v ? launch_tc_g<MODE_DENSE>(cfg, tm, c, (int)per)
+                                : launch_tc_g<MODE_SCORES>(cfg, tm, c, (int)per);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();

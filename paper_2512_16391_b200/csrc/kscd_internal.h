@@ -60,6 +60,7 @@ constexpr int kMaxMapLayers = 16;
 struct DecodeTmaps {
   CUtensorMap k[kMaxMapLayers];
   CUtensorMap v[kMaxMapLayers];
+  CUtensorMap q;                          // [layers][B*Hq][128] bf16, 16-row boxes
 };
 // k_ptrs / v_ptrs: HOST arrays of the layers' cache base pointers (v_ptrs
 // nullable for the score pass); rows past a.n read as zeros through TMA

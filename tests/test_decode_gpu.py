@@ -127,7 +127,14 @@ def test_full_budget_sparse_equals_dense(cuda_ok):
     idx = torch.arange(n, dtype=torch.int32, device="cuda").repeat(B, Hkv, 1).contiguous()
     cnt = torch.full((B, Hkv), n, dtype=torch.int32, device="cuda")
     sp = ops.sparse_decode(qd, Kd, Vd, n, idx, cnt)
-    np.testing.assert_allclose(sp.cpu().numpy(), dense.cpu().numpy(), rtol=0, atol=1e-5)
+    # the dense pass runs on the tcgen05 kernel and the sparse pass on the
+    # gather kernel: both round P to bf16 once, in different key orders, so
+    # they agree to the bf16 weight rounding (2^-9 relative per weight)
+    _, Y, _ = _oracle_dense(q, K, V, n)
+    for got in (dense, sp):
+        rel = assert_outputs_close(got.cpu().numpy(), Y)[2]
+        assert rel < 3e-3, rel
+    np.testing.assert_allclose(sp.cpu().numpy(), dense.cpu().numpy(), rtol=0, atol=1e-3)
 
 
 def test_topk_contract_golden(cuda_ok):
