@@ -10,26 +10,38 @@
 //   O^T[d][h]  += V_blk^T . P^T     M = 128 (d),  N = 16,                 K = 128 keys
 //
 // so the MMA shapes are M128 x N16 (legal kind::f16 shapes) instead of a
-// 4-row M tile, S^T and O^T live in TMEM (48 of 64 allocated columns), and a
-// softmax thread owns one key (TMEM lane) -- and, for O^T, one dimension.
+// 4-row M tile, S^T (2 buffers) and O^T (2 buffers) live in TMEM (64
+// columns), and a softmax thread owns one key (TMEM lane) -- and, for O^T,
+// one dimension.
 // V^T is the V block as TMA stored it ([key][d], SW128), read as an MN-major
 // A operand; P^T (bf16, [head][key], SW128) is written by the softmax threads
-// into shared memory as the K-major B operand.  The kernel is HBM-bound: a
-// 3-stage (dense) or 6-stage (scores, K only) ring of 32 KB TMA tile loads
-// keeps ~100-200 KB in flight per SM.
+// into shared memory as the K-major B operand.  The kernel is HBM-bound:
+// 3 K + 3 V slots (dense) or 6 K slots (scores) of 32 KB TMA tile loads keep
+// up to 192 KB in flight per SM; a K slot frees when S^T retires, a V slot
+// when PV does.
 //
-// Roles (192 threads): warp 0 lane 0 issues TMA, warp 1 lane 0 issues MMAs
-// (warp 1 owns the TMEM allocation), warps 2-5 are the softmax / epilogue
-// threads (TMEM lane quarters 2, 3, 0, 1).  Per key block j:
+// Roles (224 threads): warp 0 lane 0 issues the Q and K loads, warp 6 lane 0
+// the V loads, warp 1 lane 0 the MMAs (warp 1 owns the TMEM allocation),
+// warps 2-5 are the softmax / epilogue threads (TMEM lane quarters 2, 3, 0,
+// 1).  Per key block j:
 //
 //   MMA:      S^T_j -> TMEM buffer j&1 ; then PV_{j-1} (after P_{j-1})
-//   softmax:  load S^T_j, block max per head (warp shuffles + 4-warp smem),
-//             lazy rescale of O^T (only when the max grows by > 2^8),
-//             p = exp2(s - m), per-thread l partials, P^T_j -> smem buffer j&1
+//   softmax:  load S^T_j; one OR vote whether any key exceeds the running
+//             reference by > 2^8 -- only then the CTA-wide block max (warp
+//             shuffles + 4-warp smem) and a rescale of O^T in TMEM;
+//             p = exp2(s - m), P^T_j (bf16) -> smem buffer j&1
+//   score pass (no V): every thread keeps its own lazy reference (no
+//             barrier), merged per head in the epilogue
 //
-// Split-K over the keys of a (sequence, kv head) and the last-CTA merge use
-// the same workspace layout as decode.cu, so every decode kernel shares the
-// executor's workspace.
+// Work split ("stream-K"): a layer's (sequence, kv head, 128-key block)
+// space is cut into equal contiguous ranges, 4 waves of CTAs per layer.  A
+// CTA streams its range without draining at pair boundaries (Q of each pair
+// by TMA into a segment-parity buffer, O^T double-buffered in TMEM); each
+// pair it touches is a segment whose partial (m, l, O / l_bf16) goes to the
+// executor's split-K workspace, and the last segment of a pair to finish
+// merges them in slot order (deterministic; a layer's ranges do not depend
+// on how many layers share the launch).  O is normalised by the sum of the
+// bf16-rounded weights the MMA multiplied, the LSE by the fp32 sum.
 #include "sm100.cuh"
 #include "kscd_internal.h"
 
@@ -39,21 +51,29 @@ using namespace sm100;
 namespace dtc {
 constexpr int kBlk = 128;                 // keys per block = UMMA M
 constexpr int kN = 16;                    // UMMA N: the group's heads, padded
-constexpr int kThreads = 224;          // 7 warps: K/Q TMA, MMA, 4 softmax, V TMA
+constexpr int kThreads = 224;             // 7 warps: K/Q TMA, MMA, 4 softmax, V TMA
 constexpr int kTile = kBlk * 256;         // one K or V block, 32 KB
 constexpr int kHalf = kBlk * 128;         // one 64-column half of a block
 constexpr int kQBytes = 2 * kN * 128;     // Q of a group: [2 halves][16 rows][128 B]
 constexpr int kMaxSplits = 64;
-constexpr int kCtas = 148;                // one persistent CTA per SM
+// CTAs per layer: 4 waves of one CTA per SM (the block scheduler balances
+// SMs of unequal speed).  Measured at 128K b8, chained: 1 wave +4 %, 6 / 8 /
+// 12 waves +0 / +0.5 / +1.4 %; a persistent grid fed by an atomic chunk
+// queue (+4 %) and a two-phase split with small tail CTAs (+4 %) were slower.
+constexpr int kCtas = 4 * 148;
 constexpr uint32_t kIdescS = idesc_bf16(128, kN, false, false);   // A = K (K-major), B = Q (K-major)
 constexpr uint32_t kIdescO = idesc_bf16(128, kN, true, false);    // A = V^T (MN-major), B = P^T (K-major)
 constexpr float kRescale = 8.0f;          // log2 units
 
 template <bool HAS_V>
 struct Cfg {
-  static constexpr int kStages = HAS_V ? 3 : 6;
-  static constexpr int kStageBytes = HAS_V ? 2 * kTile : kTile;
-  static constexpr int kOffQ = kStages * kStageBytes;      // 2 segment buffers of kQBytes
+  // K slots free when S^T retires, V slots only when PV does (a 2 / 4
+  // split measured the same as 3 / 3)
+  static constexpr int kSK = HAS_V ? 3 : 6;
+  static constexpr int kSV = HAS_V ? 3 : 0;
+  static constexpr int kStages = kSK > kSV ? kSK : kSV;    // barrier slots
+  static constexpr int kOffV = kSK * kTile;
+  static constexpr int kOffQ = (kSK + kSV) * kTile;        // 2 segment buffers of kQBytes
   static constexpr int kOffP = kOffQ + 2 * kQBytes;        // 2 block buffers of P^T [2 halves][16][128 B]
   static constexpr int kOffRed = kOffP + 8192;             // float [2][4 warps][16] block max
   static constexpr int kOffSum = kOffRed + 2 * 4 * 16 * 4; // float [4][16] l, [4][16] l (bf16 p), [16] m
@@ -64,13 +84,8 @@ struct Cfg {
   static constexpr int kSmem = kOffTmem + 16 + 1024;
 };
 
-// The launch's work is a flat space of 128-key blocks,
-//   f = ((layer * B + b) * Hkv + g) * nblk + j,
-// cut into equal contiguous ranges, one per CTA ("stream-K"): a CTA streams
-// its range through ONE TMA ring without draining between (sequence, kv
-// head) pairs, and each pair it touches is a segment whose partial (m, l, O)
-// it writes; the last segment of a pair to finish merges them.  Blocks past
-// a ragged sequence's length are skipped.
+// A layer's work is a flat space of 128-key blocks f = (b * Hkv + g) * nblk
+// + j (see the header); blocks past a ragged sequence's length are skipped.
 struct Walk {
   int nblk, P, Hkv, n;
   const int* lens;
@@ -138,7 +153,7 @@ __global__ void __launch_bounds__(dtc::kThreads, 1)
   using namespace dtc;
   constexpr bool HAS_V = MODE == MODE_DENSE;
   using C = Cfg<HAS_V>;
-  constexpr int S = C::kStages;
+  constexpr int S = C::kSK, SV = C::kSV > 0 ? C::kSV : 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
@@ -153,7 +168,7 @@ __global__ void __launch_bounds__(dtc::kThreads, 1)
   uint64_t* o_done = s_full + 12;
   uint64_t* o_free = s_full + 14;
   uint64_t* vfull = s_full + 16;
-  uint64_t* vempty = vfull + S;
+  uint64_t* vempty = vfull + C::kStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffTmem);
   int* flag = reinterpret_cast<int*>(smem + C::kOffTmem + 8);
   float* red = reinterpret_cast<float*>(smem + C::kOffRed);
@@ -166,18 +181,16 @@ __global__ void __launch_bounds__(dtc::kThreads, 1)
   const int nblk = w.nblk;
   // Every layer's block space is cut identically into ranges of `per`
   // blocks (a layer's result does not depend on how many layers share the
-  // launch); CTA c streams range c of each layer in turn, so the ring never
-  // drains between layers.  Its pairs (segments) are, per layer, the
-  // layer-local pairs [pl0, pl0 + npl), each over blocks [jb, je).
-  const int cta = blockIdx.x;
+  // launch): CTA (layer, c) streams range c of that layer -- 4 waves of one
+  // CTA per SM, so the block scheduler balances SMs of unequal speed.  Its
+  // pairs (segments) are the layer-local pairs [pl0, pl0 + nv), each over
+  // blocks [jb, je).
+  const int cpl = (P * nblk + per - 1) / per;
+  const int lyr_c = blockIdx.x / cpl, cta = blockIdx.x - lyr_c * cpl;
   const int T1 = P * nblk;
   const int g0 = cta * per, g1 = min(T1, g0 + per);
-  const int pl0 = g0 / nblk, npl = (g1 + nblk - 1) / nblk - pl0;
-  const int nv = a.nl * npl;
-  auto pair_of = [&](int v) {
-    const int lc = v / npl;
-    return lc * P + pl0 + (v - lc * npl);
-  };
+  const int pl0 = g0 / nblk, nv = (g1 + nblk - 1) / nblk - pl0;
+  auto pair_of = [&](int v) { return lyr_c * P + pl0 + v; };
   auto seg_range = [&](int pair, int& jb, int& je) {
     const int pl = pair % P;
     jb = max(g0 - pl * nblk, 0);
@@ -232,7 +245,7 @@ __global__ void __launch_bounds__(dtc::kThreads, 1)
           const int st = i % S;
           if (i >= S) mbar_wait(&empty[st], ((i / S) - 1) & 1);
           mbar_expect_tx(&full[st], kTile);
-          uint8_t* dst = smem + st * C::kStageBytes;
+          uint8_t* dst = smem + st * kTile;
           for (int hf = 0; hf < 2; ++hf) tma_load_4d(dst + hf * kHalf, kmap, &full[st], hf * 64, j * kBlk, gk, b);
         }
         ++s;
@@ -245,12 +258,12 @@ __global__ void __launch_bounds__(dtc::kThreads, 1)
       const uint32_t paddr = smem_u32(smem + C::kOffP);
       // O^T_seg += V_ii^T P_ii^T
       auto issue_pv = [&](int ii, int seg, bool first, bool last) {
-        const int pb = ii & 1, ob = seg & 1, st = ii % S;
+        const int pb = ii & 1, ob = seg & 1, st = ii % SV;
         if (first && seg >= 2) mbar_wait(&o_free[ob], ((seg - 2) >> 1) & 1);
-        mbar_wait(&vfull[st], (ii / S) & 1);
+        mbar_wait(&vfull[st], (ii / SV) & 1);
         mbar_wait(&p_full[pb], (ii >> 1) & 1);
         tc_fence_after();
-        const uint32_t vaddr = smem_u32(smem + st * C::kStageBytes + kTile);
+        const uint32_t vaddr = smem_u32(smem + C::kOffV + st * kTile);
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks)
           mma_ss(tmem + 32 + ob * 16, sw128_desc(vaddr + ks * 2048, kHalf, 1024),
@@ -274,7 +287,7 @@ __global__ void __launch_bounds__(dtc::kThreads, 1)
           mbar_wait(&full[st], (i / S) & 1);
           if (i >= 2) mbar_wait(&s_free[sb], ((i - 2) >> 1) & 1);
           tc_fence_after();
-          const uint32_t kaddr = smem_u32(smem + st * C::kStageBytes);
+          const uint32_t kaddr = smem_u32(smem + st * kTile);
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks) {
             const uint32_t off = (ks >> 2) * kHalf + (ks & 3) * 32;
@@ -306,10 +319,10 @@ __global__ void __launch_bounds__(dtc::kThreads, 1)
         const int gk = g / a.kv_rep;
         const CUtensorMap* vmap = &tm.v[lyr];
         for (int j = jb; j < je; ++j, ++i) {
-          const int st = i % S;
-          if (i >= S) mbar_wait(&vempty[st], ((i / S) - 1) & 1);
+          const int st = i % SV;
+          if (i >= SV) mbar_wait(&vempty[st], ((i / SV) - 1) & 1);
           mbar_expect_tx(&vfull[st], kTile);
-          uint8_t* dst = smem + st * C::kStageBytes + kTile;
+          uint8_t* dst = smem + C::kOffV + st * kTile;
           for (int hf = 0; hf < 2; ++hf) tma_load_4d(dst + hf * kHalf, vmap, &vfull[st], hf * 64, j * kBlk, gk, b);
         }
       }
@@ -424,8 +437,8 @@ __global__ void __launch_bounds__(dtc::kThreads, 1)
           if (!valid) {
             // a key past this sequence's length (ragged batch): its V row may
             // hold anything (NaN * 0 would poison O); zero it before PV reads it
-            mbar_wait(&vfull[i % S], (i / S) & 1);
-            uint8_t* vrow = smem + (i % S) * C::kStageBytes + kTile + kin * 128;
+            mbar_wait(&vfull[i % SV], (i / SV) & 1);
+            uint8_t* vrow = smem + C::kOffV + (i % SV) * kTile + kin * 128;
 #pragma unroll
             for (int c = 0; c < 8; ++c) reinterpret_cast<uint4*>(vrow)[c] = make_uint4(0, 0, 0, 0);
 #pragma unroll
@@ -708,7 +721,7 @@ cudaError_t launch_decode_tc(int mode, const DecodeArgs& a_in, const void* const
     int64_t per = (T1 + dtc::kCtas - 1) / dtc::kCtas;
     per = std::max<int64_t>(per, (nblk - 1 + a.splits - 2) / (a.splits - 1));
     per = std::max<int64_t>(per, 1);
-    const int nctas = (int)((T1 + per - 1) / per);
+    const int nctas = (int)((T1 + per - 1) / per) * m;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nctas);
     cfg.blockDim = dim3(dtc::kThreads);
