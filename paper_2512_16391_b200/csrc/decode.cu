@@ -1,19 +1,14 @@
-// Split-K decode attention for Kascade (one query token per sequence).
+// Split-K sparse decode attention for Kascade (one query token per
+// sequence): keys idx[b][map[g]][0..cnt) -- reuse layers through the head
+// remap table, and anchors over their own fresh sets (topk_attention on a
+// decode tile, attention.py:185-253; runner.py:210-225).  The dense and
+// anchor score passes stream contiguous keys and run on the tcgen05 / TMA
+// kernel (decode_tc.cu); a gather of 256-B rows at random positions has no
+// TMA tile shape, so this one stays on cp.async + mma.sync.
 //
-// One kernel template covers the three decode layer kinds:
-//   MODE_DENSE   keys 0..n-1 of kv head g   (dense baseline and anchor-0;
-//                optionally emits the log2-domain scores the anchor-0
-//                selection pools)                    attention.py:106-144
-//   MODE_SPARSE  keys idx[b][map[g]][0..cnt) (reuse layers through the head
-//                remap table, and anchors over their own fresh sets)
-//                                                    attention.py:185-253,
-//                                                    runner.py:210-225
-//   MODE_SCORES  QK^T only: scores + LSE, V is never read (anchor pass 1)
-//
-// Grid = (splits, Hkv, B); 4 warps per CTA.  K/V rows (256 B each) stream
-// through a cp.async (LDGSTS) ring of 64-key tiles -- contiguous rows for the
-// dense modes, gathered rows for the sparse mode -- XOR-swizzled so the
-// ldmatrix reads are bank-conflict free.  Each warp owns 16 keys of a tile
+// Grid = (splits, Hkv, B x layers); 4 warps per CTA.  Gathered K/V rows
+// (256 B each) stream through a cp.async (LDGSTS) ring of 64-key tiles,
+// XOR-swizzled so the ldmatrix reads are bank-conflict free.  Each warp owns 16 keys of a tile
 // and keeps its own online-softmax state for the G query heads of the group
 // (G <= 16 rows of one m16n8k16 tile), so there is no CTA barrier per tile
 // beyond the ring's.  Partial (m, l, O) of the 4 warps are merged in shared
@@ -31,24 +26,21 @@ constexpr int kMaxSplitsDev = 64;   // = capi.cu kMaxSplits (the workspace and m
 constexpr int kThreads = 128;
 constexpr int kTileBytes = kTileKeys * kRowBytes;  // 16 KB
 
-// STG = ring depth (0 = default: 3 with V, 5 K-only).  Rings of >= 5 stages
-// with V run one CTA per SM.
-template <int MODE, int STG = 0>
 struct DecodeCfg {
-  static constexpr bool kHasV = MODE != MODE_SCORES;
-  static constexpr int kStages = STG ? STG : (kHasV ? 3 : 5);
-  static constexpr int kStageBytes = kHasV ? 2 * kTileBytes : kTileBytes;
+  static constexpr bool kHasV = true;
+  static constexpr int kStages = 3;
+  static constexpr int kStageBytes = 2 * kTileBytes;
   static constexpr int kPipeBytes = kStages * kStageBytes;
   // merge scratch reuses the ring: 4 warps x 16 rows x (128 + 2) floats
   static constexpr int kMergeBytes = 4 * 16 * (kHeadDim + 2) * 4;
   static constexpr int kSmemBytes = kPipeBytes > kMergeBytes ? kPipeBytes : kMergeBytes;
-  static constexpr int kMinBlocks = (kHasV && kStages >= 5) ? 1 : 2;
+  static constexpr int kMinBlocks = 2;
 };
 
-template <int MODE, bool G16, int STG>
-__global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
+template <bool G16>
+__global__ void __launch_bounds__(kThreads, DecodeCfg::kMinBlocks)
     decode_attn_kernel(const DecodeArgs a) {
-  using Cfg = DecodeCfg<MODE, STG>;
+  using Cfg = DecodeCfg;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int split = blockIdx.x, g = blockIdx.y;                     // g: (virtual) head group
   const int lyr = blockIdx.z / a.B, b = blockIdx.z - lyr * a.B;        // layer of a multi-layer launch
@@ -66,7 +58,6 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
   float* part_l = reinterpret_cast<float*>(reinterpret_cast<char*>(a.part) + (int64_t)lyr * a.ws_ls);
   float* part_ml_l = reinterpret_cast<float*>(reinterpret_cast<char*>(a.part_ml) + (int64_t)lyr * a.ws_ls);
   int* counters_l = reinterpret_cast<int*>(reinterpret_cast<char*>(a.counters) + (int64_t)lyr * a.ws_ls);
-  float* scores_l = a.scores ? a.scores + (int64_t)lyr * a.scores_ls : nullptr;
   float* lse_l = a.lse ? a.lse + (int64_t)lyr * a.lse_ls : nullptr;
 
   const __nv_bfloat16* kbase = k_l + (int64_t)b * a.kv_sb + (int64_t)gk * a.kv_sh;
@@ -82,7 +73,7 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
   // it writes out / lse) waits for the previous grid.
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   int count = a.lens ? min(__ldg(a.lens + b), a.n) : a.n;
-  if (MODE == MODE_SPARSE) {
+  {
     const int src = hm_l ? __ldg(hm_l + gk) : gk;
     sel = a.idx + (int64_t)lyr * a.idx_ls + (int64_t)b * a.idx_sb + (int64_t)src * a.idx_sh;
     count = min(__ldg(a.cnt + (int64_t)lyr * a.cnt_ls + (int64_t)b * a.cnt_sb + src), a.k_cap);
@@ -126,7 +117,7 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int kk = key0 + my_row0 + 8 * i;
-      pos_next[i] = (MODE == MODE_SPARSE) ? ((t < my_tiles && kk < count) ? __ldg(sel + kk) : 0) : kk;
+      pos_next[i] = (t < my_tiles && kk < count) ? __ldg(sel + kk) : 0;
     }
   };
   auto issue_tile = [&](int t, int stage) {
@@ -200,26 +191,13 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
         mma_bf16_16816(s[nt], qa0[2 * j + 1], qa1[2 * j + 1], qa2[2 * j + 1], qa3[2 * j + 1], b2, b3);
       }
     }
-    // scale to log2 domain, mask keys past the list, optionally emit scores
+    // scale to log2 domain, mask keys past the list
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int kk = key_w + nt * 8 + 2 * tig + (c & 1);
         s[nt][c] = kk < count ? s[nt][c] * a.scale_log2 : -INFINITY;
-      }
-      if (MODE != MODE_SPARSE && scores_l != nullptr) {
-        const int kk = key_w + nt * 8 + 2 * tig;
-        if (gid < G && kk < count) {
-          float* dst = scores_l + ((int64_t)b * a.Hq + g * G + gid) * a.score_stride + kk;
-          if (kk + 1 < count) *reinterpret_cast<float2*>(dst) = make_float2(s[nt][0], s[nt][1]);
-          else dst[0] = s[nt][0];
-        }
-        if (G16 && gid + 8 < G && kk < count) {
-          float* dst = scores_l + ((int64_t)b * a.Hq + g * G + gid + 8) * a.score_stride + kk;
-          if (kk + 1 < count) *reinterpret_cast<float2*>(dst) = make_float2(s[nt][2], s[nt][3]);
-          else dst[0] = s[nt][2];
-        }
       }
     }
     // online softmax per head row (quad-reduced max, thread-partial sum)
@@ -395,16 +373,15 @@ __global__ void __launch_bounds__(kThreads, DecodeCfg<MODE, STG>::kMinBlocks)
   }
 }
 
-template <int MODE, int STG = 0>
-static cudaError_t launch_mode(const DecodeArgs& a, cudaStream_t st) {
-  using Cfg = DecodeCfg<MODE, STG>;
+static cudaError_t launch_sparse(const DecodeArgs& a, cudaStream_t st) {
+  using Cfg = DecodeCfg;
   dim3 grid(a.splits, a.Hkv, a.B * (a.nl > 0 ? a.nl : 1));
   const int smem = Cfg::kSmemBytes;
   // one-time opt-in to >48 KB dynamic shared memory per instantiation
   static const cudaError_t attr_hi = cudaFuncSetAttribute(
-      decode_attn_kernel<MODE, true, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      decode_attn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   static const cudaError_t attr_lo = cudaFuncSetAttribute(
-      decode_attn_kernel<MODE, false, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      decode_attn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (attr_hi != cudaSuccess) return attr_hi;
   if (attr_lo != cudaSuccess) return attr_lo;
   // programmatic stream serialization (see the kernel's PDL note)
@@ -418,14 +395,14 @@ static cudaError_t launch_mode(const DecodeArgs& a, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (a.G > 8) return cudaLaunchKernelEx(&cfg, decode_attn_kernel<MODE, true, STG>, a);
-  return cudaLaunchKernelEx(&cfg, decode_attn_kernel<MODE, false, STG>, a);
+  if (a.G > 8) return cudaLaunchKernelEx(&cfg, decode_attn_kernel<true>, a);
+  return cudaLaunchKernelEx(&cfg, decode_attn_kernel<false>, a);
 }
 
 cudaError_t launch_decode_attn(int mode, const DecodeArgs& a, cudaStream_t st) {
   // the dense and score passes run on the tcgen05 / TMA kernel (decode_tc.cu)
   if (mode != MODE_SPARSE) return cudaErrorInvalidValue;
-  return launch_mode<MODE_SPARSE>(a, st);
+  return launch_sparse(a, st);
 }
 
 int decode_tile_keys() { return kTileKeys; }
