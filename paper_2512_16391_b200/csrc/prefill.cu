@@ -277,14 +277,32 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
       // Cp.async groups retire in order K_0, V_0, K_1, V_1, ...: K_j is
       // gathered as soon as S_{j-2} released its half-stage and is published
       // first; V_{j-1} is published while K_j is in flight.
-      auto gather = [&](uint32_t dst, const __nv_bfloat16* src, const int* pos) {
-#pragma unroll 2
-        for (int c = pt; c < 128 * 16; c += 96) {
-          const int r = c >> 4, ch = c & 15;
-          const int p = pos[r];
-          const bool valid = p != 0x7fffffff;
-          const uint32_t off = (ch >> 3) * kHalf + r * 128 + (((ch & 7) ^ (r & 7)) << 4);
-          cp_async16_zfill(dst + off, src + (int64_t)(valid ? p : 0) * 128 + ch * 8, valid);
+      // 128 rows x 16 chunks over 96 threads: thread pt always copies chunk
+      // pt % 16 (96 is a multiple of 16) of rows pt / 16 + 6 i.  Its <= 22
+      // positions are read from shared memory once per block, all loads in
+      // flight together, and reused by the K and the V gather -- a position
+      // load per copy (dependent LDS -> address -> LDGSTS) was the gather's
+      // dominant stall (ncu: short scoreboard; 14.3 -> 12.6 ms at 128K).
+      constexpr int kRowsPer = (kBlockN + 5) / 6;               // 22
+      const int gch = pt & 15, grow0 = pt >> 4;
+      int prow[kRowsPer];
+      auto load_rows = [&](const int* pos) {
+#pragma unroll
+        for (int i = 0; i < kRowsPer; ++i) {
+          const int r = grow0 + 6 * i;
+          prow[i] = r < kBlockN ? pos[r] : 0x7fffffff;
+        }
+      };
+      auto gather = [&](uint32_t dst, const __nv_bfloat16* src) {
+#pragma unroll
+        for (int i = 0; i < kRowsPer; ++i) {
+          const int r = grow0 + 6 * i;
+          if (r < kBlockN) {
+            const int p = prow[i];
+            const bool valid = p != 0x7fffffff;
+            const uint32_t off = (gch >> 3) * kHalf + r * 128 + (((gch & 7) ^ (r & 7)) << 4);
+            cp_async16_zfill(dst + off, src + (int64_t)(valid ? p : 0) * 128 + gch * 8, valid);
+          }
         }
         cp_async_commit();
       };
@@ -297,14 +315,15 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
         if (r1 < kBlockN) pos[r1] = p1;
         if (j + 1 < nb) load_sel(j + 1, p0, p1);
         named_bar_sync(1, 96);
-        gather(smem_u32(smem + kOffK + st * kTileBytes), kg, pos);
+        load_rows(pos);
+        gather(smem_u32(smem + kOffK + st * kTileBytes), kg);
         if (j > 0) {                                              // V_{j-1} landed
           cp_async_wait<1>();
           fence_proxy_async_smem();
           mbar_arrive(&bars[3 + (j - 1) % kStages]);
         }
         if (j >= kStages) mbar_wait(&bars[5 + st], ph_free);     // V half free (PV_{j-2} retired)
-        gather(smem_u32(smem + kOffV + st * kTileBytes), vg, pos);
+        gather(smem_u32(smem + kOffV + st * kTileBytes), vg);
         cp_async_wait<1>();                                       // K_j landed
         fence_proxy_async_smem();
         mbar_arrive(&bars[1 + st]);
