@@ -155,21 +155,24 @@ class KascadeDecoder:
 
     def _run_range(self, l0: int, l1: int, q, k_caches, v_caches, seq_len: int, dense: bool = False) -> None:
         """Layers [l0, l1): every run of consecutive reuse layers (every
-        layer in dense mode) is one multi-layer launch; anchors run alone."""
+        layer in dense mode) is one multi-layer launch; an anchor (or a group
+        of consecutive anchors) runs its score passes and its selection, then
+        its own sparse passes AND the reuse run that follows it -- they all
+        read the anchor's fresh lists -- as one more launch."""
         l = l0
         while l < l1:
             if not dense and self.kinds[l] == KIND_ANCHOR and not self.pre and self.seq_lens is None:
                 e = min(self.group_end[l], l1)
-                if e - l >= 2:
-                    self._anchor_group(l, e, q, k_caches, v_caches, seq_len)
-                    l = e
+                end = min(self.run_end[e], l1) if e < l1 and self.kinds[e] == KIND_REUSE else e
+                if end - l >= 2 and self._fusable(k_caches, v_caches, l, end):
+                    self._anchor_group(l, e, end, q, k_caches, v_caches, seq_len)
+                    l = end
                     continue
             end = l1 if dense else (min(self.run_end[l], l1) if self.kinds[l] == KIND_REUSE else l + 1)
             # one launch needs one cache layout; dense layers of a ragged batch
             # run per layer (the multi-layer launch has no per-sequence lengths)
-            fuse = end - l >= 2 and not (dense and self.seq_lens is not None) and all(
-                t.shape == k_caches[l].shape and t.stride() == k_caches[l].stride()
-                for t in list(k_caches[l:end]) + list(v_caches[l:end]))
+            fuse = end - l >= 2 and not (dense and self.seq_lens is not None) and \
+                self._fusable(k_caches, v_caches, l, end)
             if fuse:
                 ops.decode_layers(q[l:end], k_caches[l:end], v_caches[l:end], seq_len, out=self.out[l:end],
                                   workspace=self.ws_layers, tables=self._layer_tables(k_caches, v_caches, l, end),
@@ -180,10 +183,17 @@ class KascadeDecoder:
                     (self._dense_layer if dense else self._layer)(i, q, k_caches, v_caches, seq_len)
             l = end
 
+    @staticmethod
+    def _fusable(k_caches, v_caches, l: int, end: int) -> bool:
+        ref = k_caches[l]
+        return all(t.shape == ref.shape and t.stride() == ref.stride() for t in list(k_caches[l:end]) +
+                   list(v_caches[l:end]))
+
     def launches_per_step(self, dense: bool = False) -> int:
         """Kernel launches of one step() (post-softmax pooling, uniform batch):
         anchor 0 = dense + pool + Top-k; an anchor or a group of consecutive
-        anchors = scores + pool + Top-k + sparse; a reuse run = one launch."""
+        anchors = scores + pool + Top-k + one sparse launch that also runs the
+        reuse run behind it; any other reuse run = one launch."""
         if dense:
             return 1
         n, l = 0, 0
@@ -192,31 +202,59 @@ class KascadeDecoder:
             if kind == KIND_ANCHOR0:
                 n, l = n + 3, l + 1
             elif kind == KIND_ANCHOR:
-                n, l = n + 4, self.group_end[l]
+                e = self.group_end[l]
+                n, l = n + 4, (self.run_end[e] if e < self.L and self.kinds[e] == KIND_REUSE else e)
             else:
                 n, l = n + 1, self.run_end[l]
         return n
 
-    def _anchor_group(self, l0: int, l1: int, q, k_caches, v_caches, seq_len: int) -> None:
+    def _fused_maps(self, l0: int, l1: int, end: int) -> torch.Tensor:
+        """Head-map table of the sparse launch over [l0, end) that follows the
+        selection of anchors [l0, l1): anchor l0 + i reads its own lists in
+        slot m - 1 - i of idx_g / cnt_g -- a map entry may address any row of
+        the [slots][B][Hsrc] list space, so slot s of source head h is row
+        s * B * Hsrc + h -- and the reuse layers read slot 0 (the last
+        anchor's lists) through their own maps.  Built on the eager warm-up,
+        looked up inside graph captures."""
+        key = ("maps", l0, l1, end)
+        t = self._tables.get(key)
+        if t is None:
+            if torch.cuda.is_current_stream_capturing():
+                raise InvalidArgumentError("new launch layout inside a CUDA graph capture: run the step eagerly first")
+            m, Hs = l1 - l0, self.indices.shape[1]
+            own = torch.zeros(self.Hkv, dtype=torch.int32, device=self.device) if self.all_heads else \
+                torch.arange(self.Hkv, dtype=torch.int32, device=self.device)
+            rows = [own + (m - 1 - i) * self.B * Hs for i in range(m)]
+            rows += [self.map_table[l] for l in range(l1, end)]
+            t = self._tables[key] = torch.stack(rows).contiguous()
+        return t
+
+    def _anchor_group(self, l0: int, l1: int, end: int, q, k_caches, v_caches, seq_len: int) -> None:
         """Consecutive anchor layers [l0, l1) as three launches: their score
         passes, one select over all their (sequence, kv head) rows, and their
-        sparse passes over their own fresh sets (runner.py:263-266).  Layer
-        l0 + i uses slot m - 1 - i, so the last anchor's lists land in slot 0."""
+        sparse passes over their own fresh sets (runner.py:263-266) together
+        with the reuse layers [l1, end) over the last anchor's sets routed by
+        their head maps (runner.py:267-275).  Layer l0 + i uses slot m - 1 - i,
+        so the last anchor's lists land in slot 0 (self.indices)."""
         m = l1 - l0
         B, Hq = self.B, self.Hq
         Hs = self.indices.shape[1]
-        tabs = self._layer_tables(k_caches, v_caches, l0, l1)
-        sc_ls = self.scores_g.stride(0) * B
-        ops.decode_layers(q[l0:l1], k_caches[l0:l1], v_caches[l0:l1], seq_len, workspace=self.ws_layers, tables=tabs,
-                          scores=self.scores_g[(m - 1) * B:m * B], scores_layer_stride=-sc_ls,
-                          lse=self.lse_g[(m - 1) * B:m * B], lse_layer_stride=-B * Hq)
-        ops.select_decode(self.scores_g[:m * B], self.lse_g[:m * B], seq_len, self.plan.k_policy, self.Hkv,
-                          indices=self.idx_g[:m].view(m * B, Hs, -1), counts=self.cnt_g[:m].view(m * B, Hs),
-                          pooled=self.pooled_g[:m * B * Hs], all_heads=self.all_heads)
-        ops.decode_layers(q[l0:l1], k_caches[l0:l1], v_caches[l0:l1], seq_len, out=self.out[l0:l1],
-                          workspace=self.ws_layers, tables=tabs, indices=self.idx_g[m - 1], counts=self.cnt_g[m - 1],
-                          index_layer_stride=-self.idx_g.stride(0), count_layer_stride=-self.cnt_g.stride(0),
-                          head_maps=self.zero_maps[:m] if self.all_heads else None)
+        if m == 1:
+            ops.anchor_scores_decode(q[l0], k_caches[l0], seq_len, self.scores, self.lse, workspace=self.ws)
+            ops.select_decode(self.scores, self.lse, seq_len, self.plan.k_policy, self.Hkv, indices=self.indices,
+                              counts=self.counts, pooled=self.pooled, all_heads=self.all_heads)
+        else:
+            tabs = self._layer_tables(k_caches, v_caches, l0, l1)
+            sc_ls = self.scores_g.stride(0) * B
+            ops.decode_layers(q[l0:l1], k_caches[l0:l1], v_caches[l0:l1], seq_len, workspace=self.ws_layers,
+                              tables=tabs, scores=self.scores_g[(m - 1) * B:m * B], scores_layer_stride=-sc_ls,
+                              lse=self.lse_g[(m - 1) * B:m * B], lse_layer_stride=-B * Hq)
+            ops.select_decode(self.scores_g[:m * B], self.lse_g[:m * B], seq_len, self.plan.k_policy, self.Hkv,
+                              indices=self.idx_g[:m].view(m * B, Hs, -1), counts=self.cnt_g[:m].view(m * B, Hs),
+                              pooled=self.pooled_g[:m * B * Hs], all_heads=self.all_heads)
+        ops.decode_layers(q[l0:end], k_caches[l0:end], v_caches[l0:end], seq_len, out=self.out[l0:end],
+                          workspace=self.ws_layers, tables=self._layer_tables(k_caches, v_caches, l0, end),
+                          indices=self.indices, counts=self.counts, head_maps=self._fused_maps(l0, l1, end))
 
     def _layer(self, l: int, q, k_caches, v_caches, seq_len: int) -> None:
         """The kernels of layer l (runner.py:250-275 for one decode token)."""

@@ -213,6 +213,33 @@ def test_select_decode_matches_oracle(cuda_ok):
     assert swaps <= 2
 
 
+@pytest.mark.parametrize("B,Hq,Hkv,n,all_heads", [(2, 32, 8, 50000, False), (3, 16, 1, 20000, False),
+                                                 (2, 32, 8, 30000, True), (1, 8, 2, 3000, False)])
+def test_select_decode_fused_pooling(cuda_ok, B, Hq, Hkv, n, all_heads):
+    """The pooling runs inside the Top-k's first pass: the pooled buffer it
+    writes is sum_i exp2(s_i - lse_i log2 e) over the row's heads, and the
+    lists equal a plain Top-k over that buffer (bit-exact)."""
+    from paper_2512_16391_b200 import ops
+    from paper_2512_16391_b200.host_types import KBudgetPolicy
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q = (torch.randn(B, Hq, 128, device="cuda", generator=g) * 2).to(torch.bfloat16)
+    K = torch.randn(B, Hkv, n, 128, device="cuda", generator=g).to(torch.bfloat16)
+    V = torch.randn(B, Hkv, n, 128, device="cuda", generator=g).to(torch.bfloat16)
+    sc = ops.score_buffer(B, Hq, n, "cuda")
+    _, lse = ops.dense_decode(q, K, V, n, scores=sc)
+    pol = KBudgetPolicy(0.1, 128)
+    Hs = 1 if all_heads else Hkv
+    pooled = torch.full((B * Hs, (n + 3) // 4 * 4), float("nan"), device="cuda")
+    idx, cnt = ops.select_decode(sc, lse, n, pol, Hkv, pooled=pooled, all_heads=all_heads)
+    G = Hq // Hs
+    w = torch.exp2(sc[:, :, :n] - (lse * 1.4426950408889634)[:, :, None]).reshape(B * Hs, G, n).sum(1)
+    torch.testing.assert_close(pooled[:, :n], w, rtol=2e-6, atol=1e-12)
+    k = int(cnt.flatten()[0])
+    ridx, rcnt = ops.topk(pooled[:, :n].contiguous(), k)
+    assert torch.equal(idx.view(B * Hs, -1)[:, :k], ridx[:, :k])
+    assert torch.equal(cnt.flatten(), rcnt)
+
+
 def _config1():
     import json
     import os
@@ -317,12 +344,23 @@ def test_multi_layer_launches_equal_per_layer(cuda_ok):
     maps = {1: HeadMap(1, 0, [3, 2, 1, 0]), 5: HeadMap(5, 4, [1, 0, 3, 2]), 6: HeadMap(6, 4, [0, 0, 1, 1]),
             7: HeadMap(7, 4, [2, 3, 0, 1])}
     plan = AnchorPlan(AnchorPlanCore([0, 2, 3, 4], 4, 0.0), head_maps=maps, k_policy=KBudgetPolicy(0.1, 64))
+    _check_multi_layer(plan, L, B, Hq, Hkv, n)
+    assert engine.KascadeDecoder(plan, L, B, Hq, Hkv, n).launches_per_step() == 3 + 1 + 4
+    # a single anchor whose sparse pass shares a launch with the reuse run behind it
+    maps1 = {1: HeadMap(1, 0, [3, 2, 1, 0]), 2: HeadMap(2, 0, [0, 0, 1, 1]), 4: HeadMap(4, 3, [1, 0, 3, 2]),
+             5: HeadMap(5, 3, [2, 3, 0, 1]), 6: HeadMap(6, 3, [3, 3, 3, 3])}
+    plan1 = AnchorPlan(AnchorPlanCore([0, 3, 7], 3, 0.0), head_maps=maps1, k_policy=KBudgetPolicy(0.1, 64))
+    _check_multi_layer(plan1, L, B, Hq, Hkv, n)
+    assert engine.KascadeDecoder(plan1, L, B, Hq, Hkv, n).launches_per_step() == 3 + 1 + 4 + 4
+
+
+def _check_multi_layer(plan, L, B, Hq, Hkv, n):
+    from paper_2512_16391_b200 import engine
     g = torch.Generator(device="cuda").manual_seed(3)
     Ks = [torch.randn(B, Hkv, n, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(L)]
     Vs = [torch.randn(B, Hkv, n, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(L)]
     q = (torch.randn(L, B, Hq, 128, device="cuda", generator=g) * 2).to(torch.bfloat16)
     dec = engine.KascadeDecoder(plan, L, B, Hq, Hkv, n)
-    assert dec.run_end[5] == 8 and dec.run_end[1] == 2 and dec.group_end[2] == 5
     fused = dec.step(q, Ks, Vs, n).clone()
     lists = (dec.indices.clone(), dec.counts.clone())
     for l in range(L):
