@@ -34,7 +34,7 @@
 //             barrier), merged per head in the epilogue
 //
 // Work split ("stream-K"): a layer's (sequence, kv head, 128-key block)
-// space is cut into equal contiguous ranges, 4 waves of CTAs per layer.  A
+// space is cut into equal contiguous ranges, waves of CTAs per layer.  A
 // CTA streams its range without draining at pair boundaries (Q of each pair
 // by TMA into a segment-parity buffer, O^T double-buffered in TMEM); each
 // pair it touches is a segment whose partial (m, l, O / l_bf16) goes to the
@@ -56,11 +56,19 @@ constexpr int kTile = kBlk * 256;         // one K or V block, 32 KB
 constexpr int kHalf = kBlk * 128;         // one 64-column half of a block
 constexpr int kQBytes = 2 * kN * 128;     // Q of a group: [2 halves][16 rows][128 B]
 constexpr int kMaxSplits = 64;
-// CTAs per layer: 4 waves of one CTA per SM (the block scheduler balances
-// SMs of unequal speed).  Measured at 128K b8, chained: 1 wave +4 %, 6 / 8 /
-// 12 waves +0 / +0.5 / +1.4 %; a persistent grid fed by an atomic chunk
-// queue (+4 %) and a two-phase split with small tail CTAs (+4 %) were slower.
-constexpr int kCtas = 4 * 148;
+// CTAs per layer: waves of one CTA per SM (the block scheduler balances SMs
+// of unequal speed, and more, shorter CTAs let a launch's tail overlap the
+// next launch's start).  The score pass and single-layer dense launches
+// (anchor 0) use 16 waves per layer; the multi-layer dense launches (the
+// Top-k = 100 % baseline) 4 waves per layer.  A score pass's ranges (so its
+// LSE rounding) therefore never depend on how many layers share its launch;
+// a dense layer's do (split-K rounding only).  Measured in the 128K b8 decode step (same box, A/B): 4 / 6 / 8 /
+// 12 / 16 / 24 waves for the single-layer launches 573.9 / 568.4 / 565.6 /
+// 565.2 / 564.2 / 565.5 us/token, while the all-layer dense baseline launches
+// lose 2 % above 4 waves per layer; 1 wave and a persistent grid fed by an
+// atomic chunk queue were +4 % (round-2 history).
+constexpr int kWavesSingle = 16;
+constexpr int kWavesMultiDense = 4;
 constexpr uint32_t kIdescS = idesc_bf16(128, kN, false, false);   // A = K (K-major), B = Q (K-major)
 constexpr uint32_t kIdescO = idesc_bf16(128, kN, true, false);    // A = V^T (MN-major), B = P^T (K-major)
 constexpr float kRescale = 8.0f;          // log2 units
@@ -179,9 +187,9 @@ __global__ void __launch_bounds__(dtc::kThreads, 1)
   const int P = a.B * a.Hkv;
   const Walk w{(a.n + kBlk - 1) / kBlk, P, a.Hkv, a.n, a.lens};
   const int nblk = w.nblk;
-  // Every layer's block space is cut identically into ranges of `per`
-  // blocks (a layer's result does not depend on how many layers share the
-  // launch): CTA (layer, c) streams range c of that layer -- 4 waves of one
+  // Within a launch every layer's block space is cut identically into
+  // ranges of `per` blocks (see kWavesSingle for when the cut depends on the
+  // launch): CTA (layer, c) streams range c of that layer -- waves of one
   // CTA per SM, so the block scheduler balances SMs of unequal speed.  Its
   // pairs (segments) are the layer-local pairs [pl0, pl0 + nv), each over
   // blocks [jb, je).
@@ -718,7 +726,8 @@ cudaError_t launch_decode_tc(int mode, const DecodeArgs& a_in, const void* const
     const int64_t nblk = (a.n + dtc::kBlk - 1) / dtc::kBlk;
     const int64_t T1 = (int64_t)a.B * a.Hkv * nblk;
     if (T1 * m >= ((int64_t)1 << 31) || a.splits < 2) return cudaErrorInvalidValue;
-    int64_t per = (T1 + dtc::kCtas - 1) / dtc::kCtas;
+    const int64_t ctas_per_layer = (int64_t)(has_v && nl > 1 ? dtc::kWavesMultiDense : dtc::kWavesSingle) * 148;
+    int64_t per = (T1 + ctas_per_layer - 1) / ctas_per_layer;
     per = std::max<int64_t>(per, (nblk - 1 + a.splits - 2) / (a.splits - 1));
     per = std::max<int64_t>(per, 1);
     const int nctas = (int)((T1 + per - 1) / per) * m;

@@ -337,7 +337,8 @@ def test_multi_layer_launches_equal_per_layer(cuda_ok):
     group of consecutive anchors as one score launch + one select + one
     sparse launch over per-layer lists, and every dense layer as one launch
     in dense_step(); each layer's result (and the lists the reuse layers
-    read) is bit-identical to launching it alone."""
+    read) is bit-identical to launching it alone (the dense baseline: within
+    split-K merge rounding)."""
     from paper_2512_16391_b200 import engine
     from paper_2512_16391_b200.host_types import AnchorPlan, AnchorPlanCore, HeadMap, KBudgetPolicy
     L, B, Hq, Hkv, n = 8, 3, 16, 4, 5000
@@ -370,7 +371,9 @@ def _check_multi_layer(plan, L, B, Hq, Hkv, n):
     dfused = dec.dense_step(q, Ks, Vs, n).clone()
     for l in range(L):
         dec._dense_layer(l, q, Ks, Vs, n)
-    assert torch.equal(dec.out, dfused)
+    # the all-layer dense launch cuts each layer into fewer split-K ranges than
+    # a single-layer launch (decode_tc.cu kWavesMultiDense): merge rounding only
+    torch.testing.assert_close(dec.out, dfused, rtol=1e-5, atol=1e-6)
     # and through a CUDA graph
     graph = dec.capture(q, Ks, Vs, n)
     dec.out.zero_()
