@@ -121,6 +121,45 @@ class KascadeDecoder:
                                       self.head_maps[l].numel() == num_kv_heads else zeros
                                       for l in range(num_layers)]).contiguous()
         self.ws_layers = ops.new_decode_layers_workspace(dev, batch, num_q_heads, num_kv_heads, num_layers)
+        # Overlapped selection (step() on uniform batches, post-softmax
+        # pooling): every anchor group (consecutive anchors other than layer
+        # 0) runs its score pass and its selection on a side stream, ahead of
+        # the main stream's layer loop -- they depend only on the step's q and
+        # caches -- so the latency-bound pooled Top-k of one anchor overlaps
+        # the HBM-bound attention of other layers; the main stream waits for a
+        # group's lists right before the sparse launch that reads them.  Each
+        # group owns its scores / pooled / lists and the side stream its own
+        # split-K workspaces; the LAST group's lists are self.indices (what a
+        # step leaves behind, as in the per-layer path), layer 0's its own.
+        self.groups: List[tuple] = []
+        if not self.pre:
+            l = 1
+            while l < num_layers:
+                if self.kinds[l] == KIND_ANCHOR:
+                    self.groups.append((l, self.group_end[l]))
+                    l = self.group_end[l]
+                else:
+                    l += 1
+        self.group_bufs: Dict[int, dict] = {}
+        for gi, (gl, ge) in enumerate(self.groups):
+            m, last = ge - gl, gi == len(self.groups) - 1
+            self.group_bufs[gl] = {
+                "end": ge,
+                "scores": torch.empty(m * batch, num_q_heads, n_pad, dtype=torch.float32, device=dev),
+                "lse": torch.empty(m * batch, num_q_heads, dtype=torch.float32, device=dev),
+                "pooled": torch.empty(m * batch * Hsrc, n_pad, dtype=torch.float32, device=dev),
+                "idx": self.idx_g[:m] if last else torch.empty(m, batch, Hsrc, k_cap, dtype=torch.int32, device=dev),
+                "cnt": self.cnt_g[:m] if last else torch.zeros(m, batch, Hsrc, dtype=torch.int32, device=dev),
+                "event": torch.cuda.Event(),
+            }
+        if self.groups:
+            self.idx0 = torch.empty(batch, Hsrc, k_cap, dtype=torch.int32, device=dev)
+            self.cnt0 = torch.zeros(batch, Hsrc, dtype=torch.int32, device=dev)
+            self.ws_side = ops.new_decode_workspace(dev, batch, num_q_heads, num_kv_heads)
+            self.ws_layers_side = ops.new_decode_layers_workspace(dev, batch, num_q_heads, num_kv_heads, gmax)
+        else:
+            self.idx0, self.cnt0 = self.indices, self.counts
+        self.side: Optional[torch.cuda.Stream] = None
         self._tables = {}
         self._graphs = {}
         self.seq_lens: Optional[torch.Tensor] = None     # ragged batch (step / dense_step)
@@ -137,7 +176,14 @@ class KascadeDecoder:
         if seq_len > self.n_max:
             raise InvalidArgumentError(f"seq_len {seq_len} exceeds max_seq_len {self.n_max}")
         self.seq_lens = seq_lens
-        self._run_range(0, self.L, q, k_caches, v_caches, seq_len)
+        overlap = self._can_overlap([(0, self.L)], k_caches, v_caches)
+        if overlap:
+            main = torch.cuda.current_stream()
+            self._side_stream().wait_stream(main)      # the step's q and cache rows are in place
+            self._issue_selects(q, k_caches, v_caches, seq_len)
+        self._run_range(0, self.L, q, k_caches, v_caches, seq_len, overlap=overlap)
+        if overlap:
+            main.wait_stream(self.side)
         return self.out
 
     def _layer_tables(self, k_caches, v_caches, l0: int, l1: int):
@@ -153,12 +199,16 @@ class KascadeDecoder:
             tab = self._tables[key] = (kp, vp)
         return tab
 
-    def _run_range(self, l0: int, l1: int, q, k_caches, v_caches, seq_len: int, dense: bool = False) -> None:
+    def _run_range(self, l0: int, l1: int, q, k_caches, v_caches, seq_len: int, dense: bool = False,
+                   overlap: bool = False) -> None:
         """Layers [l0, l1): every run of consecutive reuse layers (every
         layer in dense mode) is one multi-layer launch; an anchor (or a group
         of consecutive anchors) runs its score passes and its selection, then
         its own sparse passes AND the reuse run that follows it -- they all
         read the anchor's fresh lists -- as one more launch."""
+        if overlap and not dense:
+            self._run_range_overlapped(l0, l1, q, k_caches, v_caches, seq_len)
+            return
         l = l0
         while l < l1:
             if not dense and self.kinds[l] == KIND_ANCHOR and not self.pre and self.seq_lens is None:
@@ -182,6 +232,109 @@ class KascadeDecoder:
                 for i in range(l, end):
                     (self._dense_layer if dense else self._layer)(i, q, k_caches, v_caches, seq_len)
             l = end
+
+    def _can_overlap(self, ranges, k_caches, v_caches) -> bool:
+        """Whether a step split into the layer ``ranges`` runs the overlapped
+        schedule (decided per step: its lists live in other buffers than the
+        single-stream schedule's): post-softmax pooling, a uniform batch, at
+        least one anchor group, one cache layout for every layer (multi-layer
+        launches) and no group cut by a range boundary."""
+        if not self.groups or self.pre or self.seq_lens is not None or \
+                not self._fusable(k_caches, v_caches, 0, self.L):
+            return False
+        return not any(l0 < gl < l1 < ge or gl < l0 < ge for gl, ge in self.groups for l0, l1 in ranges)
+
+    def _lists_before(self, l: int):
+        """(indices, counts) of the latest anchor before layer l in the
+        overlapped schedule: slot 0 of its group (its last anchor) or layer 0's."""
+        src = None
+        for gl, ge in self.groups:
+            if gl < l:
+                src = gl
+        if src is None:
+            return self.idx0, self.cnt0
+        b = self.group_bufs[src]
+        return b["idx"][0], b["cnt"][0]
+
+    def _group_select(self, gl: int, q, k_caches, v_caches, seq_len: int) -> None:
+        """Score pass(es) and the selection of the anchor group starting at
+        gl into its own buffers (side stream, side workspaces); layer gl + i
+        lands in list slot m - 1 - i."""
+        b = self.group_bufs[gl]
+        ge = b["end"]
+        m, B, Hq = ge - gl, self.B, self.Hq
+        Hs = self.indices.shape[1]
+        if m == 1:
+            ops.anchor_scores_decode(q[gl], k_caches[gl], seq_len, b["scores"], b["lse"], workspace=self.ws_side)
+        else:
+            sc_ls = b["scores"].stride(0) * B
+            ops.decode_layers(q[gl:ge], k_caches[gl:ge], v_caches[gl:ge], seq_len, workspace=self.ws_layers_side,
+                              tables=self._layer_tables(k_caches, v_caches, gl, ge),
+                              scores=b["scores"][(m - 1) * B:m * B], scores_layer_stride=-sc_ls,
+                              lse=b["lse"][(m - 1) * B:m * B], lse_layer_stride=-B * Hq)
+        ops.select_decode(b["scores"], b["lse"], seq_len, self.plan.k_policy, self.Hkv,
+                          indices=b["idx"].view(m * B, Hs, -1), counts=b["cnt"].view(m * B, Hs),
+                          pooled=b["pooled"], all_heads=self.all_heads)
+
+    def _run_range_overlapped(self, l0: int, l1: int, q, k_caches, v_caches, seq_len: int) -> None:
+        """The main stream's share of layers [l0, l1) in the overlapped
+        schedule (the anchor groups' score passes + selections were issued on
+        the side stream by _issue_selects): layer 0's dense pass and
+        selection, then per anchor group one sparse launch over its own sets
+        and the reuse run behind it (after waiting for that group's lists),
+        other reuse runs on the lists of the latest anchor before them.  Same
+        kernels and launch shapes per layer as the single-stream step, so the
+        outputs and lists are bit-identical to it."""
+        main = torch.cuda.current_stream()
+        pol = self.plan.k_policy
+        l = l0
+        while l < l1:
+            kind = self.kinds[l]
+            if kind == KIND_ANCHOR0:
+                ops.dense_decode(q[0], k_caches[0], v_caches[0], seq_len, out=self.out[0], lse=self.lse,
+                                 scores=self.scores, workspace=self.ws)
+                ops.select_decode(self.scores, self.lse, seq_len, pol, self.Hkv, indices=self.idx0,
+                                  counts=self.cnt0, pooled=self.pooled, all_heads=self.all_heads)
+                l += 1
+                continue
+            if kind == KIND_ANCHOR:
+                b = self.group_bufs[l]
+                ge = b["end"]
+                end = min(self.run_end[ge], l1) if ge < l1 and self.kinds[ge] == KIND_REUSE else ge
+                main.wait_event(b["event"])
+                if end - l >= 2:
+                    ops.decode_layers(q[l:end], k_caches[l:end], v_caches[l:end], seq_len, out=self.out[l:end],
+                                      workspace=self.ws_layers, tables=self._layer_tables(k_caches, v_caches, l, end),
+                                      indices=b["idx"][0], counts=b["cnt"][0], head_maps=self._fused_maps(l, ge, end))
+                else:                      # a lone last anchor: its own sets, one layer
+                    ops.sparse_decode(q[l], k_caches[l], v_caches[l], seq_len, b["idx"][0], b["cnt"][0],
+                                      self.shared_map, out=self.out[l], workspace=self.ws)
+                l = end
+                continue
+            end = min(self.run_end[l], l1)
+            idx, cnt = self._lists_before(l)
+            if end - l >= 2:
+                ops.decode_layers(q[l:end], k_caches[l:end], v_caches[l:end], seq_len, out=self.out[l:end],
+                                  workspace=self.ws_layers, tables=self._layer_tables(k_caches, v_caches, l, end),
+                                  indices=idx, counts=cnt, head_maps=self.map_table[l:end])
+            else:
+                ops.sparse_decode(q[l], k_caches[l], v_caches[l], seq_len, idx, cnt, self.head_maps[l],
+                                  out=self.out[l], workspace=self.ws)
+            l = end
+
+    def _side_stream(self) -> torch.cuda.Stream:
+        if self.side is None:
+            self.side = torch.cuda.Stream(device=self.device)
+        return self.side
+
+    def _issue_selects(self, q, k_caches, v_caches, seq_len: int) -> None:
+        """Every anchor group's score pass + selection, in layer order, on the
+        side stream (the caller orders the side stream after the step's
+        inputs and joins it back at the end of the step)."""
+        with torch.cuda.stream(self._side_stream()):
+            for gl, _ in self.groups:
+                self._group_select(gl, q, k_caches, v_caches, seq_len)
+                self.group_bufs[gl]["event"].record(self.side)
 
     @staticmethod
     def _fusable(k_caches, v_caches, l: int, end: int) -> bool:
@@ -348,7 +501,7 @@ class KascadeDecoder:
         # Few cross-stream edges keep consecutive reuse-layer kernels chained
         # by programmatic dependent launch (decode.cu).
         h2d, d2h = torch.cuda.Stream(device=self.device), torch.cuda.Stream(device=self.device)
-        ev_first, ev_rest = torch.cuda.Event(), torch.cuda.Event()
+        ev_first, ev_rest, ev_app = torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event()
         ends = sorted({e for e in self.D2H_SPLITS if 0 < e < self.L} | {self.L})
         ev_done = [torch.cuda.Event() for _ in ends]
 
@@ -369,12 +522,27 @@ class KascadeDecoder:
             # segments: layer 0 alone (its rows and queries arrive first), then
             # the layers between the output-copy boundaries
             bounds = sorted({0, 1, self.L} | set(ends))
+            overlap = not dense and self._can_overlap(list(zip(bounds[:-1], bounds[1:])), k_caches, v_caches)
+            if overlap:
+                # the other layers' rows are appended on the side stream as
+                # soon as they arrive, then the anchor groups' score passes and
+                # selections follow there, concurrent with layer 0 on main
+                side = self._side_stream()
+                side.wait_stream(main)
+                side.wait_event(ev_rest)
+                with torch.cuda.stream(side):
+                    ops.append_kv(kv_dev[1:], seq_len - 1, tables_rest, seq_lens)
+                    ev_app.record(side)
+                self._issue_selects(q, k_caches, v_caches, seq_len)
             start = 0
             for a_, b_ in zip(bounds[:-1], bounds[1:]):
                 if a_ == 1:
-                    main.wait_event(ev_rest)
-                    ops.append_kv(kv_dev[1:], seq_len - 1, tables_rest, seq_lens)
-                self._run_range(a_, b_, q, k_caches, v_caches, seq_len, dense=dense)
+                    if overlap:
+                        main.wait_event(ev_app)
+                    else:
+                        main.wait_event(ev_rest)
+                        ops.append_kv(kv_dev[1:], seq_len - 1, tables_rest, seq_lens)
+                self._run_range(a_, b_, q, k_caches, v_caches, seq_len, dense=dense, overlap=overlap)
                 if b_ in ends:
                     c = ends.index(b_)
                     ev_done[c].record(main)
@@ -384,6 +552,8 @@ class KascadeDecoder:
                     start = b_
             main.wait_stream(h2d)
             main.wait_stream(d2h)
+            if overlap:
+                main.wait_stream(self.side)
 
         body()
         torch.cuda.synchronize()

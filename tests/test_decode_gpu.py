@@ -362,8 +362,13 @@ def _check_multi_layer(plan, L, B, Hq, Hkv, n):
     Vs = [torch.randn(B, Hkv, n, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(L)]
     q = (torch.randn(L, B, Hq, 128, device="cuda", generator=g) * 2).to(torch.bfloat16)
     dec = engine.KascadeDecoder(plan, L, B, Hq, Hkv, n)
+    assert dec._can_overlap([(0, L)], Ks, Vs)       # step() runs the selections on the side stream
     fused = dec.step(q, Ks, Vs, n).clone()
     lists = (dec.indices.clone(), dec.counts.clone())
+    # the single-stream schedule of the same launches
+    dec._run_range(0, L, q, Ks, Vs, n)
+    assert torch.equal(dec.out, fused)
+    assert torch.equal(dec.indices, lists[0]) and torch.equal(dec.counts, lists[1])
     for l in range(L):
         dec._layer(l, q, Ks, Vs, n)
     assert torch.equal(dec.out, fused)
