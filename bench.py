@@ -996,7 +996,8 @@ def main():
                "d2h_bytes_per_step": out_host.numel() * 4,
                "note": "KascadeDecoder.capture_host_step: one CUDA graph per step = pinned H2D of the step's q "
                        "and new K/V rows, one append launch into the 32 layers' caches, the layer loop, D2H "
-                       "of all 32 layers' outputs (copies pipelined against the layers on two graph branches); "
+                       "of all 32 layers' outputs (copies pipelined against the layers on two graph branches; "
+                       "the other layers' appends and the anchor groups' score passes + selections on a third); "
                        "host-synchronised every step"}
 
     dec_launches = dec.launches_per_step()
@@ -1045,7 +1046,9 @@ def main():
                    "global_batch": B * world, "k": k, "anchors": LLAMA_ANCHORS, "head_maps": "non-identity",
                    "parallelism": f"batch-sharded x{world}", "kv_layers_distinct": n_distinct,
                    "l2": "inputs > L2 (each layer's KV is %.1f GB)" % (per_layer / 1e9),
-                   "cuda_graph": True},
+                   "cuda_graph": True,
+                   "streams": "anchor groups' score passes + pooled Top-k on a side stream, overlapping the "
+                              "main stream's attention (KascadeDecoder._issue_selects)"},
         "dense_us_per_token": round(ms_den * 1e3 / (B * world), 2),
         "per_layer_ms": {"dense": round(dense_ms_launch, 4), **{k_: round(v, 4) for k_, v in per_kind.items()},
                          "costmodel_weighted_us_per_token": round(cm.kascade_time * 1e3 * L / B, 2),
