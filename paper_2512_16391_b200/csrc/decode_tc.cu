@@ -64,7 +64,9 @@ constexpr int kMaxSplits = 64;
 // LSE rounding) therefore never depend on how many layers share its launch;
 // a dense layer's do (split-K rounding only).  Measured in the 128K b8 decode step (same box, A/B): 4 / 6 / 8 /
 // 12 / 16 / 24 waves for the single-layer launches 573.9 / 568.4 / 565.6 /
-// 565.2 / 564.2 / 565.5 us/token, while the all-layer dense baseline launches
+// 565.2 / 564.2 / 565.5 us/token (a (sequence, kv head) spans at most its
+// partial-slot count of ranges -- 20 for 64 pairs -- so 8 and more requested
+// waves all land near 8.2 there), while the all-layer dense baseline launches
 // lose 2 % above 4 waves per layer; 1 wave and a persistent grid fed by an
 // atomic chunk queue were +4 % (round-2 history).
 constexpr int kWavesSingle = 16;

@@ -59,7 +59,7 @@ for s in "$@"; do
   case $s in
     fullcap)
       timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-        -k 'regex:decode_attn_kernel<\(int\)1' -s 6 -c 1 -o $O/step_reuse_run_$TAG -f python scripts/prof_step.py \
+        -k 'regex:decode_attn_kernel' -s 3 -c 1 -o $O/step_reuse_run_$TAG -f python scripts/prof_step.py \
         > $O/fullcap_step_$TAG.out 2>&1
       echo "step reuse-run capture rc=$?"
       timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \

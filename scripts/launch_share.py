@@ -10,11 +10,12 @@ import sys
 
 
 def short(name: str) -> str:
+    name = name.replace("(int)", "").replace("(bool)", "")
     m = re.match(r"(?:void )?(?:kscd::)?([A-Za-z0-9_]+)(<[^()]*>)?", name)
     if not m:
         return name[:60]
     base = m.group(1)
-    if base.startswith(("decode_attn", "prefill_attn", "topk", "pool", "append", "probs", "pool_rows")):
+    if base.startswith(("decode_attn", "decode_tc", "prefill_attn", "topk", "pool", "append", "probs", "pool_rows")):
         return base + (m.group(2) or "")
     return "torch/other: " + base[:40]
 
@@ -44,16 +45,27 @@ def main():
         c = sum(h[0] for h in hits)
         return sum(h[1] for h in hits) / c if c else float("nan")
 
-    # composed 32-layer step of bench.py's default plan: 27 reuse + 4 anchors
-    # (scores, pool, top-k, sparse) + anchor 0 (dense with scores, pool, top-k)
-    sparse = mean("decode_attn_kernel<1")
-    scores = mean("decode_attn_kernel<2")
-    dense = mean("decode_attn_kernel<0")
-    pool = mean("pool_decode")
-    topk = mean("topk_kernel<4")   # decode rows run as 4-CTA clusters
-    step = 27 * sparse + 4 * (scores + pool + topk + sparse) + (dense + pool + topk)
-    print(f"\ncomposed decode step (ncu, serialised): {step:.0f} us; reuse sparse_decode {sparse:.1f} us/launch, "
-          f"27 launches = {27 * sparse / step:.1%} of the step; all sparse_decode = {31 * sparse / step:.1%}")
+    def by_grid(prefix, grid):
+        return mean(prefix, grid)
+
+    # composed 32-layer step of bench.py's default plan (anchors 0, 2, 8, 13,
+    # 14; 16 launches): layer 0 dense + scores, 3 score launches (groups [2],
+    # [8], [13, 14]), 4 + 1 pooling and Top-k launches, and the sparse
+    # launches (reuse layer 1; groups with their reuse runs 2-7, 8-12, 13-31)
+    dense0 = by_grid("decode_tc_kernel<0, 4>", "(1214, 1, 1)")
+    score1 = by_grid("decode_tc_kernel<2, 4>", "(1214, 1, 1)")
+    score2 = by_grid("decode_tc_kernel<2, 4>", "(2428, 1, 1)")
+    pool1, pool2 = by_grid("pool_decode", "(128, 8, 8)"), by_grid("pool_decode", "(128, 8, 16)")
+    topk1, topk2 = by_grid("topk_kernel<4>", "(256, 1, 1)"), by_grid("topk_kernel<4>", "(512, 1, 1)")
+    sp = {g: by_grid("decode_attn_kernel<0>", g) for g in ("(9, 8, 8)", "(9, 8, 48)", "(9, 8, 40)", "(9, 8, 152)")}
+    select = 3 * (pool1 + topk1) + pool2 + topk2
+    sparse = sum(sp.values())
+    step = dense0 + 2 * score1 + score2 + select + sparse
+    print(f"\ncomposed decode step (ncu, serialised, cold caches): {step:.0f} us = dense0 {dense0:.0f} + score passes "
+          f"{2 * score1 + score2:.0f} + selections {select:.0f} + sparse launches {sparse:.0f} "
+          f"(longest run, layers 13-31: {sp['(9, 8, 152)']:.0f})")
+    print(f"shares: sparse {sparse / step:.1%}, dense + score passes {(dense0 + 2 * score1 + score2) / step:.1%}, "
+          f"selections {select / step:.1%} (overlapped with the attention on a side stream in the step)")
 
 
 if __name__ == "__main__":

@@ -2,7 +2,7 @@
 (8 distinct KV buffers cycled over the 32 layers, each 4.3 GB >> L2), for
 ncu captures of the step's own launches -- e.g. its longest reuse run as
 the single multi-layer launch it is (dev tool).
-    ncu -k 'regex:decode_attn_kernel<\\(int\\)1' -s 6 -c 1 ... python scripts/prof_step.py"""
+    ncu -k 'regex:decode_attn_kernel' -s 3 -c 1 ... python scripts/prof_step.py  (4th sparse launch: layers 13-31)"""
 import os
 import sys
 
