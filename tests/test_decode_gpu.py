@@ -296,6 +296,34 @@ def test_decode_engine_llama_shapes_vs_oracle(cuda_ok):
         assert_outputs_close(out[:, b], Y)
 
 
+def test_decode_engine_all_heads_pooled_vs_oracle(cuda_ok):
+    """All-heads-pooled mode (runner.py:180-197) through the engine's step:
+    one shared set per sequence from the mean of every kv head's pooled
+    vector, used by every head of the anchors and the reuse layers; anchors
+    [0, 2, 3] make layers 2-3 a group (its list slots in the side-stream
+    schedule) followed by two reuse layers."""
+    from paper_2512_16391_b200 import engine
+    from paper_2512_16391_b200.host_types import AnchorPlan, AnchorPlanCore, KBudgetPolicy
+    L, B, Hq, Hkv, n = 6, 2, 16, 4, 6000
+    rng = np.random.default_rng(17)
+    plan = AnchorPlan(AnchorPlanCore([0, 2, 3], 3, 0.0), mode="all_heads_pooled", k_policy=KBudgetPolicy(0.05, 64))
+    q = orc.bf16_round((rng.standard_normal((L, B, Hq, 128)) * 2.5).astype(np.float32))
+    K = orc.bf16_round(rng.standard_normal((L, B, Hkv, n, 128)).astype(np.float32))
+    V = orc.bf16_round(rng.standard_normal((L, B, Hkv, n, 128)).astype(np.float32))
+    dec = engine.KascadeDecoder(plan, L, B, Hq, Hkv, n)
+    Ks, Vs = [_dev(K[l], torch.bfloat16) for l in range(L)], [_dev(V[l], torch.bfloat16) for l in range(L)]
+    assert dec._can_overlap([(0, L)], Ks, Vs)
+    out = dec.step(_dev(q, torch.bfloat16), Ks, Vs, n).cpu().numpy()
+    for b in range(B):
+        Y, sels, _ = orc.decode_step(q[:, b], K[:, b], V[:, b], [0, 2, 3], {}, 0.05, 64, mode=orc.ALL_HEADS_POOLED,
+                                     want_mass=False)
+        assert_outputs_close(out[:, b], Y)
+        # the last anchor's shared set (every kv head reads it)
+        c = int(dec.counts[b, 0])
+        got = dec.indices[b, 0, :c].cpu().numpy()
+        assert np.array_equal(np.sort(got), np.sort(np.asarray(sels[3][0]))) or len(np.setxor1d(got, sels[3][0])) <= 2
+
+
 @pytest.mark.parametrize("splits", [(), (1, 2)])
 def test_host_step_graph_appends_and_matches_step(cuda_ok, splits):
     """capture_host_step (pinned H2D + one-launch KV append + layer loop +
