@@ -19,7 +19,7 @@
 template <int U>
 __global__ void __launch_bounds__(256) gather_rows(const int4* __restrict__ kc, const int4* __restrict__ vc,
                                                    const int* __restrict__ idx, int lists, int k, long long n,
-                                                   int4* sink) {
+                                                   int4* sink, int rs) {
   const int half = (blockIdx.x * blockDim.x + threadIdx.x) >> 4;   // one half-warp per row group
   const int nhalf = (gridDim.x * blockDim.x) >> 4;
   const int sub = threadIdx.x & 15;
@@ -33,8 +33,8 @@ __global__ void __launch_bounds__(256) gather_rows(const int4* __restrict__ kc, 
       if (e < total) {
         const long long list = e / k;
         const long long row = list * n + __ldg(idx + e);
-        kr[u] = __ldcs(kc + row * 16 + sub);
-        vr[u] = __ldcs(vc + row * 16 + sub);
+        kr[u] = __ldcs(kc + row * rs + sub);
+        vr[u] = __ldcs(vc + row * rs + sub);
       } else {
         kr[u] = vr[u] = make_int4(0, 0, 0, 0);
       }
@@ -52,14 +52,14 @@ __global__ void __launch_bounds__(256) gather_rows(const int4* __restrict__ kc, 
 
 template <int U>
 static void run(const int4* kc, const int4* vc, const int* idx, int lists, int k, long long n, int4* sink, int grid,
-                double bytes) {
+                double bytes, int rs = 16) {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   float best = 1e30f;
   for (int it = 0; it < 5; ++it) {
     cudaEventRecord(a);
-    gather_rows<U><<<grid, 256>>>(kc, vc, idx, lists, k, n, sink);
+    gather_rows<U><<<grid, 256>>>(kc, vc, idx, lists, k, n, sink, rs);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms;
@@ -103,6 +103,20 @@ int main(int argc, char** argv) {
     run<2>(kc, vc, idx, lists, k, n, sink, g, bytes);
     run<4>(kc, vc, idx, lists, k, n, sink, g, bytes);
     run<8>(kc, vc, idx, lists, k, n, sink, g, bytes);
+  }
+  // interleaved layout: K and V rows of one position adjacent ([n][2][128]),
+  // one 512-B contiguous read per selected key instead of two 256-B reads
+  printf("interleaved K|V rows (one 512-B read per key):\n");
+  {
+    int4* kv;
+    cudaMalloc(&kv, 2 * cache);
+    cudaMemset(kv, 3, 2 * cache);
+    for (int g : {sms * 4, sms * 8}) {
+      run<2>(kv, kv + 16, idx, lists, k, n, sink, g, bytes, 32);
+      run<4>(kv, kv + 16, idx, lists, k, n, sink, g, bytes, 32);
+      run<8>(kv, kv + 16, idx, lists, k, n, sink, g, bytes, 32);
+    }
+    cudaFree(kv);
   }
   // sequential read of the same byte count for reference (contiguous rows)
   {
