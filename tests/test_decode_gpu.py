@@ -324,16 +324,19 @@ def test_decode_engine_all_heads_pooled_vs_oracle(cuda_ok):
         assert np.array_equal(np.sort(got), np.sort(np.asarray(sels[3][0]))) or len(np.setxor1d(got, sels[3][0])) <= 2
 
 
-@pytest.mark.parametrize("splits", [(), (1, 2)])
-def test_host_step_graph_appends_and_matches_step(cuda_ok, splits):
+@pytest.mark.parametrize("splits,anchors,L", [((), [0, 2], 3), ((1, 2), [0, 2], 3), ((3,), [0, 2, 3], 5),
+                                              ((4,), [0, 2, 3], 5)])
+def test_host_step_graph_appends_and_matches_step(cuda_ok, splits, anchors, L):
     """capture_host_step (pinned H2D + one-launch KV append + layer loop +
     D2H as one CUDA graph) equals appending by hand and running step(); the
-    appended rows land bit-exactly at position n-1 of every layer."""
+    appended rows land bit-exactly at position n-1 of every layer.  With
+    anchors [0, 2, 3] an output-copy boundary at 3 cuts the anchor group
+    (single-stream schedule), one at 4 does not (side-stream schedule)."""
     from paper_2512_16391_b200 import engine
     from paper_2512_16391_b200.host_types import AnchorPlan, AnchorPlanCore, HeadMap, KBudgetPolicy
-    L, B, Hq, Hkv, n, n_cap = 3, 2, 8, 2, 700, 768
-    plan = AnchorPlan(AnchorPlanCore([0, 2], 2, 0.0), head_maps={1: HeadMap(1, 0, [1, 0])},
-                      k_policy=KBudgetPolicy(0.1, 16))
+    B, Hq, Hkv, n, n_cap = 2, 8, 2, 700, 768
+    maps = {l: HeadMap(l, max(a for a in anchors if a <= l), [1, 0]) for l in range(L) if l not in anchors}
+    plan = AnchorPlan(AnchorPlanCore(anchors, len(anchors), 0.0), head_maps=maps, k_policy=KBudgetPolicy(0.1, 16))
     g = torch.Generator(device="cuda").manual_seed(5)
     Ks = [torch.randn(B, Hkv, n_cap, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(L)]
     Vs = [torch.randn(B, Hkv, n_cap, 128, device="cuda", generator=g).to(torch.bfloat16) for _ in range(L)]
@@ -345,6 +348,8 @@ def test_host_step_graph_appends_and_matches_step(cuda_ok, splits):
     dec = engine.KascadeDecoder(plan, L, B, Hq, Hkv, n_cap)
     dec.D2H_SPLITS = splits                        # one output copy, or one per layer
     q = torch.empty(L, B, Hq, 128, dtype=torch.bfloat16, device="cuda")
+    bounds = sorted({0, 1, L} | {e for e in splits if 0 < e < L})
+    assert dec._can_overlap(list(zip(bounds[:-1], bounds[1:])), Ks, Vs) == (splits != (3,))
     graph = dec.capture_host_step(q_host, kv_host, out_host, q, Ks, Vs, n)
     out_host.zero_()
     graph.replay()
