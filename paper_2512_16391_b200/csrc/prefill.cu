@@ -63,6 +63,20 @@ struct PrefillTmaps {
   CUtensorMap q, k, v;
 };
 
+#ifdef KSCD_PF_TRACE
+// dev instrumentation (variant builds only): clock64 stamps of one CTA's
+// pipeline events per key block -- see scripts/pf_trace.py
+__device__ long long g_pf_trace[256][8];
+#define PF_TRACE(e, j)                                                                                   \
+  do {                                                                                                   \
+    if (blockIdx.y == 0 && (int)blockIdx.x == (int)gridDim.x / 2 && (j) < 256) g_pf_trace[(j)][(e)] = clock64(); \
+  } while (0)
+#else
+#define PF_TRACE(e, j) \
+  do {                 \
+  } while (0)
+#endif
+
 // bars: 0 q_full | 1-2 k_full[s] | 3-4 v_full[s] | 5-6 kv_empty[s] |
 //       7-8 s_full[t] | 9-10 p_full[t] | 11-12 o_done[t] |
 //       13-14 k_empty[s] (sparse: the K half of a stage frees once S of
@@ -159,6 +173,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
           const uint32_t d = tmem + t * 256 + 128;
           const uint32_t p = tmem + t * 256;
           mbar_wait(&bars[9 + t], j & 1);          // P_t(j) written
+          PF_TRACE(2 * t, j);
           tc_fence_after();
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks) {
@@ -210,6 +225,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
             mbar_wait(&bars[1 + st1], ph1);
             tc_fence_after();
             issue_s(0, st1);
+            PF_TRACE(1, j);
           }
           if (nslots == 2) {
             if (MODE != PMODE_LSE) {
@@ -218,7 +234,10 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
             }
           }
           mma_commit(&bars[5 + st]);   // K/V stage free once everything so far retires
-          if (more && nslots == 2) issue_s(1, st1);
+          if (more && nslots == 2) {
+            issue_s(1, st1);
+            PF_TRACE(3, j);
+          }
           if (MODE == PMODE_SPARSE && more) mma_commit(&bars[13 + st1]);   // K_{j+1} consumed by both S
         }
         }  // MODE != PMODE_LSE
@@ -351,6 +370,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
         const int sb = MODE == PMODE_LSE ? 7 + t + 2 * (j & 1) : 7 + t;
         const uint32_t s_off = MODE == PMODE_LSE ? 128 * (j & 1) : 0;
         mbar_wait(&bars[sb], MODE == PMODE_LSE ? (j >> 1) & 1 : j & 1);
+        if (lane == 0 && q == 0) PF_TRACE(4 + 2 * t, j);
         tc_fence_after();
         // the whole 128-key row of S in one batch of TMEM loads, one wait
         float s[128];
@@ -382,16 +402,8 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
               if (k0 + c > lim) s[c] = -INFINITY;
           }
         }
-        // tree max for the dense / LSE modes; the sparse mode keeps the running max
-        // (measured 3 % faster there at 128K, A/B on one box)
         float mx_raw;
-        if (MODE == PMODE_SPARSE) {
-          mx_raw = -INFINITY;
-#pragma unroll
-          for (int c = 0; c < 128; ++c) mx_raw = fmaxf(mx_raw, s[c]);
-        } else {
-          mx_raw = max_tree<128>(s);
-        }
+        mx_raw = max_tree<128>(s);   // 8 FMNMX3 chains (a serial running max was 6 % slower in sparse mode)
         const float mx = mx_raw * a.scale_log2;   // scale > 0: max commutes
         // Lazy rescale: a row moves its reference max only when the block max
         // exceeds it by > 2^8.  tcgen05.ld/st are warp-collective, so the O
@@ -450,6 +462,7 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
         const float2 sum2 = __fadd2_rn(__fadd2_rn(sum4[0], sum4[1]), __fadd2_rn(sum4[2], sum4[3]));
         l += sum2.x + sum2.y;
         tc_fence_before();
+        if (lane == 0 && q == 0) PF_TRACE(5 + 2 * t, j);
         mbar_arrive(&bars[MODE == PMODE_LSE ? 11 + t + 2 * (j & 1) : 9 + t]);
       }
       // ---------------------------------------------------------- epilogue
@@ -568,6 +581,16 @@ static cudaError_t launch_prefill_mode(const PrefillArgs& a, cudaStream_t st) {
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, prefill_attn_kernel<MODE>, tm, a);
 }
+
+#ifdef KSCD_PF_TRACE
+extern "C" int kscd_debug_pf_trace(void* dst) {
+  return (int)cudaMemcpyFromSymbol(dst, g_pf_trace, sizeof(g_pf_trace));
+}
+extern "C" int kscd_debug_pf_trace_reset() {
+  static long long zeros[256][8];
+  return (int)cudaMemcpyToSymbol(g_pf_trace, zeros, sizeof(zeros));
+}
+#endif
 
 cudaError_t launch_prefill_attn(int mode, const PrefillArgs& a, cudaStream_t st) {
   // (a CTA-pair variant on 2-SM UMMA was measured slower and removed)
