@@ -402,63 +402,79 @@ __global__ void __launch_bounds__(pf::kThreads, 1)
               if (k0 + c > lim) s[c] = -INFINITY;
           }
         }
-        float mx_raw;
-        mx_raw = max_tree<128>(s);   // 8 FMNMX3 chains (a serial running max was 6 % slower in sparse mode)
-        const float mx = mx_raw * a.scale_log2;   // scale > 0: max commutes
-        // Lazy rescale: a row moves its reference max only when the block max
-        // exceeds it by > 2^8.  tcgen05.ld/st are warp-collective, so the O
-        // correction runs for the whole warp when any row needs it (alpha = 1
-        // for the others).
-        const bool need = mx > m_used + kRescaleThreshold;
-        const float alpha = (need && m_used != -INFINITY) ? exp2f(m_used - mx) : 1.f;
-        if (MODE != PMODE_LSE && __any_sync(0xffffffffu, alpha != 1.f)) {
-          // O_t holds blocks < j (their PV completed before S_j was committed)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t r[32];
-            tmem_ld32(lane_base + o_col + c * 32, r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-            tmem_st32(lane_base + o_col + c * 32, r);
-          }
-          tmem_st_wait();
-        }
-        l *= alpha;
-        if (need) m_used = mx;
-        // p = exp2(s*scale*log2e - m): one packed FFMA2 per key pair + MUFU
-        const float mu = m_used == -INFINITY ? 0.f : m_used;
         const float2 sc2 = make_float2(a.scale_log2, a.scale_log2);
-        const float2 nm2 = make_float2(-mu, -mu);
         float2 sum4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                           make_float2(0.f, 0.f)};   // 4 independent FADD2 chains
-        if (MODE == PMODE_LSE) {
+        // p = exp2(s*scale*log2e - m): one packed FFMA2 per key pair + MUFU,
+        // P (bf16 pairs) over S in TMEM; the row sum into sum4
+        auto exps = [&](float mu) {
+          const float2 nm2 = make_float2(-mu, -mu);
 #pragma unroll
-          for (int c = 0; c < 128; c += 2) {
-            const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sc2, nm2);
-            sum4[(c >> 1) & 3] = __fadd2_rn(sum4[(c >> 1) & 3], exp2_pair_sum<KSCD_LSE_POLY>(x, c >> 1));
-          }
-        } else {
+          for (int i = 0; i < 4; ++i) sum4[i] = make_float2(0.f, 0.f);
+          if (MODE == PMODE_LSE) {
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t r[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float2 x = __ffma2_rn(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sc2, nm2);
-              const float2 p = exp2_pair(x, c * 16 + i);
-              sum4[i & 3] = __fadd2_rn(sum4[i & 3], p);
-              r[i] = pack_bf16(p.x, p.y);
+            for (int c = 0; c < 128; c += 2) {
+              const float2 x = __ffma2_rn(make_float2(s[c], s[c + 1]), sc2, nm2);
+              sum4[(c >> 1) & 3] = __fadd2_rn(sum4[(c >> 1) & 3], exp2_pair_sum<KSCD_LSE_POLY>(x, c >> 1));
             }
-            // 16 packed columns: the key pairs of this 32-key chunk
-            asm volatile(
-                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n"
-                ::"r"(lane_base + s_col + c * 16), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]),
-                "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]),
-                "r"(r[13]), "r"(r[14]), "r"(r[15])
-                : "memory");
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint32_t r[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const float2 x = __ffma2_rn(make_float2(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sc2, nm2);
+                const float2 p = exp2_pair(x, c * 16 + i);
+                sum4[i & 3] = __fadd2_rn(sum4[i & 3], p);
+                r[i] = pack_bf16(p.x, p.y);
+              }
+              // 16 packed columns: the key pairs of this 32-key chunk
+              asm volatile(
+                  "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n"
+                  ::"r"(lane_base + s_col + c * 16), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]),
+                  "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]),
+                  "r"(r[13]), "r"(r[14]), "r"(r[15])
+                  : "memory");
+            }
           }
-          tmem_st_wait();
+        };
+        // Lazy rescale: a row moves its reference max only when the block max
+        // exceeds it by > 2^8.  The exponentials are taken against the current
+        // reference first; every p <= 2^8 (sum <= 2^8 proves it) means no key
+        // exceeded the reference by > 2^8, which is exactly the no-rescale
+        // case, so the block max is never formed then (no FMNMX on the
+        // per-tile chain).  Otherwise -- and while a row has no reference --
+        // the warp takes the exact path: block max, the same rescale rule,
+        // the block redone.  tcgen05.ld/st are warp-collective, so the O
+        // correction runs for the whole warp (alpha = 1 for the other rows).
+        bool slow = m_used == -INFINITY;
+        if (!__all_sync(0xffffffffu, slow)) {
+          exps(m_used == -INFINITY ? 0.f : m_used);
+          const float2 t2 = __fadd2_rn(__fadd2_rn(sum4[0], sum4[1]), __fadd2_rn(sum4[2], sum4[3]));
+          slow = slow || t2.x + t2.y > 256.f;
         }
+        if (__any_sync(0xffffffffu, slow)) {
+          const float mx = max_tree<128>(s) * a.scale_log2;   // scale > 0: max commutes
+          const bool need = mx > m_used + kRescaleThreshold;
+          const float alpha = (need && m_used != -INFINITY) ? exp2f(m_used - mx) : 1.f;
+          if (MODE != PMODE_LSE) tmem_st_wait();              // speculative P landed before it is redone
+          if (MODE != PMODE_LSE && __any_sync(0xffffffffu, alpha != 1.f)) {
+            // O_t holds blocks < j (their PV completed before S_j was committed)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint32_t r[32];
+              tmem_ld32(lane_base + o_col + c * 32, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+              tmem_st32(lane_base + o_col + c * 32, r);
+            }
+          }
+          l *= alpha;
+          if (need) m_used = mx;
+          exps(m_used == -INFINITY ? 0.f : m_used);
+        }
+        if (MODE != PMODE_LSE) tmem_st_wait();
         const float2 sum2 = __fadd2_rn(__fadd2_rn(sum4[0], sum4[1]), __fadd2_rn(sum4[2], sum4[3]));
         l += sum2.x + sum2.y;
         tc_fence_before();
