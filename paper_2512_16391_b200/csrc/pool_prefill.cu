@@ -52,6 +52,23 @@ struct PoolTmaps {
   CUtensorMap q, k;
 };
 
+#ifdef KSCD_PB_TRACE
+// dev instrumentation (variant builds only): clock64 stamps of one pass-B
+// CTA (the middle tile, kv head 0) per key block -- scripts/pb_trace.py
+__device__ long long g_pb_trace[512][8];
+#define PB_TRACE(e, j)                                                                                       \
+  do {                                                                                                       \
+    if (blockIdx.y == 0 && (int)blockIdx.x == (int)gridDim.x / 2 && (j) < 512) g_pb_trace[(j)][(e)] = clock64(); \
+  } while (0)
+extern "C" int kscd_debug_pb_trace(void* dst) {
+  return (int)cudaMemcpyFromSymbol(dst, g_pb_trace, sizeof(g_pb_trace));
+}
+#else
+#define PB_TRACE(e, j) \
+  do {                 \
+  } while (0)
+#endif
+
 // Sum over the 128 (head, row) columns of one S^T quarter held by this
 // thread (its key): exp2(s * scale * log2e - lse2[row]), rows after the key
 // zeroed on the diagonal block (the causal zeros of _post_pooled).
@@ -205,7 +222,9 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
       const bool diag = (j == nb - 1);             // only the last block crosses the staircase
       float2 acc2 = make_float2(0.f, 0.f);
       for (int qq = x; qq < nh; qq += 2) {
+        if (lane == 0 && q == 0) PB_TRACE(qq, j);           // quarter qq of block j: waiting starts
         mbar_wait(&bars[5 + qq], j & 1);
+        if (lane == 0 && q == 0) PB_TRACE(4 + qq, j);       // ... S^T ready
         tc_fence_after();
         uint32_t r[128];
 #pragma unroll
