@@ -192,7 +192,7 @@ class KascadeDecoder:
         key = (l0, l1) + tuple(t.data_ptr() for t in k_caches[l0:l1]) + tuple(t.data_ptr() for t in v_caches[l0:l1])
         tab = self._tables.get(key)
         if tab is None:
-            if torch.cuda.is_current_stream_capturing():
+            if self.device.type == "cuda" and torch.cuda.is_current_stream_capturing():
                 raise InvalidArgumentError("new cache buffers inside a CUDA graph capture: run the step eagerly first")
             kp = torch.tensor([t.data_ptr() for t in k_caches[l0:l1]], dtype=torch.int64, device=self.device)
             vp = torch.tensor([t.data_ptr() for t in v_caches[l0:l1]], dtype=torch.int64, device=self.device)
@@ -372,7 +372,7 @@ class KascadeDecoder:
         key = ("maps", l0, l1, end)
         t = self._tables.get(key)
         if t is None:
-            if torch.cuda.is_current_stream_capturing():
+            if self.device.type == "cuda" and torch.cuda.is_current_stream_capturing():
                 raise InvalidArgumentError("new launch layout inside a CUDA graph capture: run the step eagerly first")
             m, Hs = l1 - l0, self.indices.shape[1]
             own = torch.zeros(self.Hkv, dtype=torch.int32, device=self.device) if self.all_heads else \
