@@ -12,6 +12,13 @@ and ``dense_step`` is the Top-k = 100% baseline over the same layers.  All
 buffers are preallocated, so a step can be captured once in a CUDA graph
 and replayed (``capture``), which removes the per-kernel launch gaps that
 dominate the small reuse layers.
+
+On uniform batches with post-softmax pooling, ``step`` issues the anchor
+groups' score passes and selections on an internal side stream ahead of the
+layer loop (the selections overlap the attention of other layers) and joins
+that stream back into the caller's stream before it returns, so the step is
+ordered on the caller's stream exactly like a single-stream call (and a
+captured graph holds both branches).
 """
 
 from __future__ import annotations
