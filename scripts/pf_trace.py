@@ -1,7 +1,7 @@
 """Per-block pipeline timeline of one prefill CTA (the middle tile, head pair
 0) from a KSCD_PF_TRACE variant build (dev tool):
     bash scripts/build_variant.sh pftrace -DKSCD_PF_TRACE
-    KSCD_LIB_PATH=_exp/libkascade_pftrace.so python scripts/pf_trace.py {dense|sparse} [N]
+    KSCD_LIB_PATH=_exp/libkascade_pftrace.so python scripts/pf_trace.py {dense|sparse|lse} [N]
 Events per key block j (SM clock64): MMA thread after P0(j) / after issuing
 S0(j+1) / after P1(j) / after issuing S1(j+1); softmax tile 0 and tile 1
 (warp lane 0 of quarter 0): S(j) ready / P(j) written."""
@@ -25,8 +25,13 @@ def main():
     q = torch.randn(Hq, N, 128, device="cuda", generator=g).to(torch.bfloat16)
     k = torch.randn(Hkv, N, 128, device="cuda", generator=g).to(torch.bfloat16)
     v = torch.randn(Hkv, N, 128, device="cuda", generator=g).to(torch.bfloat16)
-    out, lse = ops.dense_prefill(q, k, v)
     lib = _lib.load()
+    if mode == "lse":
+        torch.cuda.synchronize()
+        lib.kscd_debug_pf_trace_reset()
+        lse = ops.anchor_lse_prefill(q, k)
+    else:
+        out, lse = ops.dense_prefill(q, k, v)
     if mode == "sparse":
         idx, cnt = ops.select_prefill(q, k, lse, KBudgetPolicy(0.1, 128))
         torch.cuda.synchronize()
