@@ -217,6 +217,9 @@ class ShardedKascadeDecoder:
         self.kinds = self.local.kinds
         self.maps = {l: local_head_map(plan.head_maps[l].map, self.g0, self.g1, dev)
                      for l, kind in enumerate(self.kinds) if kind == KIND_REUSE}
+        # [L][Hloc] table of the reuse layers' maps (rows of other layers unused)
+        zeros = torch.zeros(self.Hloc, dtype=torch.int32, device=dev)
+        self.map_table = torch.stack([self.maps.get(l, zeros) for l in range(num_layers)]).contiguous()
         kc = k_budget(plan.k_policy, max_seq_len)
         self.full_idx = torch.empty(batch, num_kv_heads, kc, dtype=torch.int32, device=dev)
         self.full_cnt = torch.zeros(batch, num_kv_heads, dtype=torch.int32, device=dev)
@@ -232,11 +235,24 @@ class ShardedKascadeDecoder:
         loc = self.local
         loc.seq_lens = seq_lens
         ws = loc.ws
-        for l, kind in enumerate(self.kinds):
+        l = 0
+        while l < len(self.kinds):
+            kind = self.kinds[l]
             ql, kl, vl = q[l], k_caches[l], v_caches[l]
             if kind == KIND_REUSE:
-                ops.sparse_decode(ql, kl, vl, seq_len, self.full_idx, self.full_cnt, self.maps[l], out=loc.out[l],
-                                  workspace=ws)
+                # a run of consecutive reuse layers reads the gathered lists
+                # through each layer's local -> global map: one multi-layer
+                # launch (uniform batch, one cache layout), as in the local step
+                end = loc.run_end[l]
+                if end - l >= 2 and seq_lens is None and loc._fusable(k_caches, v_caches, l, end):
+                    ops.decode_layers(q[l:end], k_caches[l:end], v_caches[l:end], seq_len, out=loc.out[l:end],
+                                      workspace=loc.ws_layers, tables=loc._layer_tables(k_caches, v_caches, l, end),
+                                      indices=self.full_idx, counts=self.full_cnt, head_maps=self.map_table[l:end])
+                else:
+                    for i in range(l, end):
+                        ops.sparse_decode(q[i], k_caches[i], v_caches[i], seq_len, self.full_idx, self.full_cnt,
+                                          self.maps[i], out=loc.out[i], workspace=ws)
+                l = end
                 continue
             loc._anchor_select(l, kind, ql, kl, vl, seq_len, loc.out[l])
             # the exchange overlaps the anchor's own sparse pass, which only
@@ -245,6 +261,7 @@ class ShardedKascadeDecoder:
             if kind == KIND_ANCHOR:
                 ops.sparse_decode(ql, kl, vl, seq_len, loc.indices, loc.counts, None, out=loc.out[l], workspace=ws)
             self.exchange.finish()
+            l += 1
         return loc.out
 
     def capture(self, q, k_caches, v_caches, seq_len: int, dense: bool = False, seq_lens=None):
@@ -292,6 +309,9 @@ class ShardedKascadePrefill:
         self.kinds = self.local.kinds
         self.maps = {l: local_head_map(plan.head_maps[l].map, self.g0, self.g1, dev)
                      for l, kind in enumerate(self.kinds) if kind == KIND_REUSE}
+        # [L][Hloc] table of the reuse layers' maps (rows of other layers unused)
+        zeros = torch.zeros(self.Hloc, dtype=torch.int32, device=dev)
+        self.map_table = torch.stack([self.maps.get(l, zeros) for l in range(num_layers)]).contiguous()
         T, kc = self.local.indices.shape[1], self.local.indices.shape[2]
         self.full_idx = torch.empty(num_kv_heads, T, kc, dtype=torch.int32, device=dev)
         self.full_cnt = torch.zeros(num_kv_heads, T, dtype=torch.int32, device=dev)

@@ -35,9 +35,12 @@ def _worker(rank, world, port, errq, backend="gloo"):
         from oracle import kascade_oracle as orc
         from paper_2512_16391_b200 import engine, sharding
         from paper_2512_16391_b200.host_types import AnchorPlan, AnchorPlanCore, HeadMap, KBudgetPolicy
-        L, B, Hq, Hkv, n = 3, 2, 8, 4, 1200
+        L, B, Hq, Hkv, n = 6, 2, 8, 4, 1200
         G = Hq // Hkv
-        plan = AnchorPlan(AnchorPlanCore([0, 2], 2, 0.0), head_maps={1: HeadMap(1, 0, [2, 0, 3, 1])},
+        # reuse layers 3-5 run as one multi-layer launch over the gathered lists
+        plan = AnchorPlan(AnchorPlanCore([0, 2], 2, 0.0),
+                          head_maps={1: HeadMap(1, 0, [2, 0, 3, 1]), 3: HeadMap(3, 2, [3, 2, 1, 0]),
+                                     4: HeadMap(4, 2, [1, 1, 2, 2]), 5: HeadMap(5, 2, [0, 3, 0, 3])},
                           k_policy=KBudgetPolicy(0.1, 64))
         rng = np.random.default_rng(5)
         q = orc.bf16_round((rng.standard_normal((L, B, Hq, 128)) * 2).astype(np.float32))
