@@ -254,6 +254,30 @@ class ShardedKascadeDecoder:
                                           self.maps[i], out=loc.out[i], workspace=ws)
                 l = end
                 continue
+            ge = loc.group_end.get(l, l + 1) if kind == KIND_ANCHOR else l + 1
+            if ge - l >= 2 and seq_lens is None and not loc.pre and loc._fusable(k_caches, v_caches, l, ge):
+                # consecutive anchors as one group (as the local step): one
+                # score launch, one select over their (sequence, kv head) rows
+                # (layer l + i into list slot m - 1 - i), ONE all-gather of the
+                # last anchor's lists (slot 0, what the reuse layers read),
+                # overlapping the group's sparse launch over its own sets
+                m, B, Hs = ge - l, loc.B, loc.indices.shape[1]
+                tabs = loc._layer_tables(k_caches, v_caches, l, ge)
+                sc_ls = loc.scores_g.stride(0) * B
+                ops.decode_layers(q[l:ge], k_caches[l:ge], v_caches[l:ge], seq_len, workspace=loc.ws_layers,
+                                  tables=tabs, scores=loc.scores_g[(m - 1) * B:m * B], scores_layer_stride=-sc_ls,
+                                  lse=loc.lse_g[(m - 1) * B:m * B], lse_layer_stride=-B * loc.Hq)
+                ops.select_decode(loc.scores_g[:m * B], loc.lse_g[:m * B], seq_len, loc.plan.k_policy, loc.Hkv,
+                                  indices=loc.idx_g[:m].view(m * B, Hs, -1), counts=loc.cnt_g[:m].view(m * B, Hs),
+                                  pooled=loc.pooled_g[:m * B * Hs])
+                self.exchange.start()
+                ops.decode_layers(q[l:ge], k_caches[l:ge], v_caches[l:ge], seq_len, out=loc.out[l:ge],
+                                  workspace=loc.ws_layers, tables=tabs, indices=loc.idx_g[m - 1],
+                                  counts=loc.cnt_g[m - 1], index_layer_stride=-loc.idx_g.stride(0),
+                                  count_layer_stride=-loc.cnt_g.stride(0))
+                self.exchange.finish()
+                l = ge
+                continue
             loc._anchor_select(l, kind, ql, kl, vl, seq_len, loc.out[l])
             # the exchange overlaps the anchor's own sparse pass, which only
             # needs this rank's lists

@@ -35,12 +35,13 @@ def _worker(rank, world, port, errq, backend="gloo"):
         from oracle import kascade_oracle as orc
         from paper_2512_16391_b200 import engine, sharding
         from paper_2512_16391_b200.host_types import AnchorPlan, AnchorPlanCore, HeadMap, KBudgetPolicy
-        L, B, Hq, Hkv, n = 6, 2, 8, 4, 1200
+        L, B, Hq, Hkv, n = 7, 2, 8, 4, 1200
         G = Hq // Hkv
-        # reuse layers 3-5 run as one multi-layer launch over the gathered lists
-        plan = AnchorPlan(AnchorPlanCore([0, 2], 2, 0.0),
-                          head_maps={1: HeadMap(1, 0, [2, 0, 3, 1]), 3: HeadMap(3, 2, [3, 2, 1, 0]),
-                                     4: HeadMap(4, 2, [1, 1, 2, 2]), 5: HeadMap(5, 2, [0, 3, 0, 3])},
+        # anchors 2-3 run as one group (one all-gather of layer 3's lists);
+        # reuse layers 4-6 run as one multi-layer launch over the gathered lists
+        plan = AnchorPlan(AnchorPlanCore([0, 2, 3], 3, 0.0),
+                          head_maps={1: HeadMap(1, 0, [2, 0, 3, 1]), 4: HeadMap(4, 3, [3, 2, 1, 0]),
+                                     5: HeadMap(5, 3, [1, 1, 2, 2]), 6: HeadMap(6, 3, [0, 3, 0, 3])},
                           k_policy=KBudgetPolicy(0.1, 64))
         rng = np.random.default_rng(5)
         q = orc.bf16_round((rng.standard_normal((L, B, Hq, 128)) * 2).astype(np.float32))
