@@ -56,6 +56,7 @@ struct PoolTmaps {
 // dev instrumentation (variant builds only): clock64 stamps of one pass-B
 // CTA (the middle tile, kv head 0) per key block -- scripts/pb_trace.py
 __device__ long long g_pb_trace[512][8];
+__device__ long long g_pb_tail[4];     // CTA start, column sums done, fused Top-k done
 #define PB_TRACE(e, j)                                                                                       \
   do {                                                                                                       \
     if (blockIdx.y == 0 && (int)blockIdx.x == (int)gridDim.x / 2 && (j) < 512) g_pb_trace[(j)][(e)] = clock64(); \
@@ -63,9 +64,19 @@ __device__ long long g_pb_trace[512][8];
 extern "C" int kscd_debug_pb_trace(void* dst) {
   return (int)cudaMemcpyFromSymbol(dst, g_pb_trace, sizeof(g_pb_trace));
 }
+extern "C" int kscd_debug_pb_tail(void* dst) {
+  return (int)cudaMemcpyFromSymbol(dst, g_pb_tail, sizeof(g_pb_tail));
+}
+#define PB_TAIL(e)                                                                                 \
+  do {                                                                                             \
+    if (blockIdx.y == 0 && (int)blockIdx.x == (int)gridDim.x / 2) g_pb_tail[(e)] = clock64();     \
+  } while (0)
 #else
 #define PB_TRACE(e, j) \
   do {                 \
+  } while (0)
+#define PB_TAIL(e) \
+  do {             \
   } while (0)
 #endif
 
@@ -131,6 +142,7 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
   const int hbase = g * a.G + a.head_begin;
 
   if (threadIdx.x == 0) {
+    PB_TAIL(0);
     mbar_init(&bars[0], 1);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&bars[1 + s], 1);
@@ -255,7 +267,12 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
     // before the last column sums were read).  Out of line, so the select's
     // registers never compete with the column-sum loop's.
     asm volatile("bar.sync 1, 256;\n" ::: "memory");
+    if (threadIdx.x == 128) PB_TAIL(1);
     fused_select_tail(a, smem + kOffQ, t1, (int64_t)g * T + ti);
+#ifdef KSCD_PB_TRACE
+    asm volatile("bar.sync 1, 256;\n" ::: "memory");
+    if (threadIdx.x == 128) PB_TAIL(2);
+#endif
   }
   __syncthreads();
   if (warp == 0) {

@@ -40,6 +40,11 @@ def main():
     print("period per block:          ", q(per[mid]))
     print("quarter 0: wait for S^T    ", q(wait0[mid]), "  work", q(work0[mid]))
     print("quarter 2: wait for S^T    ", q(wait2[mid]), "  work", q(work2[mid]))
+    tb = (ctypes.c_longlong * 4)()
+    _lib.load().kscd_debug_pb_tail(ctypes.cast(tb, ctypes.c_void_p))
+    t0, t1, t2 = tb[0], tb[1], tb[2]
+    print(f"CTA: column sums {t1 - t0} clocks ({nb} blocks, {(t1 - t0) / nb:.0f} per block incl. prologue), "
+          f"fused Top-k tail {t2 - t1} clocks ({(t2 - t1) / max(t2 - t0, 1):.1%} of the CTA)")
 
 
 if __name__ == "__main__":
