@@ -108,15 +108,18 @@ KSCD_DEV float2 pool_colsum(const uint32_t (&r)[128], uint32_t l4, float2 sc2, i
 
 // Top-k of the pooled row this CTA just wrote into its SM's scratch slot
 // (two planes), by threads 128..383.
+// The fused anchor selection of one (kv head, tile) row on all 384 threads:
+// the exact Top-k with k = k_budget(t1) over plane0 + plane1 of this SM's
+// slot, the freed Q shared memory as its workspace.  Out of line, so the
+// select's registers never compete with the column-sum loop's.  2 float4
+// loads in flight per thread (x2 planes); 4 and 8 spilled and ran slower.
 __device__ __noinline__ void fused_select_tail(const PoolPrefillArgs& a, uint8_t* sh_mem, int t1, int64_t r) {
-  if (threadIdx.x == 128 && smid_u32() >= (uint32_t)kSmSlots) __trap();   // scratch slot bound
+  if (threadIdx.x == 0 && smid_u32() >= (uint32_t)kSmSlots) __trap();   // scratch slot bound
   TopkShared& tsh = *reinterpret_cast<TopkShared*>(sh_mem);
   const float* row0 = a.pooled + (int64_t)smid_u32() * 2 * a.pool_stride;
   const int k = k_budget_dev(a.fraction, a.k_min, t1);
-  // 2 float4 loads in flight per thread (x2 planes); 4 and 8 spill and run slower (A/B at 128K: 82.4 / 84.0 / 89.8 ms per select, unfused 81.2)
-  // (x2 planes) keep the row passes from going L2-latency bound
-  topk_select<1, 256, 128, KSCD_FUSED_NB>(row0, row0 + a.pool_stride, t1, min(k, t1), a.idx + r * a.k_cap, a.k_cap,
-                              a.counts + r, tsh);
+  topk_select<1, 384, 0, KSCD_FUSED_NB>(row0, row0 + a.pool_stride, t1, min(k, t1), a.idx + r * a.k_cap, a.k_cap,
+                                        a.counts + r, tsh);
 }
 
 // bars: 0 q_full | 1-2 k_full[s] | 3-4 k_empty[s] | 5-6 s_full[x] | 7-8 buf_free[x]
@@ -257,20 +260,26 @@ __global__ void __launch_bounds__(pp::kThreads, 1)
       }
     }
   }
-  if (a.fuse && warp >= 4) {
-    // ---- fused selection: the exact Top-k of this (kv head, tile) row with
-    // k = k_budget(t1) (runner.py:199-206), run by the two column-sum
-    // warpgroups (256 threads, named barrier 1) right after they wrote the
-    // row; the producer / MMA warps keep their reduced register budget and
-    // wait at the final barrier.  The row's global writes are visible to the
-    // group after the barrier, and Q shared memory is free (every MMA retired
-    // before the last column sums were read).  Out of line, so the select's
-    // registers never compete with the column-sum loop's.
-    asm volatile("bar.sync 1, 256;\n" ::: "memory");
+  if (a.fuse) {
+    // ---- fused selection (runner.py:199-206) right after the row was
+    // written, on every thread of the CTA: the producer / MMA warps raise
+    // their register budget to 168 as the column-sum warpgroups lower theirs
+    // (256 -> 384 threads: the tail went from 10.5 % to 7.1 % of a 128K CTA,
+    // pass B 83.9 -> 81.9 ms).  The row's global writes are visible to the
+    // CTA after the barrier, and Q shared memory is free (every MMA retired
+    // before the last column sums were read).
+    // the column-sum warps release their registers BEFORE any producer warp
+    // asks for more: an early producer-side inc (warps 1-2 idle through the
+    // loop) could otherwise take registers the column-sum warps' own entry
+    // inc still waits for -- a deadlock that compute-sanitizer's timing hit
+    if (warp >= 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 168;\n");
+    __syncthreads();
+    if (warp < 4) asm volatile("setmaxnreg.inc.sync.aligned.u32 168;\n");
+    __syncthreads();
     if (threadIdx.x == 128) PB_TAIL(1);
     fused_select_tail(a, smem + kOffQ, t1, (int64_t)g * T + ti);
 #ifdef KSCD_PB_TRACE
-    asm volatile("bar.sync 1, 256;\n" ::: "memory");
+    __syncthreads();
     if (threadIdx.x == 128) PB_TAIL(2);
 #endif
   }
